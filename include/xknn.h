@@ -1,0 +1,159 @@
+/*
+ * xknn.h -- C ABI of the B200-native (sm_100a) model-parallel KNN-softmax layer.
+ *
+ * Drop-in boundary for the reference's fc hot path (namespace xcls, /root/reference/proj):
+ * one layer object per GPU owns that GPU's contiguous class shard (ShardLayout,
+ * knn_graph.cpp:94-115), its weight rows, momentum velocity and compressed KNN graph, and runs
+ * the fc half of HybridSim::train_step (parallel.cpp:455-572, :638-668) on device: active-class
+ * selection -> active-row gather/normalize -> logit GEMM + distributed softmax-CE -> feature- and
+ * weight-gradient GEMMs -> sparse momentum-SGD row update.  Collectives are NCCL over
+ * NVLink/NVSwitch on a caller-provided communicator.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "_dev" pointers are device memory of the layer's GPU,
+ *    "_host" pointers host memory.  Row-major fp32 matrices, u32 class ids, u64 offsets.
+ *  - Every call is ordered on the layer's CUDA stream.  Calls that return host values
+ *    (counts, loss) synchronize that stream; the rest are asynchronous.
+ *  - Errors are the xcls::Error classes of errors.hpp:10-54, one code each, checked before
+ *    state changes as the reference does.  xknn_last_error_row() carries ZeroNormRow::row.
+ *  - Thread-safety: a layer is single-owner (like HybridSim); distinct layers are independent.
+ */
+#ifndef XKNN_H_
+#define XKNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:10-54 -> status codes */
+typedef enum {
+  XKNN_OK = 0,
+  XKNN_ERR_SHAPE_MISMATCH = 1,     /* ShapeMismatch   */
+  XKNN_ERR_ZERO_NORM_ROW = 2,      /* ZeroNormRow     */
+  XKNN_ERR_LABEL_OUT_OF_RANGE = 3, /* LabelOutOfRange */
+  XKNN_ERR_K_TOO_LARGE = 4,        /* KTooLarge       */
+  XKNN_ERR_EMPTY_SHARD = 5,        /* EmptyShard      */
+  XKNN_ERR_M_TOO_SMALL = 6,        /* MTooSmall       */
+  XKNN_ERR_LABEL_NOT_ACTIVE = 7,   /* LabelNotActive  */
+  XKNN_ERR_INVALID_ARGUMENT = 8,   /* InvalidArgument */
+  XKNN_ERR_IO = 9,                 /* IoError         */
+  XKNN_ERR_CONFIG = 10,            /* ConfigError     */
+  XKNN_ERR_CUDA = 20,
+  XKNN_ERR_NCCL = 21,
+  XKNN_ERR_OUT_OF_MEMORY = 22,
+  XKNN_ERR_UNSUPPORTED = 23
+} xknn_status_t;
+
+/* Arithmetic of the three fc GEMMs.  Selection, indices and the update are identical in both. */
+typedef enum {
+  /* tcgen05/TMEM tensor cores, bf16 operands, fp32 accumulation (the performance path) */
+  XKNN_PREC_BF16 = 0,
+  /* CUDA-core fp32 with the reference's summation order (matrix.cpp:57-98), logits
+     materialized; the parity path, 1e-5 relative to the reference */
+  XKNN_PREC_FP32_EXACT = 1
+} xknn_precision_t;
+
+typedef struct {
+  float scale;           /* SimOptions::scale (parallel.hpp:140), cosine logit scale s      */
+  float momentum;        /* SimOptions::momentum (parallel.hpp:141)                          */
+  float weight_decay;    /* SimOptions::weight_decay (parallel.hpp:142)                      */
+  uint64_t m_active;     /* SelectionConfig::m_active (knn_softmax.hpp:27), global M         */
+  uint64_t rng_seed;     /* SelectionConfig::rng_seed (knn_softmax.hpp:28)                   */
+  uint64_t max_batch;    /* largest global batch B a step will see (sizes scratch)           */
+  int32_t precision;     /* xknn_precision_t                                                 */
+  int32_t reserved;
+} xknn_config_t;
+
+typedef struct xknn_layer xknn_layer_t;
+
+/* Status of the last failing call on this thread, human readable. */
+const char* xknn_status_string(xknn_status_t s);
+const char* xknn_last_error_message(void);
+/* ZeroNormRow::row of the last XKNN_ERR_ZERO_NORM_ROW (errors.hpp:18-22). */
+uint64_t xknn_last_error_row(void);
+
+/* ShardLayout::class_range (knn_graph.cpp:102-115), host-only, no GPU needed. */
+xknn_status_t xknn_shard_range(uint64_t num_classes, uint64_t num_shards, uint64_t shard,
+                               uint64_t* begin, uint64_t* end);
+
+/* NCCL bootstrap helpers (plumbing for callers without nccl.h, e.g. ctypes/cgo):
+   rank 0 calls xknn_nccl_unique_id, the caller broadcasts the 128 bytes, every rank calls
+   xknn_nccl_comm_init on its device.  The returned handle is an ncclComm_t. */
+xknn_status_t xknn_nccl_unique_id(uint8_t out_id[128]);
+xknn_status_t xknn_nccl_comm_init(const uint8_t id[128], int world, int rank, void** comm);
+xknn_status_t xknn_nccl_comm_destroy(void* comm);
+
+/* HybridSim ctor (parallel.cpp:351-379) restricted to the fc shard of `rank`.
+   comm: ncclComm_t over `world` ranks (NULL iff world == 1).  stream: cudaStream_t (NULL =
+   the legacy default stream).  The velocity starts at zero (SgdMomentum::ensure_state,
+   fccs.cpp:58-62).  The weights must be set before the first step. */
+xknn_status_t xknn_layer_create(int rank, int world, uint64_t num_classes, uint64_t dim,
+                                const xknn_config_t* cfg, void* comm, void* stream,
+                                xknn_layer_t** out);
+xknn_status_t xknn_layer_destroy(xknn_layer_t* h);
+xknn_status_t xknn_layer_shard(const xknn_layer_t* h, uint64_t* begin, uint64_t* end);
+xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg);
+
+/* Weights of this shard, (end-begin) x dim fp32 row-major.  HybridSim::load_model /
+   fc_weights (parallel.cpp:401-409, :425-431).  on_device selects the pointer space. */
+xknn_status_t xknn_layer_set_weights(xknn_layer_t* h, const float* w, int on_device);
+xknn_status_t xknn_layer_get_weights(xknn_layer_t* h, float* w, int on_device);
+xknn_status_t xknn_layer_get_velocity(xknn_layer_t* h, float* v, int on_device);
+/* Device pointer to the resident weight shard (for callers that initialise in place). */
+xknn_status_t xknn_layer_weights_ptr(xknn_layer_t* h, float** w_dev);
+
+/* HybridSim::set_shard_graphs (parallel.cpp:381-388): this shard's CompressedKnnGraph
+   (knn_graph.hpp:46-55): k_per_class[num_classes], offsets[num_classes], flat[flat_len]. */
+xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* k_per_class,
+                                       const uint64_t* offsets, const uint32_t* flat,
+                                       uint64_t flat_len, int on_device);
+
+/* select_active_classes(span<CompressedKnnGraph>, ...) (knn_softmax.cpp:117-134 +
+   finish_selection :17-81) for the global batch `labels_dev` (B u32, identical on every
+   rank), executed shard-parallel.  Writes this shard's slice of the ActiveSet (sorted global
+   class ids; the rank-order concatenation over ranks is ActiveSet::class_indices) to
+   out_active_dev (capacity >= min(shard size, m_active)) and its length to *count_host;
+   *contains_all_host = ActiveSet::contains_all_labels restricted to labels this shard owns.
+   Synchronizes. */
+xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t batch,
+                          uint32_t* out_active_dev, uint64_t* count_host,
+                          int* contains_all_host);
+
+/* One synchronous step of the fc half of HybridSim::train_step in SoftmaxMode::kKnn with one
+   micro-batch (parallel.cpp:455-572, :638-668):
+     features_local_dev : this rank's B/P rows of extracted features (fp32, dim wide), in the
+                          reference's rank-major slicing (parallel.cpp:447-453)
+     labels_local_dev   : the matching B/P labels (u32, global class ids)
+   The layer all-gathers features and labels, selects the active classes, computes the
+   distributed softmax cross-entropy, updates its active weight rows with momentum SGD at
+   learning rate lr, and writes d loss / d features for its own B/P rows (through the row
+   normalization, the tensor handed to mlp_backward at parallel.cpp:585-586) to
+   grad_features_local_dev (may be NULL).  loss_dev (device double, may be NULL) receives the
+   mean loss, identical on all ranks.  Asynchronous: use xknn_layer_sync to collect errors. */
+xknn_status_t xknn_step(xknn_layer_t* h, const float* features_local_dev,
+                        const uint32_t* labels_local_dev, uint64_t batch_local, float lr,
+                        double* loss_dev, float* grad_features_local_dev);
+
+/* Synchronizes the layer stream, returns the first device-side error of the preceding
+   asynchronous calls (label range, ZeroNormRow, MTooSmall, ...) and clears it. */
+xknn_status_t xknn_layer_sync(xknn_layer_t* h);
+
+/* Diagnostics of the last step (host values, synchronizes): |ActiveSet| (global), this
+   shard's active row count. */
+xknn_status_t xknn_layer_last_active(xknn_layer_t* h, uint64_t* active_global,
+                                     uint64_t* active_local);
+
+/* Copies the last step's logits (B x active_local, fp32) -- FP32_EXACT precision only; for
+   parity tests of the logit GEMM (matmul(f_hat, w_sub, T) * scale, parallel.cpp:550-551). */
+xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out_host, uint64_t capacity);
+
+/* Kernel launch counter (all kernels this library launched on this layer since creation). */
+uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XKNN_H_ */

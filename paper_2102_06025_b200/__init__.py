@@ -1,0 +1,289 @@
+"""B200-native (sm_100a) model-parallel KNN-softmax layer -- Python host binding.
+
+Mirrors the reference's C++ layer API (namespace ``xcls``, /root/reference/proj/include/xcls)
+for the fc hot path over the C ABI in ``include/xknn.h`` (``libxknn.so``, built in-tree by
+``make -C paper_2102_06025_b200``).  PyTorch is used only for device memory and streams.
+
+There is no CPU fallback: importing this package without the built CUDA library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libxknn.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA library with `make -C {_HERE}` "
+        "(there is no CPU fallback)")
+
+import torch as _torch  # noqa: F401  (plumbing; loads the NCCL build torch was linked against first)
+
+_lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+U64 = C.c_uint64
+VP = C.c_void_p
+
+PREC_BF16 = 0
+PREC_FP32_EXACT = 1
+
+
+class XknnConfig(C.Structure):
+    """xknn_config_t (include/xknn.h) == SimOptions + SelectionConfig of the reference."""
+    _fields_ = [("scale", C.c_float), ("momentum", C.c_float), ("weight_decay", C.c_float),
+                ("m_active", U64), ("rng_seed", U64), ("max_batch", U64),
+                ("precision", C.c_int32), ("reserved", C.c_int32)]
+
+
+# ---- errors.hpp:10-54 -------------------------------------------------------------------------
+class Error(RuntimeError):
+    code = -1
+
+
+class ShapeMismatch(Error): code = 1
+class ZeroNormRow(Error):
+    code = 2
+
+    def __init__(self, msg, row=0):
+        super().__init__(msg)
+        self.row = row
+class LabelOutOfRange(Error): code = 3
+class KTooLarge(Error): code = 4
+class EmptyShard(Error): code = 5
+class MTooSmall(Error): code = 6
+class LabelNotActive(Error): code = 7
+class InvalidArgument(Error): code = 8
+class IoError(Error): code = 9
+class ConfigError(Error): code = 10
+class CudaError(Error): code = 20
+class NcclError(Error): code = 21
+class OutOfMemory(Error): code = 22
+class Unsupported(Error): code = 23
+
+
+_ERRS = {c.code: c for c in (ShapeMismatch, ZeroNormRow, LabelOutOfRange, KTooLarge, EmptyShard,
+                             MTooSmall, LabelNotActive, InvalidArgument, IoError, ConfigError,
+                             CudaError, NcclError, OutOfMemory, Unsupported)}
+
+_lib.xknn_last_error_message.restype = C.c_char_p
+_lib.xknn_last_error_row.restype = U64
+_lib.xknn_layer_kernel_launches.restype = U64
+_lib.xknn_layer_kernel_launches.argtypes = [VP]
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    cls = _ERRS.get(rc, Error)
+    msg = _lib.xknn_last_error_message().decode()
+    if cls is ZeroNormRow:
+        raise ZeroNormRow(msg, int(_lib.xknn_last_error_row()))
+    raise cls(msg)
+
+
+for _name, _args in {
+    "xknn_shard_range": [U64, U64, U64, C.POINTER(U64), C.POINTER(U64)],
+    "xknn_nccl_unique_id": [C.c_char_p],
+    "xknn_nccl_comm_init": [C.c_char_p, C.c_int, C.c_int, C.POINTER(VP)],
+    "xknn_nccl_comm_destroy": [VP],
+    "xknn_layer_create": [C.c_int, C.c_int, U64, U64, C.POINTER(XknnConfig), VP, VP, C.POINTER(VP)],
+    "xknn_layer_destroy": [VP],
+    "xknn_layer_shard": [VP, C.POINTER(U64), C.POINTER(U64)],
+    "xknn_layer_set_config": [VP, C.POINTER(XknnConfig)],
+    "xknn_layer_set_weights": [VP, VP, C.c_int],
+    "xknn_layer_get_weights": [VP, VP, C.c_int],
+    "xknn_layer_get_velocity": [VP, VP, C.c_int],
+    "xknn_layer_weights_ptr": [VP, C.POINTER(VP)],
+    "xknn_layer_set_graph_csr": [VP, VP, VP, VP, U64, C.c_int],
+    "xknn_select": [VP, VP, U64, VP, C.POINTER(U64), C.POINTER(C.c_int)],
+    "xknn_step": [VP, VP, VP, U64, C.c_float, VP, VP],
+    "xknn_layer_sync": [VP],
+    "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
+    "xknn_layer_last_logits": [VP, VP, U64],
+}.items():
+    getattr(_lib, _name).argtypes = _args
+    getattr(_lib, _name).restype = C.c_int
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+# ---- ShardLayout (knn_graph.hpp:30-41) -------------------------------------------------------
+class ShardLayout:
+    def __init__(self, num_classes: int, num_shards: int = 1):
+        self.num_classes = num_classes
+        self.num_shards = num_shards
+
+    def class_range(self, shard: int) -> tuple[int, int]:
+        b, e = U64(), U64()
+        _check(_lib.xknn_shard_range(self.num_classes, self.num_shards, shard, C.byref(b),
+                                     C.byref(e)))
+        return b.value, e.value
+
+    def shard_size(self, shard: int) -> int:
+        b, e = self.class_range(shard)
+        return e - b
+
+    def shard_of(self, cls: int) -> int:
+        base, rem = divmod(self.num_classes, self.num_shards)
+        big = rem * (base + 1)
+        return cls // (base + 1) if cls < big else rem + (cls - big) // base
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.xknn_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, world: int, rank: int) -> int:
+    comm = VP()
+    _check(_lib.xknn_nccl_comm_init(uid, world, rank, C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm) -> None:
+    _check(_lib.xknn_nccl_comm_destroy(comm))
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+class KnnSoftmaxLayer:
+    """One GPU's shard of the model-parallel KNN-softmax fc layer.
+
+    The composite HybridSim fc half (parallel.cpp:433-677) restricted to one worker: owns the
+    weight shard, the SgdMomentum velocity and the shard's CompressedKnnGraph on device.
+    All tensor arguments are torch CUDA tensors on this layer's device.
+    """
+
+    def __init__(self, num_classes: int, dim: int, *, rank: int = 0, world: int = 1,
+                 m_active: int, max_batch: int, scale: float = 30.0, momentum: float = 0.9,
+                 weight_decay: float = 0.0, rng_seed: int = 0, precision: int = PREC_BF16,
+                 comm=None, stream=None):
+        import torch  # plumbing only: device memory and streams
+
+        self._torch = torch
+        self.num_classes, self.dim, self.rank, self.world = num_classes, dim, rank, world
+        self.cfg = XknnConfig(scale, momentum, weight_decay, m_active, rng_seed, max_batch,
+                              precision, 0)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = VP()
+        _check(_lib.xknn_layer_create(rank, world, num_classes, dim, C.byref(self.cfg),
+                                      comm, self.stream.cuda_stream, C.byref(h)))
+        self.h = h.value
+        b, e = U64(), U64()
+        _check(_lib.xknn_layer_shard(self.h, C.byref(b), C.byref(e)))
+        self.begin, self.end = b.value, e.value
+        self._loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    # -- state ----------------------------------------------------------------------------------
+    @property
+    def shard_rows(self) -> int:
+        return self.end - self.begin
+
+    def set_weights(self, w) -> None:
+        """HybridSim::load_model for this shard: w is (shard_rows, dim) fp32."""
+        assert w.shape == (self.shard_rows, self.dim) and w.dtype == self._torch.float32
+        w = w.contiguous()
+        _check(_lib.xknn_layer_set_weights(self.h, w.data_ptr(), int(w.is_cuda)))
+
+    def weights(self):
+        out = self._torch.empty(self.shard_rows, self.dim, dtype=self._torch.float32,
+                                device="cuda")
+        _check(_lib.xknn_layer_get_weights(self.h, out.data_ptr(), 1))
+        return out
+
+    def velocity(self):
+        out = self._torch.empty(self.shard_rows, self.dim, dtype=self._torch.float32,
+                                device="cuda")
+        _check(_lib.xknn_layer_get_velocity(self.h, out.data_ptr(), 1))
+        return out
+
+    def weights_view(self):
+        """The resident weight shard as a torch tensor aliasing device memory (in-place init)."""
+        p = VP()
+        _check(_lib.xknn_layer_weights_ptr(self.h, C.byref(p)))
+        return _DeviceView(p.value, (self.shard_rows, self.dim), self._torch)
+
+    def set_shard_graph(self, k_per_class, offsets, flat) -> None:
+        """HybridSim::set_shard_graphs for this shard (knn_graph.hpp:46-55 arrays)."""
+        dev = int(k_per_class.is_cuda)
+        kpc = k_per_class.contiguous()
+        off = offsets.contiguous()
+        fl = flat.contiguous()
+        _check(_lib.xknn_layer_set_graph_csr(self.h, kpc.data_ptr(), off.data_ptr(),
+                                             fl.data_ptr() if fl.numel() else 0, fl.numel(), dev))
+
+    # -- hot path ------------------------------------------------------------------------------
+    def select_active_classes(self, labels):
+        """This shard's slice of select_active_classes(span<CompressedKnnGraph>, ...)."""
+        torch = self._torch
+        cap = min(self.shard_rows, int(self.cfg.m_active)) + 32
+        out = torch.empty(cap, dtype=torch.int32, device="cuda")
+        cnt = U64()
+        ca = C.c_int()
+        lab = labels.to(torch.int32).contiguous()
+        _check(_lib.xknn_select(self.h, lab.data_ptr(), lab.numel(), out.data_ptr(), C.byref(cnt),
+                                C.byref(ca)))
+        return out[: cnt.value].clone(), bool(ca.value)
+
+    def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
+                   loss_out=None, sync: bool = True):
+        """The fc half of HybridSim::train_step (kKnn, one micro-batch) for this rank's rows.
+        Returns the mean loss (float) when sync, else None (loss in loss_out/self._loss)."""
+        torch = self._torch
+        assert features_local.dtype == torch.float32 and features_local.is_contiguous()
+        lab = labels_local if labels_local.dtype == torch.int32 else labels_local.to(torch.int32)
+        loss = self._loss if loss_out is None else loss_out
+        _check(_lib.xknn_step(self.h, features_local.data_ptr(), lab.data_ptr(),
+                              features_local.shape[0], float(lr), loss.data_ptr(),
+                              _ptr(grad_features_local)))
+        if sync:
+            _check(_lib.xknn_layer_sync(self.h))
+            return float(loss.item())
+        return None
+
+    def sync(self) -> None:
+        _check(_lib.xknn_layer_sync(self.h))
+
+    def last_active(self) -> tuple[int, int]:
+        t, l = U64(), U64()
+        _check(_lib.xknn_layer_last_active(self.h, C.byref(t), C.byref(l)))
+        return t.value, l.value
+
+    def last_logits(self, batch: int):
+        import numpy as np
+
+        _, loc = self.last_active()
+        out = np.zeros((batch, loc), np.float32)
+        _check(_lib.xknn_layer_last_logits(self.h, out.ctypes.data, out.size))
+        return out
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.xknn_layer_kernel_launches(self.h))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.xknn_layer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _DeviceView:
+    """Minimal __cuda_array_interface__ wrapper so torch.as_tensor can alias library memory."""
+
+    def __init__(self, ptr, shape, torch):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": "<f4",
+                                         "version": 2}
+        self.tensor = torch.as_tensor(self, device="cuda")

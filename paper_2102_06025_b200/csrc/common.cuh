@@ -1,0 +1,49 @@
+// common.cuh -- shared helpers for the xknn sm_100a kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "xknn.h"
+
+#define XKNN_FULL_MASK 0xffffffffu
+
+namespace xknn {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kNumSMs = 148;
+
+// Device-side error word (first error wins): code in the low 8 bits, row in the high bits.
+struct DevError {
+  unsigned long long word;  // 0 = no error
+};
+
+__device__ __forceinline__ void raise_error(unsigned long long* err, int code, uint64_t row = 0) {
+  unsigned long long w = (unsigned long long)code | ((unsigned long long)row << 8);
+  atomicCAS(err, 0ull, w);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(XKNN_FULL_MASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* v, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (v[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
+  uint64_t g = (n + block - 1) / block;
+  if (g == 0) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace xknn

@@ -1,0 +1,40 @@
+// kernels.cuh -- host launchers of the device kernels (all asynchronous on `s`).
+#pragma once
+#include "layer.cuh"
+
+namespace xknn {
+
+// rowops.cu
+cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
+                                  const uint32_t* row_ids, const unsigned int* count,
+                                  uint64_t id_base, float* out32, __nv_bfloat16* out16,
+                                  float* norms, unsigned long long* err, cudaStream_t s);
+cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
+                               const unsigned int* count, uint64_t max_rows, uint64_t begin,
+                               uint32_t d, const float* wnorm, float lr, float mu, float wd,
+                               const unsigned long long* err, cudaStream_t s);
+cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
+                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s);
+
+// exact.cu
+cudaError_t launch_logits_exact(const float* xhat, const float* wsub, uint64_t rows,
+                                const unsigned int* cols, uint64_t max_cols, uint32_t d,
+                                float scale, float* out, cudaStream_t s);
+cudaError_t launch_dw_exact(const float* G, const float* xhat, uint64_t rows,
+                            const unsigned int* cols, uint64_t max_cols, uint32_t d, float sw,
+                            float* out, cudaStream_t s);
+cudaError_t launch_dx_exact(const float* G, const float* wsub, uint64_t rows,
+                            const unsigned int* cols, uint32_t d, float scale, float* out,
+                            cudaStream_t s);
+cudaError_t launch_rowmax(const float* L, uint64_t rows, const unsigned int* cols, float* rowmax,
+                          cudaStream_t s);
+cudaError_t launch_rowsum(const float* L, uint64_t rows, const unsigned int* cols,
+                          const float* rowmax, const int32_t* label_col, double* red,
+                          cudaStream_t s);
+cudaError_t launch_loss(const double* red, uint64_t rows, double* loss, SelState* st,
+                        unsigned long long* err, cudaStream_t s);
+cudaError_t launch_softmax_grad(float* L, uint64_t rows, const unsigned int* cols,
+                                uint64_t max_cols, const float* rowmax, const double* red,
+                                const int32_t* label_col, cudaStream_t s);
+
+}  // namespace xknn

@@ -1,0 +1,551 @@
+// layer.cu -- the xknn C ABI (include/xknn.h) and the per-step orchestration.
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace xknn {
+
+static thread_local std::string g_msg;
+static thread_local uint64_t g_row = 0;
+
+static xknn_status_t fail(xknn_status_t s, const std::string& msg) {
+  g_msg = msg;
+  return s;
+}
+
+xknn_status_t Layer::cuda_ok(cudaError_t e) {
+  if (e == cudaSuccess) return XKNN_OK;
+  if (e == cudaErrorMemoryAllocation)
+    return fail(XKNN_ERR_OUT_OF_MEMORY, std::string("cuda: ") + cudaGetErrorString(e));
+  return fail(XKNN_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e));
+}
+
+xknn_status_t Layer::nccl_ok(ncclResult_t r) {
+  if (r == ncclSuccess) return XKNN_OK;
+  return fail(XKNN_ERR_NCCL, std::string("nccl: ") + ncclGetErrorString(r));
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, uint64_t count) {
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
+                          const xknn_config_t* cfg_, void* comm_, void* stream_) {
+  rank = rank_;
+  world = world_;
+  n = n_;
+  d = d_;
+  cfg = *cfg_;
+  comm = static_cast<ncclComm_t>(comm_);
+  stream = static_cast<cudaStream_t>(stream_);
+  XK_CUDA(cudaGetDevice(&device));
+  const uint64_t base = n / world, rem = n % world;  // ShardLayout::class_range
+  if ((uint64_t)rank < rem) {
+    begin = rank * (base + 1);
+    end = begin + base + 1;
+  } else {
+    begin = rem * (base + 1) + (rank - rem) * base;
+    end = begin + base;
+  }
+  nw = end - begin;
+  nwords = (nw + 31) / 32;
+  bmax = cfg.max_batch;
+  mw_cap = std::min<uint64_t>(nw, cfg.m_active);
+
+  XK_CUDA(dalloc(&W, nw * d));
+  XK_CUDA(dalloc(&V, nw * d));
+  XK_CUDA(cudaMemsetAsync(V, 0, nw * d * sizeof(float), stream));
+  XK_CUDA(dalloc(&sel_best, nw));
+  XK_CUDA(dalloc(&sel_occ, nw));
+  XK_CUDA(cudaMemsetAsync(sel_best, 0xff, nw * sizeof(uint32_t), stream));
+  XK_CUDA(cudaMemsetAsync(sel_occ, 0, nw * sizeof(uint32_t), stream));
+  XK_CUDA(dalloc(&pool_bits, nwords));
+  XK_CUDA(dalloc(&act_bits, nwords));
+  XK_CUDA(dalloc(&lab_bits, nwords));
+  XK_CUDA(dalloc(&pool_list, nw));
+  XK_CUDA(dalloc(&active, mw_cap + 32));
+  const uint64_t nblocks = (nwords + 255) / 256;
+  XK_CUDA(dalloc(&blk_counts, 2 * (nblocks + 2)));
+  XK_CUDA(cudaMemsetAsync(blk_counts, 0, 2 * (nblocks + 2) * sizeof(uint32_t), stream));
+  const uint64_t m = cfg.m_active;
+  XK_CUDA(dalloc(&pick_key, m));
+  XK_CUDA(dalloc(&pick_val, m));
+  XK_CUDA(dalloc(&pick_key_s, m));
+  XK_CUDA(dalloc(&pick_val_s, m));
+  XK_CUDA(dalloc(&pred, m));
+  XK_CUDA(dalloc(&lw, m));
+  XK_CUDA(dalloc(&labels_all, bmax));
+  XK_CUDA(dalloc(&labels_sorted, bmax));
+  XK_CUDA(dalloc(&labels_distinct, bmax));
+  XK_CUDA(dalloc(&n_distinct, 1));
+  XK_CUDA(dalloc(&label_col, bmax));
+  XK_CUDA(dalloc(&pool_counts, world));
+  XK_CUDA(dalloc(&tie_counts, world));
+  XK_CUDA(dalloc(&st, 1));
+  XK_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), stream));
+  XK_CUDA(dalloc(&err, 1));
+  XK_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned long long), stream));
+  XK_CUDA(dalloc(&loss_dev, 1));
+
+  // cub temp: max over the sorts/scans/selects we run
+  size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, labels_all, labels_sorted, (int)bmax, 0, 32, stream);
+  cub::DeviceSelect::Unique(nullptr, b2, labels_sorted, labels_distinct, n_distinct, (int)bmax,
+                            stream);
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, blk_counts, blk_counts, (int)(nblocks + 1), stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, b4, pick_key, pick_key_s, pick_val, pick_val_s,
+                                  (int)std::max<uint64_t>(m, 1), 0, 32, stream);
+  cub_tmp_bytes = std::max(std::max(b1, b2), std::max(b3, b4)) + 256;
+  XK_CUDA(cudaMalloc(&cub_tmp, cub_tmp_bytes));
+
+  // step scratch
+  XK_CUDA(dalloc(&X, bmax * d));
+  XK_CUDA(dalloc(&xnorm, bmax));
+  XK_CUDA(dalloc(&wnorm, mw_cap));
+  XK_CUDA(dalloc(&rowmax, bmax));
+  XK_CUDA(dalloc(&rowred, 3 * bmax));
+  XK_CUDA(dalloc(&dW, mw_cap * d));
+  XK_CUDA(dalloc(&dX, bmax * d));
+  if (cfg.precision == XKNN_PREC_FP32_EXACT) {
+    XK_CUDA(dalloc(&Xhat, bmax * d));
+    XK_CUDA(dalloc(&Wsub, mw_cap * d));
+    XK_CUDA(dalloc(&logits, bmax * mw_cap * 2));  // logits, then G
+    XK_CUDA(dalloc(&dXpart, bmax * d));
+  } else {
+    XK_TRY(init_fast());
+  }
+  XK_CUDA(cudaStreamSynchronize(stream));
+  return XKNN_OK;
+}
+
+void Layer::free_all() {
+  void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, act_bits, lab_bits,
+                  pool_list, active, blk_counts, mt_cache, pick_key, pick_val, pick_key_s,
+                  pick_val_s, pred, lw, labels_all, labels_sorted, labels_distinct, n_distinct,
+                  label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
+                  Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
+                  dXpart, loss_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  free_fast();
+}
+
+// The padding draw's raw stream: std::mt19937_64(rng_seed), re-seeded by the reference on every
+// select_active_classes call (knn_softmax.cpp:43) -- generated here with the same libstdc++
+// engine, once per (seed, M).
+xknn_status_t Layer::ensure_mt_cache() {
+  const uint64_t want = cfg.m_active + 64;
+  if (mt_cache && mt_len == want && mt_seed == cfg.rng_seed) return XKNN_OK;
+  if (mt_cache) cudaFree(mt_cache);
+  mt_cache = nullptr;
+  std::vector<uint64_t> h(want);
+  std::mt19937_64 g(cfg.rng_seed);
+  for (auto& v : h) v = g();
+  XK_CUDA(dalloc(&mt_cache, want));
+  XK_CUDA(cudaMemcpyAsync(mt_cache, h.data(), want * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                          stream));
+  XK_CUDA(cudaStreamSynchronize(stream));
+  mt_len = want;
+  mt_seed = cfg.rng_seed;
+  return XKNN_OK;
+}
+
+xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_local,
+                              uint64_t bl, float lr, double* loss_out, float* gfeat_local) {
+  const uint64_t B = bl * world;
+  const uint32_t D = (uint32_t)d;
+  last_b = B;
+  // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544)
+  if (world > 1) {
+    XK_NCCL(ncclGroupStart());
+    XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm, stream));
+    XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
+    XK_NCCL(ncclGroupEnd());
+  } else {
+    XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                            stream));
+  }
+  // (1) Algorithm 1 selection -> this shard's sorted active rows
+  XK_TRY(run_selection(B));
+  unsigned int* cnt = &st->active_count;
+  // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
+  // whole shard as parallel.cpp:490-492 does -- row-wise identical)
+  if (cfg.precision == XKNN_PREC_FP32_EXACT) {
+    XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, Xhat, nullptr, xnorm, err, stream));
+    ++launches;
+    XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, cnt, begin, Wsub, nullptr, wnorm, err,
+                                  stream));
+    ++launches;
+    float* L = logits;
+    float* G = logits + bmax * mw_cap;
+    // (3) logits
+    XK_CUDA(launch_logits_exact(Xhat, Wsub, B, cnt, mw_cap, D, cfg.scale, L, stream));
+    ++launches;
+    // (4) distributed softmax-CE: global row max, then [exp-sum, label term, owner] sums
+    XK_CUDA(launch_rowmax(L, B, cnt, rowmax, stream));
+    ++launches;
+    if (world > 1) XK_NCCL(ncclAllReduce(rowmax, rowmax, B, ncclFloat, ncclMax, comm, stream));
+    XK_CUDA(launch_rowsum(L, B, cnt, rowmax, label_col, rowred, stream));
+    ++launches;
+    if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
+    XK_CUDA(launch_loss(rowred, B, loss_dev, st, err, stream));
+    ++launches;
+    XK_CUDA(cudaMemcpyAsync(G, L, B * mw_cap * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    XK_CUDA(launch_softmax_grad(G, B, cnt, mw_cap, rowmax, rowred, label_col, stream));
+    ++launches;
+    // (5) weight side and feature side
+    XK_CUDA(launch_dw_exact(G, Xhat, B, cnt, mw_cap, D, cfg.scale * 1.0f, dW, stream));
+    ++launches;
+    XK_CUDA(launch_dx_exact(G, Wsub, B, cnt, D, cfg.scale, dXpart, stream));
+    ++launches;
+    if (world > 1)
+      XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
+    else
+      XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  } else {
+    XK_TRY(run_fast_core(B));
+  }
+  // (6) feature normalize-backward on this rank's rows (parallel.cpp:574-585)
+  if (gfeat_local) {
+    XK_CUDA(launch_feature_backward(X + (uint64_t)rank * bl * d, xnorm + (uint64_t)rank * bl, dX,
+                                    bl, D, gfeat_local, stream));
+    ++launches;
+  }
+  // (8) normalize-backward + momentum SGD on the active rows only (parallel.cpp:649-667)
+  XK_CUDA(launch_update_rows(W, V, dW, active, cnt, mw_cap, begin, D, wnorm, lr, cfg.momentum,
+                             cfg.weight_decay, err, stream));
+  ++launches;
+  if (loss_out)
+    XK_CUDA(cudaMemcpyAsync(loss_out, loss_dev, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  return XKNN_OK;
+}
+
+}  // namespace xknn
+
+using xknn::Layer;
+using xknn::fail;
+
+struct xknn_layer {
+  Layer L;
+};
+
+#define GUARD_H(h) \
+  if (!(h)) return fail(XKNN_ERR_INVALID_ARGUMENT, "null layer handle")
+
+extern "C" {
+
+const char* xknn_status_string(xknn_status_t s) {
+  switch (s) {
+    case XKNN_OK: return "ok";
+    case XKNN_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case XKNN_ERR_ZERO_NORM_ROW: return "ZeroNormRow";
+    case XKNN_ERR_LABEL_OUT_OF_RANGE: return "LabelOutOfRange";
+    case XKNN_ERR_K_TOO_LARGE: return "KTooLarge";
+    case XKNN_ERR_EMPTY_SHARD: return "EmptyShard";
+    case XKNN_ERR_M_TOO_SMALL: return "MTooSmall";
+    case XKNN_ERR_LABEL_NOT_ACTIVE: return "LabelNotActive";
+    case XKNN_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case XKNN_ERR_IO: return "IoError";
+    case XKNN_ERR_CONFIG: return "ConfigError";
+    case XKNN_ERR_CUDA: return "CudaError";
+    case XKNN_ERR_NCCL: return "NcclError";
+    case XKNN_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    case XKNN_ERR_UNSUPPORTED: return "Unsupported";
+  }
+  return "unknown";
+}
+
+const char* xknn_last_error_message(void) { return xknn::g_msg.c_str(); }
+uint64_t xknn_last_error_row(void) { return xknn::g_row; }
+
+xknn_status_t xknn_shard_range(uint64_t n, uint64_t p, uint64_t s, uint64_t* b, uint64_t* e) {
+  if (p == 0 || s >= p) return fail(XKNN_ERR_INVALID_ARGUMENT, "ShardLayout: shard index out of range");
+  const uint64_t base = n / p, rem = n % p;
+  if (s < rem) {
+    *b = s * (base + 1);
+    *e = *b + base + 1;
+  } else {
+    *b = rem * (base + 1) + (s - rem) * base;
+    *e = *b + base;
+  }
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_nccl_unique_id(uint8_t out_id[128]) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(XKNN_ERR_NCCL, ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out_id, &id, 128);
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_nccl_comm_init(const uint8_t id[128], int world, int rank, void** comm) {
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t c;
+  ncclResult_t r = ncclCommInitRank(&c, world, uid, rank);
+  if (r != ncclSuccess) return fail(XKNN_ERR_NCCL, ncclGetErrorString(r));
+  *comm = c;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_nccl_comm_destroy(void* comm) {
+  if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_create(int rank, int world, uint64_t n, uint64_t d,
+                                const xknn_config_t* cfg, void* comm, void* stream,
+                                xknn_layer_t** out) {
+  if (!cfg || !out) return fail(XKNN_ERR_INVALID_ARGUMENT, "null argument");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(XKNN_ERR_INVALID_ARGUMENT, "HybridSim: need >= 1 worker and 0 <= rank < world");
+  if (world > 1 && !comm) return fail(XKNN_ERR_INVALID_ARGUMENT, "world > 1 needs an NCCL comm");
+  if ((uint64_t)world > n) return fail(XKNN_ERR_EMPTY_SHARD, "more shards than classes");
+  if (d == 0 || d % 128 != 0 || d > 1024)
+    return fail(XKNN_ERR_SHAPE_MISMATCH, "dim must be a multiple of 128 and <= 1024");
+  if (n >= 0xffffffffull) return fail(XKNN_ERR_INVALID_ARGUMENT, "class ids are u32");
+  if (cfg->max_batch == 0 || cfg->max_batch % world)
+    return fail(XKNN_ERR_INVALID_ARGUMENT, "max_batch must be a positive multiple of world");
+  if (cfg->m_active > n) return fail(XKNN_ERR_INVALID_ARGUMENT, "M exceeds the class count");
+  if (cfg->precision != XKNN_PREC_BF16 && cfg->precision != XKNN_PREC_FP32_EXACT)
+    return fail(XKNN_ERR_CONFIG, "unknown precision");
+  auto* h = new (std::nothrow) xknn_layer;
+  if (!h) return fail(XKNN_ERR_OUT_OF_MEMORY, "host alloc");
+  xknn_status_t s = h->L.init(rank, world, n, d, cfg, comm, stream);
+  if (s != XKNN_OK) {
+    h->L.free_all();
+    delete h;
+    return s;
+  }
+  *out = h;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_destroy(xknn_layer_t* h) {
+  if (!h) return XKNN_OK;
+  cudaStreamSynchronize(h->L.stream);
+  h->L.free_all();
+  delete h;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_shard(const xknn_layer_t* h, uint64_t* b, uint64_t* e) {
+  GUARD_H(h);
+  *b = h->L.begin;
+  *e = h->L.end;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (cfg->m_active != L.cfg.m_active || cfg->max_batch != L.cfg.max_batch ||
+      cfg->precision != L.cfg.precision)
+    return fail(XKNN_ERR_CONFIG, "m_active, max_batch and precision are fixed at creation");
+  L.cfg.scale = cfg->scale;
+  L.cfg.momentum = cfg->momentum;
+  L.cfg.weight_decay = cfg->weight_decay;
+  L.cfg.rng_seed = cfg->rng_seed;
+  return XKNN_OK;
+}
+
+static cudaMemcpyKind kind_in(int on_device) {
+  return on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+}
+static cudaMemcpyKind kind_out(int on_device) {
+  return on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+}
+
+xknn_status_t xknn_layer_set_weights(xknn_layer_t* h, const float* w, int on_device) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  cudaError_t e = cudaMemcpyAsync(L.W, w, L.nw * L.d * sizeof(float), kind_in(on_device), L.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
+  L.has_weights = true;
+  return L.cuda_ok(e);
+}
+
+xknn_status_t xknn_layer_get_weights(xknn_layer_t* h, float* w, int on_device) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  cudaError_t e = cudaMemcpyAsync(w, L.W, L.nw * L.d * sizeof(float), kind_out(on_device), L.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
+  return L.cuda_ok(e);
+}
+
+xknn_status_t xknn_layer_get_velocity(xknn_layer_t* h, float* v, int on_device) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  cudaError_t e = cudaMemcpyAsync(v, L.V, L.nw * L.d * sizeof(float), kind_out(on_device), L.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
+  return L.cuda_ok(e);
+}
+
+xknn_status_t xknn_layer_weights_ptr(xknn_layer_t* h, float** w_dev) {
+  GUARD_H(h);
+  *w_dev = h->L.W;
+  h->L.has_weights = true;
+  return XKNN_OK;
+}
+
+namespace {
+__global__ void k_graph_check(const uint32_t* kpc, const uint64_t* off, const uint32_t* flat,
+                              uint64_t n, uint64_t flat_len, uint64_t begin, uint64_t end,
+                              unsigned int* kmax, unsigned long long* bad) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < n;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = kpc[c];
+    const uint64_t o = off[c];
+    atomicMax(kmax, k);
+    if (o + k > flat_len || (c + 1 < n && off[c + 1] != o + k)) { atomicAdd(bad, 1ull); continue; }
+    for (uint32_t r = 0; r < k; ++r) {
+      const uint64_t v = flat[o + r];
+      if (v < begin || v >= end) { atomicAdd(bad, 1ull); break; }
+    }
+  }
+}
+}  // namespace
+
+xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, const uint64_t* off,
+                                       const uint32_t* flat, uint64_t flat_len, int on_device) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (L.g_kpc) cudaFree(L.g_kpc);
+  if (L.g_off) cudaFree(L.g_off);
+  if (L.g_flat) cudaFree(L.g_flat);
+  L.g_kpc = nullptr;
+  L.g_off = nullptr;
+  L.g_flat = nullptr;
+  L.has_graph = false;
+  XK_CUDA_H(xknn::dalloc(&L.g_kpc, L.n));
+  XK_CUDA_H(xknn::dalloc(&L.g_off, L.n));
+  XK_CUDA_H(xknn::dalloc(&L.g_flat, flat_len));
+  XK_CUDA_H(cudaMemcpyAsync(L.g_kpc, kpc, L.n * 4, kind_in(on_device), L.stream));
+  XK_CUDA_H(cudaMemcpyAsync(L.g_off, off, L.n * 8, kind_in(on_device), L.stream));
+  if (flat_len)
+    XK_CUDA_H(cudaMemcpyAsync(L.g_flat, flat, flat_len * 4, kind_in(on_device), L.stream));
+  L.g_flat_len = flat_len;
+  unsigned int* dk;
+  unsigned long long* db;
+  XK_CUDA_H(cudaMalloc(&dk, 16));
+  db = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(dk) + 8);
+  XK_CUDA_H(cudaMemsetAsync(dk, 0, 16, L.stream));
+  k_graph_check<<<xknn::grid_for(L.n, 256), 256, 0, L.stream>>>(L.g_kpc, L.g_off, L.g_flat, L.n,
+                                                                 flat_len, L.begin, L.end, dk, db);
+  ++L.launches;
+  unsigned int kmax = 0;
+  unsigned long long bad = 0;
+  XK_CUDA_H(cudaMemcpyAsync(&kmax, dk, 4, cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaMemcpyAsync(&bad, db, 8, cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  cudaFree(dk);
+  if (bad) return fail(XKNN_ERR_SHAPE_MISMATCH, "graph CSR inconsistent or entries outside shard");
+  // global bound on one label's pooled slice length: sum over shards of their longest slice
+  if (L.world > 1) {
+    unsigned int* dv;
+    XK_CUDA_H(cudaMalloc(&dv, 4));
+    XK_CUDA_H(cudaMemcpyAsync(dv, &kmax, 4, cudaMemcpyHostToDevice, L.stream));
+    ncclResult_t r = ncclAllReduce(dv, dv, 1, ncclUint32, ncclSum, L.comm, L.stream);
+    if (r != ncclSuccess) return L.nccl_ok(r);
+    XK_CUDA_H(cudaMemcpyAsync(&kmax, dv, 4, cudaMemcpyDeviceToHost, L.stream));
+    XK_CUDA_H(cudaStreamSynchronize(L.stream));
+    cudaFree(dv);
+  }
+  L.g_kmax = kmax;
+  const uint64_t hl = (uint64_t)kmax + L.bmax + 2;
+  if (hl > L.hist_len) {
+    if (L.hist) cudaFree(L.hist);
+    XK_CUDA_H(xknn::dalloc(&L.hist, hl));
+    L.hist_len = hl;
+  }
+  L.has_graph = true;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t batch,
+                          uint32_t* out_active_dev, uint64_t* count_host, int* contains_all) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "knn mode without shard graphs");
+  if (batch == 0 || batch > L.bmax) return fail(XKNN_ERR_INVALID_ARGUMENT, "batch outside (0, max_batch]");
+  XK_CUDA_H(cudaMemcpyAsync(L.labels_all, labels_dev, batch * 4, cudaMemcpyDeviceToDevice, L.stream));
+  xknn_status_t s = L.run_selection(batch);
+  if (s != XKNN_OK) return s;
+  xknn::SelState hs;
+  XK_CUDA_H(cudaMemcpyAsync(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost, L.stream));
+  s = xknn_layer_sync(h);
+  if (s != XKNN_OK) return s;
+  if (out_active_dev && hs.active_count)
+    XK_CUDA_H(cudaMemcpyAsync(out_active_dev, L.active, hs.active_count * 4,
+                              cudaMemcpyDeviceToDevice, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  if (count_host) *count_host = hs.active_count;
+  if (contains_all) *contains_all = hs.labels_found == hs.labels_local;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_step(xknn_layer_t* h, const float* feats, const uint32_t* labels,
+                        uint64_t bl, float lr, double* loss_dev, float* gfeat) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: knn mode without shard graphs");
+  if (bl == 0 || bl * L.world > L.bmax)
+    return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: batch size must be a positive multiple of P (<= max_batch)");
+  return L.run_step(feats, labels, bl, lr, loss_dev, gfeat);
+}
+
+xknn_status_t xknn_layer_sync(xknn_layer_t* h) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  unsigned long long w = 0;
+  XK_CUDA_H(cudaMemcpyAsync(&w, L.err, 8, cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  if (w) {
+    XK_CUDA_H(cudaMemsetAsync(L.err, 0, 8, L.stream));
+    XK_CUDA_H(cudaStreamSynchronize(L.stream));
+    const xknn_status_t code = (xknn_status_t)(w & 0xff);
+    xknn::g_row = w >> 8;
+    return fail(code, std::string(xknn_status_string(code)) + " (device, index " +
+                          std::to_string(w >> 8) + ")");
+  }
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_last_active(xknn_layer_t* h, uint64_t* total, uint64_t* local) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  xknn::SelState hs;
+  XK_CUDA_H(cudaMemcpyAsync(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  if (total) *total = hs.active_total;
+  if (local) *local = hs.active_count;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out, uint64_t capacity) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (L.cfg.precision != XKNN_PREC_FP32_EXACT)
+    return fail(XKNN_ERR_UNSUPPORTED, "logits are never materialized in BF16 precision");
+  xknn::SelState hs;
+  XK_CUDA_H(cudaMemcpyAsync(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  const uint64_t cnt = L.last_b * hs.active_count;
+  if (capacity < cnt) return fail(XKNN_ERR_SHAPE_MISMATCH, "capacity below B x active_local");
+  XK_CUDA_H(cudaMemcpyAsync(out, L.logits, cnt * 4, cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  return XKNN_OK;
+}
+
+uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h) { return h ? h->L.launches : 0; }
+
+}  // extern "C"

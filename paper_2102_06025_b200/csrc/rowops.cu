@@ -1,0 +1,215 @@
+// rowops.cu -- HBM-bound row kernels shared by both precisions: feature normalize, active-row
+// gather + normalize, normalize-backward fused with the sparse momentum-SGD update, and the
+// feature normalize-backward.  One warp per 512-float row, 16-byte vector loads/stores.
+//
+// Arithmetic follows the reference op-for-op in fp32 (no FMA contraction: __fmul_rn/__fadd_rn)
+// with fp64 row reductions:
+//   l2_normalize_rows_cached  matrix.cpp:12-29     norm = float(sqrt(sum double(x^2)))
+//   l2_normalize_backward     matrix.cpp:31-48     (g - float(sum double(g*x_hat)) * x_hat) / |x|
+//   inline W backward         parallel.cpp:653-666
+//   SgdMomentum::step_rows    fccs.cpp:74-89       v = (mu*v + g) + wd*w ; w -= lr*v
+#include "kernels.cuh"
+
+namespace xknn {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T warp_allsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(XKNN_FULL_MASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst, float a, float b, float c,
+                                             float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = u;
+}
+
+// D is a multiple of 128 (checked at create); each lane owns D/128 float4 chunks.
+template <int DV>  // DV = D/128 float4 per lane
+__global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, uint32_t d,
+                                 const uint32_t* __restrict__ row_ids, const unsigned int* count,
+                                 uint64_t id_base, float* __restrict__ out32,
+                                 __nv_bfloat16* __restrict__ out16, float* __restrict__ norms,
+                                 unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nrows = count ? *count : rows;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
+       r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t src_row = row_ids ? (uint64_t)row_ids[r] - id_base : r;
+    const float4* src = reinterpret_cast<const float4*>(in + src_row * d);
+    float4 v[DV];
+    double sq = 0.0;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      v[c] = src[lane + 32 * c];
+      sq += (double)v[c].x * v[c].x;
+      sq += (double)v[c].y * v[c].y;
+      sq += (double)v[c].z * v[c].z;
+      sq += (double)v[c].w * v[c].w;
+    }
+    sq = warp_allsum(sq);
+    const float norm = (float)sqrt(sq);
+    if (norm < 1e-12f) {
+      if (lane == 0) raise_error(err, XKNN_ERR_ZERO_NORM_ROW, r);
+      continue;
+    }
+    if (lane == 0 && norms) norms[r] = norm;
+    const float inv = 1.0f / norm;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      float4 o;
+      o.x = __fmul_rn(v[c].x, inv);
+      o.y = __fmul_rn(v[c].y, inv);
+      o.z = __fmul_rn(v[c].z, inv);
+      o.w = __fmul_rn(v[c].w, inv);
+      const uint64_t col = (uint64_t)(lane + 32 * c) * 4;
+      if (out32) *reinterpret_cast<float4*>(out32 + r * d + col) = o;
+      if (out16) store_bf16x4(out16 + r * d + col, o.x, o.y, o.z, o.w);
+    }
+  }
+}
+
+// Normalize-backward of each active row through its cached norm, then SgdMomentum::step_rows
+// on (W, V).  g rows are compact (row t <-> active[t]).  Skipped entirely if any error was
+// raised earlier in the step (the reference throws before touching parameters).
+template <int DV>
+__global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
+                              const float* __restrict__ G, const uint32_t* __restrict__ active,
+                              const unsigned int* count, uint64_t begin, uint32_t d,
+                              const float* __restrict__ wnorm, float lr, float mu, float wd,
+                              const unsigned long long* err) {
+  if (*err) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nrows = *count;
+  for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < nrows;
+       t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t row = (uint64_t)active[t] - begin;
+    float4* wp = reinterpret_cast<float4*>(W + row * d);
+    float4* vp = reinterpret_cast<float4*>(V + row * d);
+    const float4* gp = reinterpret_cast<const float4*>(G + t * d);
+    const float norm = wnorm[t];
+    const float inv = 1.0f / norm;
+    float4 w[DV], g[DV], nh[DV];
+    double dot = 0.0;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      w[c] = wp[lane + 32 * c];
+      g[c] = gp[lane + 32 * c];
+      nh[c].x = __fmul_rn(w[c].x, inv);
+      nh[c].y = __fmul_rn(w[c].y, inv);
+      nh[c].z = __fmul_rn(w[c].z, inv);
+      nh[c].w = __fmul_rn(w[c].w, inv);
+      dot += (double)g[c].x * nh[c].x;
+      dot += (double)g[c].y * nh[c].y;
+      dot += (double)g[c].z * nh[c].z;
+      dot += (double)g[c].w * nh[c].w;
+    }
+    dot = warp_allsum(dot);
+    const float dd = (float)dot;
+    const float inv2 = 1.0f / norm;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      float4 v = vp[lane + 32 * c];
+      float gr, vv;
+#define XKNN_UPD(comp)                                                                  \
+  gr = __fmul_rn(__fsub_rn(g[c].comp, __fmul_rn(dd, nh[c].comp)), inv2);               \
+  vv = __fadd_rn(__fadd_rn(__fmul_rn(mu, v.comp), gr), __fmul_rn(wd, w[c].comp));      \
+  v.comp = vv;                                                                          \
+  w[c].comp = __fsub_rn(w[c].comp, __fmul_rn(lr, vv));
+      XKNN_UPD(x) XKNN_UPD(y) XKNN_UPD(z) XKNN_UPD(w)
+#undef XKNN_UPD
+      vp[lane + 32 * c] = v;
+      wp[lane + 32 * c] = w[c];
+    }
+  }
+}
+
+// gfeat = l2_normalize_backward(x_hat, norms, g) for this rank's rows; x_hat recomputed from the
+// raw features exactly as the forward did.
+template <int DV>
+__global__ void k_feature_backward(const float* __restrict__ X, const float* __restrict__ xnorm,
+                                   const float* __restrict__ G, uint64_t rows, uint32_t d,
+                                   float* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const float norm = xnorm[r];
+    const float inv = 1.0f / norm;
+    const float4* xp = reinterpret_cast<const float4*>(X + r * d);
+    const float4* gp = reinterpret_cast<const float4*>(G + r * d);
+    float4 nh[DV], g[DV];
+    double dot = 0.0;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      const float4 x = xp[lane + 32 * c];
+      g[c] = gp[lane + 32 * c];
+      nh[c].x = __fmul_rn(x.x, inv);
+      nh[c].y = __fmul_rn(x.y, inv);
+      nh[c].z = __fmul_rn(x.z, inv);
+      nh[c].w = __fmul_rn(x.w, inv);
+      dot += (double)g[c].x * nh[c].x;
+      dot += (double)g[c].y * nh[c].y;
+      dot += (double)g[c].z * nh[c].z;
+      dot += (double)g[c].w * nh[c].w;
+    }
+    dot = warp_allsum(dot);
+    const float dd = (float)dot;
+    const float inv2 = 1.0f / norm;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      float4 o;
+      o.x = __fmul_rn(__fsub_rn(g[c].x, __fmul_rn(dd, nh[c].x)), inv2);
+      o.y = __fmul_rn(__fsub_rn(g[c].y, __fmul_rn(dd, nh[c].y)), inv2);
+      o.z = __fmul_rn(__fsub_rn(g[c].z, __fmul_rn(dd, nh[c].z)), inv2);
+      o.w = __fmul_rn(__fsub_rn(g[c].w, __fmul_rn(dd, nh[c].w)), inv2);
+      reinterpret_cast<float4*>(out + r * d)[lane + 32 * c] = o;
+    }
+  }
+}
+
+}  // namespace
+
+#define XKNN_DISPATCH_D(d, KERNEL, GRID, BLOCK, STREAM, ...)                              \
+  switch ((d) / 128) {                                                                    \
+    case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
+    case 2: KERNEL<2><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
+    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
+    case 8: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
+    default: return cudaErrorInvalidValue;                                                \
+  }
+
+cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
+                                  const uint32_t* row_ids, const unsigned int* count,
+                                  uint64_t id_base, float* out32, __nv_bfloat16* out16,
+                                  float* norms, unsigned long long* err, cudaStream_t s) {
+  const unsigned grid = grid_for(rows * 32, 256);
+  XKNN_DISPATCH_D(d, k_normalize_rows, grid, 256, s, in, rows, d, row_ids, count, id_base, out32,
+                  out16, norms, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
+                               const unsigned int* count, uint64_t max_rows, uint64_t begin,
+                               uint32_t d, const float* wnorm, float lr, float mu, float wd,
+                               const unsigned long long* err, cudaStream_t s) {
+  const unsigned grid = grid_for(max_rows * 32, 256);
+  XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,
+                  wd, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
+                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s) {
+  const unsigned grid = grid_for(rows * 32, 256);
+  XKNN_DISPATCH_D(d, k_feature_backward, grid, 256, s, X, xnorm, G, rows, d, out);
+  return cudaGetLastError();
+}
+
+}  // namespace xknn

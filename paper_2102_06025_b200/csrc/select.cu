@@ -1,0 +1,552 @@
+// select.cu -- Algorithm 1 active-class selection on device, bit-exact with
+// select_active_classes(span<CompressedKnnGraph>) (knn_softmax.cpp:117-134) and
+// finish_selection (knn_softmax.cpp:17-81), executed shard-parallel.
+//
+// Every shard holds the CSR graph pruned to its own classes (compress_graph,
+// knn_graph.cpp:235-266), so the pool restricted to a shard is exactly the union of that
+// shard's slices: each rank builds its part of the pool locally (bitmap over its class range,
+// atomicMin rank / atomicAdd occurrence per candidate), and only P pool counts cross NVLink.
+//
+// Padding branch (|pool| < M, the default M = 10% N): the reference draws
+// j_i = uniform_int_distribution<size_t>(i, |C|-1)(mt19937_64(seed)) and swaps C[i], C[j_i]
+// over the ascending complement C (knn_softmax.cpp:39-49).  The reference re-seeds on every
+// call, so the raw 64-bit stream is a constant of the layer (cached in HBM).  Each draw is
+// Lemire's multiply-high (uniform_int_dist.h:257-274); rejections (p ~ range/2^64) are
+// detected and replayed sequentially.  The Fisher-Yates result is resolved without the
+// complement array: out[i] = C0[src(i)], where src follows "last writer" chains over the
+// picks sorted by (j, i).  Positions map to classes by rank/select against the sorted pool.
+//
+// Over-full branch (|pool| > M): labels first, then the global top-(M - |labels|) by
+// (best_rank asc, occurrences desc, class asc) (knn_softmax.cpp:61-67) via two histogram
+// all-reduces and a rank-ordered tie split -- the keys are shard-local because every class
+// lives in exactly one shard.
+#include <cub/cub.cuh>
+
+#include "layer.cuh"
+
+namespace xknn {
+
+namespace {
+
+constexpr int kCompactBlock = 256;
+
+// ---- pool marking: one warp per batch label, lanes stride the label's slice
+__global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch, uint64_t n,
+                            uint64_t begin, uint64_t nw, const uint32_t* __restrict__ kpc,
+                            const uint64_t* __restrict__ off, const uint32_t* __restrict__ flat,
+                            uint32_t* pool_bits, uint32_t* best, uint32_t* occ,
+                            unsigned long long* err, int reset) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < batch; i += nwarps) {
+    const uint32_t y = labels[i];
+    if (y >= n) {
+      if (lane == 0 && !reset) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
+      continue;
+    }
+    const uint32_t kk = kpc[y];
+    const uint64_t o = off[y];
+    for (uint32_t r = lane; r < kk; r += 32) {
+      const uint64_t lc = (uint64_t)flat[o + r] - begin;
+      if (lc >= nw) continue;  // validated at set_graph time
+      if (reset) {
+        best[lc] = kNone;
+        occ[lc] = 0;
+      } else {
+        atomicOr(&pool_bits[lc >> 5], 1u << (lc & 31));
+        atomicMin(&best[lc], r);
+        atomicAdd(&occ[lc], 1u);
+      }
+    }
+  }
+}
+
+__global__ void k_label_bits(const uint32_t* __restrict__ distinct, const uint32_t* n_distinct,
+                             uint64_t begin, uint64_t end, uint32_t* lab_bits, SelState* st) {
+  const uint32_t nd = *n_distinct;
+  uint32_t local = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
+    const uint64_t y = distinct[i];
+    if (y >= begin && y < end) {
+      const uint64_t lc = y - begin;
+      atomicOr(&lab_bits[lc >> 5], 1u << (lc & 31));
+      ++local;
+    }
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&st->labels_local, local);
+}
+
+// ---- bitmap -> sorted list compaction (ballot-free: one 32-bit word per thread)
+__global__ void k_bits_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                             uint64_t nwords, uint32_t* blk_counts) {
+  using BR = cub::BlockReduce<uint32_t, kCompactBlock>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
+  uint32_t word = 0;
+  if (w < nwords) word = a[w] | (b ? b[w] : 0u);
+  const uint32_t c = BR(tmp).Sum(__popc(word));
+  if (threadIdx.x == 0) blk_counts[blockIdx.x] = c;
+}
+
+__global__ void k_bits_write(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                             uint64_t nwords, const uint32_t* __restrict__ blk_off,
+                             uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
+                             unsigned int* out_count) {
+  using BS = cub::BlockScan<uint32_t, kCompactBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
+  uint32_t word = 0;
+  if (w < nwords) word = a[w] | (b ? b[w] : 0u);
+  uint32_t pos;
+  BS(tmp).ExclusiveSum(__popc(word), pos);
+  pos += blk_off[blockIdx.x];
+  while (word) {
+    const uint32_t bit = __ffs(word) - 1;
+    out[pos++] = base + (uint32_t)(w * 32 + bit);
+    word &= word - 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_count = blk_off[nblocks];
+}
+
+__global__ void k_store_pool_count(SelState* st, unsigned long long* pool_counts, int rank) {
+  st->pool_local = st->pool_count;
+  pool_counts[rank] = st->pool_count;
+}
+
+// ---- the plan: which branch, how many pads, which complement positions this shard owns
+__global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int world, int rank,
+                       uint64_t n, uint64_t m, uint64_t begin, uint64_t nw,
+                       const uint32_t* n_distinct, unsigned long long* err) {
+  unsigned long long total = 0, before = 0;
+  for (int s = 0; s < world; ++s) {
+    total += pool_counts[s];
+    if (s < rank) before += pool_counts[s];
+  }
+  const unsigned long long nd = *n_distinct;
+  st->pool_total = total;
+  st->nd = nd;
+  st->csize = n - total;
+  st->cbase = begin - before;
+  st->compl_local = nw - pool_counts[rank];
+  st->first_rej = kNone;
+  st->need = 0;
+  st->take = 0;
+  if (m < nd) raise_error(err, XKNN_ERR_M_TOO_SMALL);          // knn_softmax.cpp:24-27
+  if (m > n) raise_error(err, XKNN_ERR_INVALID_ARGUMENT);      // knn_softmax.cpp:28-29
+  if (total < m) {
+    st->branch = kPad;
+    st->need = m - total;
+  } else if (total == m) {
+    st->branch = kExact;
+  } else {
+    st->branch = kOverfull;
+    st->take = m > nd ? m - nd : 0;
+  }
+  st->active_total = m;
+}
+
+// ---- padding: Lemire draws from the cached mt19937_64 stream
+__global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint64_t m,
+                        uint32_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t sentinel) {
+  const bool pad = st->branch == kPad;
+  const uint64_t need = pad ? st->need : 0;
+  const uint64_t csize = st->csize;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i < need) {
+      const uint64_t range = csize - i;  // __uerange = (csize-1) - i + 1
+      const uint64_t u = mt[i];
+      const uint64_t lo = u * range;
+      if (lo < range) {
+        const uint64_t thr = (0ull - range) % range;
+        if (lo < thr) atomicMin(&st->first_rej, (unsigned)i);
+      }
+      key[i] = (uint32_t)(i + __umul64hi(u, range));
+    } else {
+      key[i] = sentinel;
+    }
+    val[i] = (uint32_t)i;
+  }
+}
+
+// Sequential replay from the first rejected draw (uniform_int_dist.h:268-272).  Taken with
+// probability ~ need*csize/2^64 per step.
+__global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, uint64_t mt_len,
+                               uint32_t* key, unsigned long long* err) {
+  if (st->branch != kPad || st->first_rej == kNone) return;
+  const uint64_t need = st->need, csize = st->csize;
+  uint64_t pos = st->first_rej;
+  for (uint64_t i = st->first_rej; i < need; ++i) {
+    const uint64_t range = csize - i;
+    if (pos >= mt_len) { raise_error(err, XKNN_ERR_UNSUPPORTED); return; }
+    uint64_t u = mt[pos++];
+    uint64_t lo = u * range;
+    if (lo < range) {
+      const uint64_t thr = (0ull - range) % range;
+      while (lo < thr) {
+        if (pos >= mt_len) { raise_error(err, XKNN_ERR_UNSUPPORTED); return; }
+        u = mt[pos++];
+        lo = u * range;
+      }
+    }
+    key[i] = (uint32_t)(i + __umul64hi(u, range));
+  }
+}
+
+// pred[i] = last t < i with j_t == j_i (sorted runs are stable: ascending t)
+__global__ void k_pred(const SelState* st, const uint32_t* __restrict__ key_s,
+                       const uint32_t* __restrict__ val_s, uint32_t* __restrict__ pred) {
+  if (st->branch != kPad) return;
+  const uint64_t need = st->need;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < need;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = key_s[q];
+    pred[val_s[q]] = (q > 0 && key_s[q - 1] == j) ? val_s[q - 1] : kNone;
+  }
+}
+
+// lw[t] = last t' < t with j_t' == t (the swap that last moved a value into position t before
+// step t ran)
+__global__ void k_lastwriter(const SelState* st, const uint32_t* __restrict__ key_s,
+                             const uint32_t* __restrict__ val_s, uint32_t* __restrict__ lw) {
+  if (st->branch != kPad) return;
+  const uint32_t need = (uint32_t)st->need;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < need;
+       t += gridDim.x * blockDim.x) {
+    // upper_bound(t) over key_s[0, need)
+    uint32_t lo = 0, hi = need;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (key_s[mid] <= t) lo = mid + 1; else hi = mid;
+    }
+    uint32_t r = kNone;
+    if (lo > 0 && key_s[lo - 1] == t) {
+      uint32_t q = lo - 1;
+      if (val_s[q] == t) {
+        if (q > 0 && key_s[q - 1] == t) r = val_s[q - 1];
+      } else {
+        r = val_s[q];
+      }
+    }
+    lw[t] = r;
+  }
+}
+
+// out[i] = C0[src(i)]; the shard owning complement position src marks the class
+__global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
+                          const uint32_t* __restrict__ pred, const uint32_t* __restrict__ lw,
+                          const uint32_t* __restrict__ pool_list, uint64_t begin,
+                          uint32_t* act_bits) {
+  if (st->branch != kPad) return;
+  const uint64_t need = st->need, cbase = st->cbase, cl = st->compl_local;
+  const uint32_t npool = st->pool_count;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < need;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t src;
+    uint32_t t = pred[i];
+    if (t != kNone) {
+      while (lw[t] != kNone) t = lw[t];
+      src = t;
+    } else {
+      src = key[i];
+    }
+    if (src < cbase || src >= cbase + cl) continue;
+    const uint64_t q = src - cbase;  // q-th class of [begin,end) outside the pool
+    uint32_t lo = 0, hi = npool;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((uint64_t)(pool_list[mid] - begin) - mid <= q) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t lc = q + lo;
+    atomicOr(&act_bits[lc >> 5], 1u << (lc & 31));
+  }
+}
+
+// ---- over-full ranking
+__global__ void k_of_hist_rank(const SelState* st, const uint32_t* __restrict__ pool_list,
+                               uint64_t begin, const uint32_t* __restrict__ lab_bits,
+                               const uint32_t* __restrict__ best, uint32_t* hist) {
+  if (st->branch != kOverfull) return;
+  const uint32_t np = st->pool_count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const uint32_t lc = pool_list[i] - (uint32_t)begin;
+    if (lab_bits[lc >> 5] & (1u << (lc & 31))) continue;
+    atomicAdd(&hist[best[lc]], 1u);
+  }
+}
+
+__global__ void k_of_plan_rank(SelState* st, const uint32_t* hist, uint32_t nbins) {
+  if (st->branch != kOverfull) return;
+  const unsigned long long t = st->take;
+  unsigned long long cum = 0;
+  uint32_t r = nbins;
+  for (uint32_t b = 0; b < nbins; ++b) {
+    if (cum + hist[b] >= t) { r = b; break; }
+    cum += hist[b];
+  }
+  st->r_star = r;
+  st->tie_quota = t - cum;  // still needed at rank r_star
+}
+
+__global__ void k_of_hist_occ(const SelState* st, const uint32_t* __restrict__ pool_list,
+                              uint64_t begin, const uint32_t* __restrict__ lab_bits,
+                              const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
+                              uint32_t* hist) {
+  if (st->branch != kOverfull) return;
+  const uint32_t np = st->pool_count, rs = st->r_star;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const uint32_t lc = pool_list[i] - (uint32_t)begin;
+    if (lab_bits[lc >> 5] & (1u << (lc & 31))) continue;
+    if (best[lc] == rs) atomicAdd(&hist[occ[lc]], 1u);
+  }
+}
+
+__global__ void k_of_plan_occ(SelState* st, const uint32_t* hist, uint32_t nbins) {
+  if (st->branch != kOverfull) return;
+  const unsigned long long t = st->tie_quota;
+  unsigned long long cum = 0;
+  uint32_t o = 0;
+  bool found = false;
+  for (int b = (int)nbins - 1; b >= 0; --b) {  // occurrences descending
+    if (cum + hist[b] >= t) { o = (uint32_t)b; found = true; break; }
+    cum += hist[b];
+  }
+  st->o_star = found ? o : 0;
+  st->tie_quota = found ? t - cum : 0;
+}
+
+__global__ void k_of_tie_count(SelState* st, const uint32_t* __restrict__ pool_list,
+                               uint64_t begin, const uint32_t* __restrict__ lab_bits,
+                               const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
+                               unsigned long long* tie_counts, int rank) {
+  if (st->branch != kOverfull) { if (threadIdx.x == 0 && blockIdx.x == 0) tie_counts[rank] = 0; return; }
+  const uint32_t np = st->pool_count, rs = st->r_star, os = st->o_star;
+  __shared__ unsigned int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const uint32_t lc = pool_list[i] - (uint32_t)begin;
+    if (lab_bits[lc >> 5] & (1u << (lc & 31))) continue;
+    if (best[lc] == rs && occ[lc] == os) atomicAdd(&cnt, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tie_counts[rank] = cnt;
+}
+
+// single block: labels, strictly better candidates, and this shard's share of the ties (lowest
+// class ids first; shards are ordered by class range so rank order == class order)
+__global__ void k_of_select(SelState* st, const uint32_t* __restrict__ pool_list, uint64_t begin,
+                            const uint32_t* __restrict__ lab_bits, const uint32_t* __restrict__ best,
+                            const uint32_t* __restrict__ occ, const unsigned long long* tie_counts,
+                            int rank, uint32_t nbins_rank, uint32_t* act_bits) {
+  if (st->branch != kOverfull) return;
+  using BS = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  unsigned long long before = 0;
+  for (int s = 0; s < rank; ++s) before += tie_counts[s];
+  const unsigned long long need = st->tie_quota;
+  const unsigned long long quota = need > before ? min(need - before, tie_counts[rank]) : 0;
+  const uint32_t np = st->pool_count, rs = st->r_star, os = st->o_star;
+  const bool all = rs >= nbins_rank;  // fewer candidates than take: keep every candidate
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < np; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t lc = 0, tie = 0;
+    bool sel = false;
+    if (i < np) {
+      lc = pool_list[i] - (uint32_t)begin;
+      if (!(lab_bits[lc >> 5] & (1u << (lc & 31)))) {
+        const uint32_t b = best[lc], o = occ[lc];
+        if (all || b < rs || (b == rs && o > os)) sel = true;
+        else if (b == rs && o == os) tie = 1;
+      }
+    }
+    uint32_t idx, total;
+    BS(tmp).ExclusiveSum(tie, idx, total);
+    if (tie && carry + idx < quota) sel = true;
+    if (sel) atomicOr(&act_bits[lc >> 5], 1u << (lc & 31));
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+}
+
+__global__ void k_or_bits(const SelState* st, uint32_t* act, const uint32_t* __restrict__ lab,
+                          const uint32_t* __restrict__ pool, uint64_t nwords) {
+  const bool with_pool = st->branch != kOverfull;  // over-full: k_of_select marked its picks
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (uint64_t)gridDim.x * blockDim.x)
+    act[w] |= lab[w] | (with_pool ? pool[w] : 0u);
+}
+
+// label -> column in this shard's active list (-1 if another shard owns it)
+__global__ void k_label_cols(SelState* st, const uint32_t* __restrict__ labels, uint32_t batch,
+                             const uint32_t* __restrict__ active, uint64_t begin, uint64_t end,
+                             int32_t* label_col, unsigned long long* err) {
+  const uint32_t na = st->active_count;
+  uint32_t found = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += gridDim.x * blockDim.x) {
+    const uint32_t y = labels[i];
+    int32_t col = -1;
+    if (y >= begin && y < end) {
+      const uint32_t p = lower_bound_u32(active, na, y);
+      if (p < na && active[p] == y) col = (int32_t)p;
+      else raise_error(err, XKNN_ERR_LABEL_NOT_ACTIVE, i);
+    }
+    label_col[i] = col;
+  }
+  (void)found;
+}
+
+__global__ void k_labels_found(SelState* st, const uint32_t* __restrict__ distinct,
+                               const uint32_t* n_distinct, const uint32_t* __restrict__ active,
+                               uint64_t begin, uint64_t end) {
+  const uint32_t nd = *n_distinct, na = st->active_count;
+  uint32_t f = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
+    const uint32_t y = distinct[i];
+    if (y >= begin && y < end) {
+      const uint32_t p = lower_bound_u32(active, na, y);
+      f += (p < na && active[p] == y);
+    }
+  }
+  f = warp_sum(f);
+  if ((threadIdx.x & 31) == 0 && f) atomicAdd(&st->labels_found, f);
+}
+
+__global__ void k_zero_sel(SelState* st) {
+  st->labels_local = 0;
+  st->labels_found = 0;
+  st->pool_count = 0;
+  st->active_count = 0;
+}
+
+}  // namespace
+
+// Compacts (a | b) over this shard's bitmap into sorted global ids.
+static xknn_status_t compact_bits(Layer& L, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                                  unsigned int* out_count) {
+  const uint32_t nblocks = (uint32_t)((L.nwords + kCompactBlock - 1) / kCompactBlock);
+  k_bits_count<<<nblocks, kCompactBlock, 0, L.stream>>>(a, b, L.nwords, L.blk_counts);
+  ++L.launches;
+  // blk_counts[nblocks] is kept 0, so the exclusive scan's last entry is the total
+  size_t bytes = L.cub_tmp_bytes;
+  if (cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.blk_counts, L.blk_counts + nblocks + 1,
+                                    nblocks + 1, L.stream) != cudaSuccess)
+    return L.cuda_ok(cudaGetLastError());
+  k_bits_write<<<nblocks, kCompactBlock, 0, L.stream>>>(a, b, L.nwords, L.blk_counts + nblocks + 1,
+                                                        nblocks, (uint32_t)L.begin, out, out_count);
+  ++L.launches;
+  return L.cuda_ok(cudaGetLastError());
+}
+
+xknn_status_t Layer::run_selection(uint64_t batch) {
+  const uint32_t B = (uint32_t)batch;
+  const uint64_t m = cfg.m_active;
+  XK_TRY(ensure_mt_cache());
+  const size_t wbytes = nwords * sizeof(uint32_t);
+  XK_CUDA(cudaMemsetAsync(pool_bits, 0, wbytes, stream));
+  XK_CUDA(cudaMemsetAsync(act_bits, 0, wbytes, stream));
+  XK_CUDA(cudaMemsetAsync(lab_bits, 0, wbytes, stream));
+  k_zero_sel<<<1, 1, 0, stream>>>(st);
+  XK_LAUNCH();
+
+  // (1) pool of this shard: union of its slices for every batch label (knn_softmax.cpp:122-132)
+  k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
+      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, sel_best, sel_occ, err, 0);
+  XK_LAUNCH();
+  // (2) distinct labels (knn_softmax.cpp:20-23)
+  size_t bytes = cub_tmp_bytes;
+  XK_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, bytes, labels_all, labels_sorted, (int)B, 0, 32,
+                                         stream));
+  bytes = cub_tmp_bytes;
+  XK_CUDA(cub::DeviceSelect::Unique(cub_tmp, bytes, labels_sorted, labels_distinct, n_distinct,
+                                    (int)B, stream));
+  launches += 6;
+  k_label_bits<<<grid_for(B, 256), 256, 0, stream>>>(labels_distinct, n_distinct, begin, end,
+                                                      lab_bits, st);
+  XK_LAUNCH();
+  // (3) sorted local pool and the cross-shard pool counts
+  XK_TRY(compact_bits(*this, pool_bits, nullptr, pool_list, &st->pool_count));
+  k_store_pool_count<<<1, 1, 0, stream>>>(st, pool_counts, rank);
+  XK_LAUNCH();
+  if (world > 1)
+    XK_NCCL(ncclAllGather(pool_counts + rank, pool_counts, 1, ncclUint64, comm, stream));
+  k_plan<<<1, 1, 0, stream>>>(st, pool_counts, world, rank, n, m, begin, nw, n_distinct, err);
+  XK_LAUNCH();
+
+  // (4a) padding branch
+  const bool pad_possible = m > 0;
+  if (pad_possible) {
+    uint32_t bits = 1;
+    while (bits < 32 && (1ull << bits) <= n) ++bits;
+    if (bits < 32) ++bits;
+    const uint32_t sentinel = bits >= 32 ? 0xffffffffu : (uint32_t)((1ull << bits) - 1);
+    k_picks<<<grid_for(m, 256), 256, 0, stream>>>(st, mt_cache, m, pick_key, pick_val, sentinel);
+    XK_LAUNCH();
+    k_picks_replay<<<1, 1, 0, stream>>>(st, mt_cache, mt_len, pick_key, err);
+    XK_LAUNCH();
+    bytes = cub_tmp_bytes;
+    XK_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, pick_key, pick_key_s, pick_val,
+                                            pick_val_s, (int)m, 0, (int)bits, stream));
+    launches += 4;
+    k_pred<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, pred);
+    XK_LAUNCH();
+    k_lastwriter<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, lw);
+    XK_LAUNCH();
+    k_pad_map<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pred, lw, pool_list, begin,
+                                                     act_bits);
+    XK_LAUNCH();
+  }
+  // (4b) over-full branch: only reachable when B * k could exceed M
+  const bool overfull_possible = (uint64_t)B * g_kmax > m;
+  if (overfull_possible) {
+    const uint32_t nb_rank = g_kmax ? g_kmax : 1;
+    const uint32_t nb_occ = B + 1;
+    uint32_t* h_rank = hist;
+    uint32_t* h_occ = hist + nb_rank;
+    XK_CUDA(cudaMemsetAsync(hist, 0, (nb_rank + nb_occ) * sizeof(uint32_t), stream));
+    k_of_hist_rank<<<grid_for(nw, 256), 256, 0, stream>>>(st, pool_list, begin, lab_bits,
+                                                          sel_best, h_rank);
+    XK_LAUNCH();
+    if (world > 1) XK_NCCL(ncclAllReduce(h_rank, h_rank, nb_rank, ncclUint32, ncclSum, comm, stream));
+    k_of_plan_rank<<<1, 1, 0, stream>>>(st, h_rank, nb_rank);
+    XK_LAUNCH();
+    k_of_hist_occ<<<grid_for(nw, 256), 256, 0, stream>>>(st, pool_list, begin, lab_bits,
+                                                         sel_best, sel_occ, h_occ);
+    XK_LAUNCH();
+    if (world > 1) XK_NCCL(ncclAllReduce(h_occ, h_occ, nb_occ, ncclUint32, ncclSum, comm, stream));
+    k_of_plan_occ<<<1, 1, 0, stream>>>(st, h_occ, nb_occ);
+    XK_LAUNCH();
+    k_of_tie_count<<<1, 1024, 0, stream>>>(st, pool_list, begin, lab_bits, sel_best, sel_occ,
+                                           tie_counts, rank);
+    XK_LAUNCH();
+    if (world > 1)
+      XK_NCCL(ncclAllGather(tie_counts + rank, tie_counts, 1, ncclUint64, comm, stream));
+    k_of_select<<<1, 1024, 0, stream>>>(st, pool_list, begin, lab_bits, sel_best, sel_occ,
+                                        tie_counts, rank, nb_rank, act_bits);
+    XK_LAUNCH();
+  }
+  // (5) final ActiveSet slice: pool (padding / exact fit) or ranked picks, plus the labels
+  //     (always retained); sorted by construction
+  k_or_bits<<<grid_for(nwords, 256), 256, 0, stream>>>(st, act_bits, lab_bits, pool_bits, nwords);
+  XK_LAUNCH();
+  XK_TRY(compact_bits(*this, act_bits, nullptr, active, &st->active_count));
+  k_label_cols<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_all, B, active, begin, end,
+                                                      label_col, err);
+  XK_LAUNCH();
+  k_labels_found<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_distinct, n_distinct, active,
+                                                        begin, end);
+  XK_LAUNCH();
+  // (6) reset the candidate ranks touched this step
+  k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
+      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, sel_best, sel_occ, err, 1);
+  XK_LAUNCH();
+  return XKNN_OK;
+}
+
+}  // namespace xknn

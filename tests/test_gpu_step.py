@@ -1,0 +1,89 @@
+"""One fc train step on device vs the oracle restatement of HybridSim::train_step's fc half
+(bit-exact with the reference, tests/test_oracle.py).
+
+FP32_EXACT: logits bit-identical (same summation order, no FMA); loss, weights, velocity and
+feature gradients within 1e-5 relative (CUDA expf vs glibc expf, NCCL/parallel reduction order).
+BF16: tensor-core GEMMs with bf16 operands; the stated bound is 2e-4 relative on the
+loss and 1e-2 relative (Frobenius) on the weight update and the feature gradient.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from gpu_util import make_layer, rel_err, torch_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(n, d, b, k, m, precision, steps=2, seed=42, lr=0.1, wd=0.0, check_logits=False):
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    rng = np.random.default_rng(n + b)
+    w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 3)
+    shards = [O.compress(g, 1, 0)]
+    layer = make_layer(n, d, 1, 0, m, b, w, g, precision=precision, seed=seed, wd=wd)
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    out = []
+    for step in range(steps):
+        x = rng.standard_normal((b, d)).astype(np.float32)
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        rc, loss_or, act, gf_or, logits_or = O.fc_train_step(w_or, v_or, x, lab, shards, m, seed,
+                                                             lr=lr, wd=wd,
+                                                             want_logits=check_logits)
+        assert rc == 0
+        gf = torch.empty(b, d, device="cuda")
+        loss = layer.train_step(torch.from_numpy(x).cuda(),
+                                torch.from_numpy(lab.view(np.int32)).cuda(), lr,
+                                grad_features_local=gf)
+        if check_logits:
+            lg = layer.last_logits(b)
+            assert lg.shape == logits_or.shape
+            if step == 0:  # identical inputs: identical fp32 logits (reference summation order)
+                assert np.array_equal(lg, logits_or), np.abs(lg - logits_or).max()
+            else:  # weights now carry the (tolerance-level) update difference
+                assert rel_err(lg, logits_or) <= 1e-5
+        out.append(dict(loss=loss, loss_or=loss_or, gf=gf.cpu().numpy(), gf_or=gf_or))
+    wg = layer.weights().cpu().numpy()
+    vg = layer.velocity().cpu().numpy()
+    layer.close()
+    return out, wg, w_or, vg, v_or, w
+
+
+@pytest.mark.parametrize("n,b,k,m", [(20_000, 128, 10, 2_000), (12_000, 64, 20, 500)])
+def test_step_fp32_exact(n, b, k, m):
+    import paper_2102_06025_b200 as X
+
+    out, wg, w_or, vg, v_or, w0 = _run(n, 512, b, k, m, X.PREC_FP32_EXACT, steps=3,
+                                       check_logits=True)
+    for o in out:
+        assert abs(o["loss"] - o["loss_or"]) <= 1e-5 * abs(o["loss_or"])
+        assert rel_err(o["gf"], o["gf_or"]) <= 1e-5
+    assert rel_err(wg - w0, w_or - w0) <= 1e-5  # the update itself
+    assert rel_err(vg, v_or) <= 1e-5
+    untouched = np.all(w_or == w0, axis=1)  # non-active rows unchanged
+    assert np.array_equal(wg[untouched], w0[untouched])
+
+
+def test_step_fp32_exact_weight_decay():
+    import paper_2102_06025_b200 as X
+
+    out, wg, w_or, vg, v_or, w0 = _run(8_000, 256, 32, 8, 800, X.PREC_FP32_EXACT, steps=2,
+                                       wd=1e-3)
+    assert rel_err(wg - w0, w_or - w0) <= 1e-5
+    for o in out:
+        assert abs(o["loss"] - o["loss_or"]) <= 1e-5 * abs(o["loss_or"])
+
+
+@pytest.mark.parametrize("n,b,k,m", [(100_000, 256, 10, 10_000), (20_000, 512, 10, 2_000)])
+def test_step_bf16(n, b, k, m):
+    import paper_2102_06025_b200 as X
+
+    out, wg, w_or, vg, v_or, w0 = _run(n, 512, b, k, m, X.PREC_BF16, steps=2)
+    for o in out:
+        assert abs(o["loss"] - o["loss_or"]) <= 2e-4 * abs(o["loss_or"]), (o["loss"], o["loss_or"])
+        assert rel_err(o["gf"], o["gf_or"]) <= 1e-2
+    assert rel_err(wg - w0, w_or - w0) <= 1e-2
+    untouched = np.all(w_or == w0, axis=1)
+    assert np.array_equal(wg[untouched], w0[untouched])
