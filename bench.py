@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""KNN-softmax fwd+bwd+update throughput on B200 (samples/s), driver contract of this repo.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|c4|c1] [--precision bf16|fp32]
+
+One step = the fc half of HybridSim::train_step (parallel.cpp:455-572, :638-668) over one global
+batch: feature/label all-gather, Algorithm-1 active-class selection, active-row gather +
+normalize, logit GEMM + distributed softmax-CE, weight- and feature-gradient GEMMs, feature
+normalize-backward, sparse momentum-SGD update of the active rows.
+
+Workloads (BASELINE.json configs, D = 512, M = 10% N, s = 30, lr = 0.1, mu = 0.9):
+    c1  N=100K  B=256   k=10    (the reference's CPU-runnable case; parity config)
+    c2  N=1M    B=1024  k=50    single B200 -- the default at N=1 (configs[1])
+    c3  N=10M   B=4096  k=100   class-sharded over 2/4/8 GPUs -- the default at N>1 (strong)
+    c4  N=100M  B=8192  k=100   8 GPUs (paper headline scale)
+Synthetic data: W ~ N(0, 0.05^2), features ~ N(0,1), labels uniform, a seeded self-first random
+graph of k neighbours per class (random-init W makes the true KNN graph statistically random).
+The per-step working set (weight shard, P~ of B x M_w bf16) exceeds the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": dict(n=100_000, b=256, k=10),
+    "c2": dict(n=1_000_000, b=1024, k=50),
+    "c3": dict(n=10_000_000, b=4096, k=100),
+    "c4": dict(n=100_000_000, b=8192, k=100),
+}
+D = 512
+SCALE, LR, MOMENTUM, SEED = 30.0, 0.1, 0.9, 42
+PHASES = ["allgather", "select", "gather_normalize", "gemm_logits_softmax", "softmax_stats",
+          "gemm_dW", "gemm_dX", "dX_reduce_scatter", "update", "feature_backward"]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------------------------
+class ClockSampler:
+    """SM clock and throttle reasons sampled through NVML every ~10 ms in a thread."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.mask = 0
+        self.maxclk = None
+        self._stop = None
+
+    def __enter__(self):
+        import threading
+
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.maxclk = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    self.mask |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    pass
+                self._stop.wait(0.01)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.maxclk, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.maxclk,
+                "reasons": sorted(k for k, v in self.REASONS.items() if self.mask & v),
+                "samples": len(self.samples), "source": "nvml, 10 ms"}
+
+
+# ----------------------------------------------------------------------------------------------
+# synthetic inputs
+# ----------------------------------------------------------------------------------------------
+def build_shard_graph(torch, n, k, p, rank, seed=7, chunk=1 << 20):
+    """This shard's CompressedKnnGraph (compress_graph, knn_graph.cpp:235-266) of a seeded
+    self-first random graph, generated chunk-wise on device identically on every rank."""
+    import paper_2102_06025_b200 as X
+
+    lo, hi = X.ShardLayout(n, p).class_range(rank)
+    kpc = torch.empty(n, dtype=torch.int32, device="cuda")
+    flats = []
+    g = torch.Generator(device="cuda")
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        g.manual_seed(seed * 1_000_003 + c0)
+        nb = torch.randint(0, n, (c1 - c0, k), device="cuda", dtype=torch.int32, generator=g)
+        nb[:, 0] = torch.arange(c0, c1, device="cuda", dtype=torch.int32)
+        mask = (nb >= lo) & (nb < hi)
+        kpc[c0:c1] = mask.sum(1, dtype=torch.int32)
+        flats.append(nb[mask])
+        del nb, mask
+    flat = torch.cat(flats)
+    del flats
+    off = torch.cumsum(kpc.to(torch.int64), 0) - kpc.to(torch.int64)
+    return kpc, off, flat
+
+
+def make_batches(torch, n, b_local, rank, count=4):
+    g = torch.Generator(device="cuda")
+    out = []
+    for i in range(count):
+        g.manual_seed(1000 + 31 * rank + i)
+        x = torch.randn(b_local, D, device="cuda", generator=g)
+        y = torch.randint(0, n, (b_local,), device="cuda", dtype=torch.int32, generator=g)
+        out.append((x, y))
+    return out
+
+
+# ----------------------------------------------------------------------------------------------
+# the reference (CPU) arm
+# ----------------------------------------------------------------------------------------------
+def reference_cpu(wl, steps, warmup, budget_s=150.0, log=print):
+    """The reference's stock HybridSim::train_step (kKnn) from oracle/_ref (compiled from the
+    unmodified reference sources), P = nproc worker threads (SimOptions::worker_threads, the
+    reference's only multi-core mechanism).  Falls back to the oracle port (1 thread)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    n, b_full, k = wl["n"], wl["b"], wl["k"]
+    m = max(1, int(math.ceil(0.1 * n)))
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(SEED)
+    w = (rng.standard_normal((n, D), dtype=np.float32) * np.float32(0.05)).astype(np.float32)
+    g = O.random_graph(n, k, 7)
+    kind = "reference" if O.ref_available() else "port"
+    p = cores if kind == "reference" else 1
+    while b_full % p:
+        p -= 1
+    shards = [O.compress(g, p, s) for s in range(p)]
+    del g
+
+    def batch(bs, i):
+        r = np.random.default_rng(100 + i)
+        return (r.standard_normal((bs, D), dtype=np.float32),
+                r.integers(0, n, bs).astype(np.uint32))
+
+    if kind == "reference":
+        sim = O.RefSim(w, p, threads=True, scale=SCALE, momentum=MOMENTUM)
+        sim.set_graphs(shards)
+
+        def one(bs, i):
+            x, y = batch(bs, i)
+            t = time.perf_counter()
+            rc, loss, _ = sim.step(x, y, m, SEED, LR, reset_fe=False)
+            assert rc == 0, rc
+            return time.perf_counter() - t
+    else:
+        vel = np.zeros_like(w)
+
+        def one(bs, i):
+            x, y = batch(bs, i)
+            t = time.perf_counter()
+            rc, *_ = O.fc_train_step(w, vel, x, y, shards, m, SEED, SCALE, LR, MOMENTUM, 0.0)
+            assert rc == 0, rc
+            return time.perf_counter() - t
+
+    # bounded sample: the full global batch if the run fits the budget, else a sub-batch
+    bs = b_full
+    t0 = one(bs, 0)  # also the velocity-allocating first step
+    total = steps + max(warmup - 1, 0)
+    while t0 * total > budget_s and bs // 2 >= 16 and (bs // 2) % p == 0:
+        bs //= 2
+        t0 = one(bs, 1)
+    for i in range(max(warmup - 1, 0)):
+        one(bs, 2 + i)
+    times = [one(bs, 100 + i) for i in range(steps)]
+    med = float(np.median(times))
+    return dict(value=bs / med, unit="samples/s", cores=p if kind == "reference" else 1,
+                kind=kind,
+                sample=(f"{'HybridSim::train_step(kKnn)' if kind == 'reference' else 'oracle port'}"
+                        f" at N={n}, k={k}, M={m}, D={D}, batch {bs} of {b_full}, P={p} worker "
+                        f"threads, median of {steps} steps on {cores} host cores"),
+                ms_per_step=med * 1e3)
+
+
+# ----------------------------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------------------------
+def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
+    import torch
+
+    import paper_2102_06025_b200 as X
+
+    torch.cuda.set_device(local_rank)
+    n, b, k = wl["n"], wl["b"], wl["k"]
+    m = max(1, int(math.ceil(0.1 * n)))
+    b_local = b // world
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(X.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = X.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+    prec = X.PREC_BF16 if args.precision == "bf16" else X.PREC_FP32_EXACT
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        layer = X.KnnSoftmaxLayer(n, D, rank=rank, world=world, m_active=m, max_batch=b,
+                                  scale=SCALE, momentum=MOMENTUM, rng_seed=SEED, precision=prec,
+                                  comm=comm, stream=stream)
+        gw = torch.Generator(device="cuda")
+        gw.manual_seed(10 + rank)
+        wv = layer.weights_view().tensor
+        for r0 in range(0, wv.shape[0], 1 << 20):
+            wv[r0:r0 + (1 << 20)].normal_(0.0, 0.05, generator=gw)
+        kpc, off, flat = build_shard_graph(torch, n, k, world, rank)
+        layer.set_shard_graph(kpc, off, flat)
+        del kpc, off, flat
+        batches = make_batches(torch, n, b_local, rank)
+        gfeat = torch.empty(b_local, D, device="cuda")
+        loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(i):
+        x, y = batches[i % len(batches)]
+        with torch.cuda.stream(stream):
+            layer.train_step(x, y, LR, grad_features_local=gfeat, loss_out=loss, sync=False)
+
+    for i in range(args.warmup):
+        step(i)
+    layer.sync()
+    barrier()
+    clk = ClockSampler(local_rank)
+    clk.__enter__()  # NVML sampling during the timed region
+
+    # ---- timed region (device time, CUDA events on the layer stream) ----
+    layer_launch0 = layer.kernel_launches
+    X.lib().xknn_layer_profile(layer.h, 1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if True:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    clk.__exit__(None, None, None)
+    ms = ev0.elapsed_time(ev1)
+    launches = layer.kernel_launches - layer_launch0
+    import ctypes as C
+
+    ph = (C.c_double * len(PHASES))()
+    nsteps = C.c_uint64()
+    X.lib().xknn_layer_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int,
+                                            C.POINTER(C.c_uint64)]
+    X.lib().xknn_layer_phase_ms(layer.h, ph, len(PHASES), C.byref(nsteps))
+    X.lib().xknn_layer_profile(layer.h, 0)
+    phase_ms = {PHASES[i]: ph[i] / max(nsteps.value, 1) for i in range(len(PHASES))}
+    layer.sync()
+    active_total, active_local = layer.last_active()
+    loss_v = float(loss.item())
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region ----
+    hx = [bt[0].cpu().pin_memory() for bt in batches]
+    hy = [bt[1].cpu().pin_memory() for bt in batches]
+    dx = torch.empty(b_local, D, device="cuda")
+    dy = torch.empty(b_local, dtype=torch.int32, device="cuda")
+    hloss = torch.zeros(1, dtype=torch.float64).pin_memory()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_ev0 = torch.cuda.Event(enable_timing=True)
+    e2e_ev1 = torch.cuda.Event(enable_timing=True)
+    e2e_ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            dx.copy_(hx[i % len(hx)], non_blocking=True)
+            dy.copy_(hy[i % len(hy)], non_blocking=True)
+            layer.train_step(dx, dy, LR, grad_features_local=gfeat, loss_out=loss, sync=False)
+            hloss.copy_(loss, non_blocking=True)
+            stream.synchronize()  # the caller reads the step's loss
+    e2e_ev1.record(stream)
+    e2e_ev1.synchronize()
+    barrier()
+    e2e_ms = e2e_ev0.elapsed_time(e2e_ev1)
+    layer.sync()
+
+    # ---- max over ranks ----
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), float(t[1])
+        tg = torch.tensor([float(active_local)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        mw_max = int(tg.item())
+    else:
+        mw_max = active_local
+
+    res = None
+    if rank == 0:
+        ms_step = ms / args.steps
+        value = b / (ms_step / 1e3)
+        hbm, tf_burst, tf_sus, pk_src = peaks()
+        gemms = {k_: phase_ms[k_] for k_ in ("gemm_logits_softmax", "gemm_dW", "gemm_dX")}
+        dom = max(gemms, key=gemms.get)
+        if args.precision == "bf16":
+            flops = 2.0 * (((b + 127) // 128) * 128) * active_local * D  # per launch, algorithmic
+            achieved = flops / (gemms[dom] / 1e3) / 1e12
+            traffic = None
+            tp = os.path.join(ROOT, "profiles", f"traffic_{wl_name}.json")
+            if os.path.exists(tp):
+                try:
+                    traffic = json.load(open(tp)).get(dom)
+                except Exception:
+                    traffic = None
+            roof = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 2),
+                    "peak": tf_sus, "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4),
+                    "traffic": traffic, "peak_source": f"{pk_src} bf16 sustained",
+                    "flops_per_launch": flops, "launch_ms": round(gemms[dom], 4)}
+        else:
+            roof = {"bound": "tensor", "kernel": dom, "achieved": None, "peak": tf_sus,
+                    "unit": "TFLOP/s", "frac": None, "traffic": None}
+        # whole-step roofline: max(6 B M_w D / Pi, 16 M_w D / beta)
+        t_roof = max(6.0 * b * mw_max * D / (tf_sus * 1e12), 16.0 * mw_max * D / (hbm * 1e9))
+        clocks = clk.summary()
+        res = {
+            "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
+                      "B200 vs roofline",
+            "value": round(value, 1),
+            "unit": "samples/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None,
+            "dtype": "bf16" if args.precision == "bf16" else "f32",
+            "data": "synthetic (W~N(0,0.05^2), X~N(0,1), uniform labels, seeded random "
+                    "self-first k-NN graph)",
+            "config": {"workload": wl_name, "num_classes": n, "dim": D, "global_batch": b,
+                       "k": k, "m_active": m, "active_per_shard": active_local,
+                       "scale": SCALE, "parallelism": f"class-sharded mp{world}",
+                       "l2": "per-step working set > 126 MB L2 (weight shard, P~ bf16)"},
+            "e2e": {"value": round(b / (e2e_ms / args.steps / 1e3), 1), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(b_local * D * 4 + b_local * 4),
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4),
+                              "frac": round(t_roof * 1e3 / ms_step, 4)},
+            "phase_ms": {k_: round(v, 4) for k_, v in phase_ms.items()},
+            "clocks": clocks,
+            "loss": loss_v,
+            "active_classes": int(active_total),
+        }
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    wl_name = args.workload or ("c2" if world == 1 else "c3")
+    wl = WORKLOADS[wl_name]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = reference_cpu(wl, args.steps, args.warmup)
+        print(json.dumps({
+            "impl": "reference",
+            "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
+                      "B200 vs roofline",
+            "value": round(r["value"], 3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_step"], 2),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl_name, "num_classes": wl["n"], "dim": D,
+                       "global_batch": wl["b"], "k": wl["k"]},
+            "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": round(r["value"], 3), "unit": "samples/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, wl_name, wl, rank, world, local_rank, dist)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline and wl_name in ("c1", "c2"):
+            try:
+                r = reference_cpu(wl, 1, 1, budget_s=40.0)
+                res["cpu_baseline"] = {k_: r[k_] for k_ in ("value", "unit", "cores", "kind",
+                                                            "sample")}
+                res["cpu_baseline"]["value"] = round(res["cpu_baseline"]["value"], 3)
+            except Exception as e:  # the baseline is reported, never required
+                res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        else:
+            res["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": 0,
+                                   "kind": "reference",
+                                   "sample": "not run: reference needs >80 GB host RAM and "
+                                             "~10 min/step beyond c2 (SURVEY 7.7)"}
+        print(json.dumps(res), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

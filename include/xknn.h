@@ -64,8 +64,15 @@ typedef struct {
   uint64_t rng_seed;     /* SelectionConfig::rng_seed (knn_softmax.hpp:28)                   */
   uint64_t max_batch;    /* largest global batch B a step will see (sizes scratch)           */
   int32_t precision;     /* xknn_precision_t                                                 */
-  int32_t reserved;
+  int32_t flags;         /* XKNN_FLAG_*                                                      */
 } xknn_config_t;
+
+/* The step's device work (selection .. update) is captured once per batch size into a CUDA
+   graph and replayed; this flag launches it kernel by kernel instead. */
+#define XKNN_FLAG_NO_GRAPH 1
+/* BF16: apply the normalize-backward + momentum-SGD update inside the weight-gradient GEMM's
+   epilogue instead of a separate row kernel (experimental). */
+#define XKNN_FLAG_FUSED_UPDATE 2
 
 typedef struct xknn_layer xknn_layer_t;
 
@@ -149,6 +156,17 @@ xknn_status_t xknn_layer_last_active(xknn_layer_t* h, uint64_t* active_global,
 /* Copies the last step's logits (B x active_local, fp32) -- FP32_EXACT precision only; for
    parity tests of the logit GEMM (matmul(f_hat, w_sub, T) * scale, parallel.cpp:550-551). */
 xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out_host, uint64_t capacity);
+
+/* Phase profiler.  xknn_layer_profile(h, 1) resets and starts recording CUDA events on the
+   layer stream at the phase boundaries of every step (asynchronous; no extra syncs in the step
+   loop); xknn_layer_phase_ms returns the accumulated milliseconds per phase over the recorded
+   steps (synchronizes; with the CUDA-graph step, the phases of the last step):
+   0 feature/label all-gather, 1 selection, 2 operand normalize/gather, 3 logit GEMM (+ fused
+   softmax epilogue in BF16), 4 softmax statistics + all-reduce + loss, 5 weight-gradient GEMM,
+   6 feature-gradient GEMM, 7 feature-gradient reduce(-scatter), 8 normalize-backward +
+   momentum-SGD row update, 9 feature normalize-backward. */
+xknn_status_t xknn_layer_profile(xknn_layer_t* h, int enable);
+xknn_status_t xknn_layer_phase_ms(xknn_layer_t* h, double* out_ms, int n, uint64_t* steps);
 
 /* Kernel launch counter (all kernels this library launched on this layer since creation). */
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);

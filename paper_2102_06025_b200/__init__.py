@@ -28,13 +28,14 @@ VP = C.c_void_p
 
 PREC_BF16 = 0
 PREC_FP32_EXACT = 1
+FLAG_NO_GRAPH = 1
 
 
 class XknnConfig(C.Structure):
     """xknn_config_t (include/xknn.h) == SimOptions + SelectionConfig of the reference."""
     _fields_ = [("scale", C.c_float), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("m_active", U64), ("rng_seed", U64), ("max_batch", U64),
-                ("precision", C.c_int32), ("reserved", C.c_int32)]
+                ("precision", C.c_int32), ("flags", C.c_int32)]
 
 
 # ---- errors.hpp:10-54 -------------------------------------------------------------------------
@@ -164,14 +165,16 @@ class KnnSoftmaxLayer:
     def __init__(self, num_classes: int, dim: int, *, rank: int = 0, world: int = 1,
                  m_active: int, max_batch: int, scale: float = 30.0, momentum: float = 0.9,
                  weight_decay: float = 0.0, rng_seed: int = 0, precision: int = PREC_BF16,
-                 comm=None, stream=None):
+                 comm=None, stream=None, use_graph: bool = True):
         import torch  # plumbing only: device memory and streams
 
         self._torch = torch
         self.num_classes, self.dim, self.rank, self.world = num_classes, dim, rank, world
         self.cfg = XknnConfig(scale, momentum, weight_decay, m_active, rng_seed, max_batch,
-                              precision, 0)
-        self.stream = stream if stream is not None else torch.cuda.current_stream()
+                              precision, 0 if use_graph else FLAG_NO_GRAPH)
+        # the layer works on its own stream (capturable into a CUDA graph); every call is
+        # ordered after the caller's current stream and the caller's stream after it
+        self.stream = stream if stream is not None else torch.cuda.Stream()
         h = VP()
         _check(_lib.xknn_layer_create(rank, world, num_classes, dim, C.byref(self.cfg),
                                       comm, self.stream.cuda_stream, C.byref(h)))
@@ -180,6 +183,16 @@ class KnnSoftmaxLayer:
         _check(_lib.xknn_layer_shard(self.h, C.byref(b), C.byref(e)))
         self.begin, self.end = b.value, e.value
         self._loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def _enter(self):
+        cur = self._torch.cuda.current_stream()
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+
+    def _leave(self):
+        cur = self._torch.cuda.current_stream()
+        if cur != self.stream:
+            cur.wait_stream(self.stream)
 
     # -- state ----------------------------------------------------------------------------------
     @property
@@ -190,18 +203,23 @@ class KnnSoftmaxLayer:
         """HybridSim::load_model for this shard: w is (shard_rows, dim) fp32."""
         assert w.shape == (self.shard_rows, self.dim) and w.dtype == self._torch.float32
         w = w.contiguous()
+        self._enter()
         _check(_lib.xknn_layer_set_weights(self.h, w.data_ptr(), int(w.is_cuda)))
 
     def weights(self):
         out = self._torch.empty(self.shard_rows, self.dim, dtype=self._torch.float32,
                                 device="cuda")
+        self._enter()
         _check(_lib.xknn_layer_get_weights(self.h, out.data_ptr(), 1))
+        self._leave()
         return out
 
     def velocity(self):
         out = self._torch.empty(self.shard_rows, self.dim, dtype=self._torch.float32,
                                 device="cuda")
+        self._enter()
         _check(_lib.xknn_layer_get_velocity(self.h, out.data_ptr(), 1))
+        self._leave()
         return out
 
     def weights_view(self):
@@ -216,6 +234,7 @@ class KnnSoftmaxLayer:
         kpc = k_per_class.contiguous()
         off = offsets.contiguous()
         fl = flat.contiguous()
+        self._enter()
         _check(_lib.xknn_layer_set_graph_csr(self.h, kpc.data_ptr(), off.data_ptr(),
                                              fl.data_ptr() if fl.numel() else 0, fl.numel(), dev))
 
@@ -228,8 +247,10 @@ class KnnSoftmaxLayer:
         cnt = U64()
         ca = C.c_int()
         lab = labels.to(torch.int32).contiguous()
+        self._enter()
         _check(_lib.xknn_select(self.h, lab.data_ptr(), lab.numel(), out.data_ptr(), C.byref(cnt),
                                 C.byref(ca)))
+        self._leave()
         return out[: cnt.value].clone(), bool(ca.value)
 
     def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
@@ -240,9 +261,11 @@ class KnnSoftmaxLayer:
         assert features_local.dtype == torch.float32 and features_local.is_contiguous()
         lab = labels_local if labels_local.dtype == torch.int32 else labels_local.to(torch.int32)
         loss = self._loss if loss_out is None else loss_out
+        self._enter()
         _check(_lib.xknn_step(self.h, features_local.data_ptr(), lab.data_ptr(),
                               features_local.shape[0], float(lr), loss.data_ptr(),
                               _ptr(grad_features_local)))
+        self._leave()
         if sync:
             _check(_lib.xknn_layer_sync(self.h))
             return float(loss.item())

@@ -39,6 +39,12 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* v, uint32_t 
   return lo;
 }
 
+template <typename T>
+inline cudaError_t dalloc(T** p, uint64_t count) {
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
   uint64_t g = (n + block - 1) / block;
   if (g == 0) g = 1;

@@ -1,13 +1,661 @@
-// fast.cu -- XKNN_PREC_BF16 path (tcgen05/TMEM/TMA GEMMs with fused softmax epilogues).
+// fast.cu -- XKNN_PREC_BF16: the three fc GEMMs on 5th-gen tensor cores (tcgen05.mma,
+// accumulators in TMEM, operands staged by TMA into 128B/64B-swizzled shared memory), with the
+// softmax fused into the forward epilogue so logits never reach HBM.
+//
+// Forward (parallel.cpp:550-557, the logits GEMM + softmax statistics):
+//   GEMM-F   S = X_hat * W_subᵀ   (M = 128 batch rows, N = 256 classes, K = D)
+//            epilogue: P~ = exp(s*S - s) -> bf16 (B x M_w), per-tile row sums, label logit.
+//            A fixed stabiliser c = s replaces the row max: |cosine| <= 1 bounds every logit
+//            to [-s, s], so exp(s*S - s) lies in [e^-2s, 1] (fp32-safe for s <= 40).
+// Backward, with r_b = 1 / (B * sum_b) and P~' = P~ minus sum_b at the label column
+// (so G = r * P~' reproduces softmax - onehot over m, parallel.cpp:168-186, exactly):
+//   GEMM-dW  dW  = P~'ᵀ * (diag(s*r) X_hat)    (M = 128 classes, N = 512, K = B) -> fp32
+//   GEMM-dX  dX  = diag(s*r) * (P~' * W_sub)   (M = 128 batch, N = 512, K = M_w split) -> fp32
+// Warp roles (384 threads, one CTA per SM, persistent over tiles): warp 0 TMA producer,
+// warp 1 MMA issuer (one thread), warp 2 TMEM allocator, warps 4-11 epilogue (TMEM -> regs).
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
+#include "tc.cuh"
 
 namespace xknn {
 
-xknn_status_t Layer::init_fast() { return XKNN_OK; }
-void Layer::free_fast() {}
-xknn_status_t Layer::run_fast_core(uint64_t) {
-  last_msg = "bf16 path not built yet";
-  return XKNN_ERR_UNSUPPORTED;
+namespace {
+
+enum Kind : int { kF = 0, kDX = 1, kDW = 2 };
+
+template <int KIND>
+struct Cfg;
+template <>
+struct Cfg<kF> {
+  static constexpr uint32_t BK = 64, STAGES = 4;
+  static constexpr uint32_t A_BYTES = 128 * 64 * 2, B_BYTES = 256 * 64 * 2;
+  static constexpr uint32_t NBUF = 2, ACC = 256;
+};
+template <>
+struct Cfg<kDX> {
+  static constexpr uint32_t BK = 32, STAGES = 5;
+  static constexpr uint32_t A_BYTES = 128 * 32 * 2, B_BYTES = 512 * 32 * 2;
+  static constexpr uint32_t NBUF = 1, ACC = 512;
+};
+template <>
+struct Cfg<kDW> {
+  static constexpr uint32_t BK = 32, STAGES = 5;
+  static constexpr uint32_t A_BYTES = 128 * 32 * 2, B_BYTES = 512 * 32 * 2;
+  static constexpr uint32_t NBUF = 1, ACC = 512;
+};
+
+template <int KIND>
+constexpr uint32_t smem_bytes() {
+  return Cfg<KIND>::STAGES * (Cfg<KIND>::A_BYTES + Cfg<KIND>::B_BYTES) + 1024 + 256 + 2048;
+}
+
+__device__ __forceinline__ void epilogue_bar() {  // the 8 epilogue warps only
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+struct GemmArgs {
+  const SelState* st;
+  uint32_t B, bpad, nbt, splits, dim;
+  float scale;
+  const int32_t* label_col;
+  __nv_bfloat16* Pt;
+  uint64_t ldp;
+  float* partial;
+  float* labelterm;
+  float* out;
+  // GEMM-dW fused update (normalize-backward + SgdMomentum::step_rows) -- out == nullptr
+  float* W;
+  float* V;
+  const uint32_t* active;
+  uint64_t begin;
+  const float* wnorm;
+  const float* lr;
+  float mu, wd;
+  const unsigned long long* err;
+};
+
+struct Tile {
+  uint32_t a_row, b_row;  // meaning depends on KIND
+  uint32_t k0, nk;
+  uint32_t id;
+};
+
+template <int KIND>
+__device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a, uint32_t mw) {
+  if (KIND == kF) return a.nbt * ((mw + 255) / 256);
+  if (KIND == kDX) return a.nbt * a.splits;
+  return (mw + 127) / 128;
+}
+
+template <int KIND>
+__device__ __forceinline__ Tile tile_of(const GemmArgs& a, uint32_t mw, uint32_t t) {
+  Tile x{};
+  x.id = t;
+  if (KIND == kF) {  // consecutive tiles share the class tile: W_sub streamed once through L2
+    x.a_row = (t % a.nbt) * 128;
+    x.b_row = (t / a.nbt) * 256;
+    x.k0 = 0;
+    x.nk = a.dim / 64;
+  } else if (KIND == kDX) {
+    const uint32_t nkc = (mw + 31) / 32;
+    const uint32_t per = (nkc + a.splits - 1) / a.splits;
+    const uint32_t s = t / a.nbt;
+    x.a_row = (t % a.nbt) * 128;
+    x.k0 = s * per;
+    const uint32_t k1 = min(nkc, x.k0 + per);
+    x.nk = k1 > x.k0 ? k1 - x.k0 : 0;
+  } else {
+    x.a_row = t * 128;  // class tile
+    x.k0 = 0;
+    x.nk = a.bpad / 32;
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(384, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           GemmArgs a) {
+  using C = Cfg<KIND>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  double* xdot = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [2][128]
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (uint32_t s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (uint32_t s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 8);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+  }
+  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  const uint32_t mw = a.st->active_count;
+  const uint32_t ntiles = num_tiles<KIND>(a, mw);
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile x = tile_of<KIND>(a, mw, t);
+        for (uint32_t k = 0; k < x.nk; ++k) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          uint8_t* dA = sA + stage * C::A_BYTES;
+          uint8_t* dB = sB + stage * C::B_BYTES;
+          const int32_t kk = (int32_t)((x.k0 + k) * C::BK);
+          if (KIND == kF) {
+            tc::tma_load_2d(dA, &tmA, &full[stage], kk, (int32_t)x.a_row);
+            tc::tma_load_2d(dB, &tmB, &full[stage], kk, (int32_t)x.b_row);
+          } else if (KIND == kDX) {
+            tc::tma_load_2d(dA, &tmA, &full[stage], kk, (int32_t)x.a_row);  // P~ [b][class]
+#pragma unroll
+            for (int j = 0; j < 8; ++j)  // W_sub [class][d], 64-wide d atoms
+              tc::tma_load_2d(dB + j * 4096, &tmB, &full[stage], j * 64, kk);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)  // P~ᵀ: class atoms of 64 at batch rows kk..kk+31
+              tc::tma_load_2d(dA + j * 4096, &tmA, &full[stage], (int32_t)x.a_row + j * 64, kk);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)  // X_hat' [b][d]
+              tc::tma_load_2d(dB + j * 4096, &tmB, &full[stage], j * 64, kk);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile x = tile_of<KIND>(a, mw, t);
+        tc::mbar_wait(&tempty[buf], tphase ^ 1);
+        tc::fence_after_sync();
+        const uint32_t dcol = tbase + buf * C::ACC;
+        for (uint32_t k = 0; k < x.nk; ++k) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::fence_after_sync();
+          const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = tc::smem_u32(sB + stage * C::B_BYTES);
+          if (KIND == kF) {
+            constexpr uint32_t id = tc::idesc_bf16(128, 256, false, false);
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              const uint64_t da = tc::smem_desc(a0 + kk * 32, 16, 1024, tc::kSwizzle128);
+              const uint64_t db = tc::smem_desc(b0 + kk * 32, 16, 1024, tc::kSwizzle128);
+              tc::mma_bf16(dcol, da, db, id, (k | kk) != 0);
+            }
+          } else {
+            constexpr uint32_t id = tc::idesc_bf16(128, 256, KIND == kDW, true);
+#pragma unroll
+            for (uint32_t kk = 0; kk < 2; ++kk) {
+              const uint64_t da = KIND == kDX
+                                      ? tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64)
+                                      : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+#pragma unroll
+              for (uint32_t nh = 0; nh < 2; ++nh) {
+                const uint64_t db =
+                    tc::smem_desc(b0 + nh * 16384 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                tc::mma_bf16(dcol + nh * 256, da, db, id, (k | kk) != 0);
+              }
+            }
+          }
+          tc::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (x.nk) tc::mma_commit(&tfull[buf]);
+        else tc::mbar_arrive(&tfull[buf]);
+        if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue: TMEM -> registers -> HBM =================
+    const uint32_t q = warp & 3;          // TMEM lane quadrant this warp may access
+    const uint32_t h = (warp - 4) >> 2;   // column half
+    const uint32_t row = q * 32 + lane;
+    const uint32_t lane_addr = (q * 32) << 16;
+    uint32_t buf = 0, tphase = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const Tile x = tile_of<KIND>(a, mw, t);
+      tc::mbar_wait(&tfull[buf], tphase);
+      tc::fence_after_sync();
+      const uint32_t tb = tbase + buf * C::ACC + lane_addr;
+      if (KIND == kF) {
+        const uint32_t b = x.a_row + row;
+        const bool vrow = b < a.B;
+        const int32_t lc = vrow ? a.label_col[b] : -1;
+        const float k2 = a.scale * 1.4426950408889634f;
+        float sum = 0.f, lab = 0.f;
+        bool has = false;
+#pragma unroll 1
+        for (uint32_t ch = 0; ch < 4; ++ch) {
+          const uint32_t col = h * 128 + ch * 32;
+          float v[32];
+          tc::tmem_ld32(tb + col, v);
+          const uint32_t c0 = x.b_row + col;
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float e[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t c = c0 + j + u;
+              const bool ok = vrow && c < mw;
+              e[u] = ok ? exp2f(fmaf(v[j + u], k2, -k2)) : 0.f;
+              sum += e[u];
+              if ((int32_t)c == lc) { lab = v[j + u] * a.scale; has = true; }
+            }
+            pk[j / 2] = pack_bf16(e[0], e[1]);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(a.Pt + (uint64_t)b * a.ldp + c0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        const uint32_t ct = x.b_row / 256;
+        a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
+        if (has) a.labelterm[b] = lab - a.scale;
+      } else if (KIND == kDW && a.out == nullptr) {
+        // dW tile stays in TMEM: normalize-backward through the cached row norm, then momentum
+        // SGD on the weight and velocity rows (parallel.cpp:653-667, fccs.cpp:74-89), per
+        // active row.  The two column halves of a row meet through shared memory for the dot.
+        const uint32_t c = x.a_row + row;
+        const bool valid = c < mw && *a.err == 0;
+        const uint64_t grow = valid ? (uint64_t)a.active[c] - a.begin : 0;
+        float* wrow = a.W + grow * 512;
+        float* vrow = a.V + grow * 512;
+        const float norm = valid ? a.wnorm[c] : 1.f;
+        const float inv = 1.0f / norm;
+        double dot = 0.0;
+#pragma unroll 1
+        for (uint32_t ch = 0; ch < 8; ++ch) {
+          const uint32_t col = h * 256 + ch * 32;
+          float g[32];
+          tc::tmem_ld32(tb + col, g);
+          if (valid) {
+            const float4* w4 = reinterpret_cast<const float4*>(wrow + col);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float4 w = w4[u];
+              dot += (double)g[4 * u + 0] * __fmul_rn(w.x, inv);
+              dot += (double)g[4 * u + 1] * __fmul_rn(w.y, inv);
+              dot += (double)g[4 * u + 2] * __fmul_rn(w.z, inv);
+              dot += (double)g[4 * u + 3] * __fmul_rn(w.w, inv);
+            }
+          }
+        }
+        double* xd = xdot;  // one buffer: the barrier pair keeps tiles apart
+        xd[h * 128 + row] = dot;
+        epilogue_bar();
+        const float dd = (float)(xd[row] + xd[128 + row]);
+        epilogue_bar();
+        const float lr = *a.lr, mu = a.mu, wd = a.wd;
+#pragma unroll 1
+        for (uint32_t ch = 0; ch < 8; ++ch) {
+          const uint32_t col = h * 256 + ch * 32;
+          float g[32];
+          tc::tmem_ld32(tb + col, g);
+          if (valid) {
+            float4* w4 = reinterpret_cast<float4*>(wrow + col);
+            float4* v4 = reinterpret_cast<float4*>(vrow + col);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float4 w = w4[u], v = v4[u];
+              float gr, vv;
+#define XKNN_UPD(comp, j)                                                                     \
+  gr = __fmul_rn(__fsub_rn(g[4 * u + j], __fmul_rn(dd, __fmul_rn(w.comp, inv))), inv);      \
+  vv = __fadd_rn(__fadd_rn(__fmul_rn(mu, v.comp), gr), __fmul_rn(wd, w.comp));              \
+  v.comp = vv;                                                                                \
+  w.comp = __fsub_rn(w.comp, __fmul_rn(lr, vv));
+              XKNN_UPD(x, 0) XKNN_UPD(y, 1) XKNN_UPD(z, 2) XKNN_UPD(w, 3)
+#undef XKNN_UPD
+              w4[u] = w;
+              v4[u] = v;
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+      } else {
+        // dX: split-K partial rows (128 x 512 fp32);  dW: dW rows of this class tile
+        float* dst_row;
+        bool valid;
+        if (KIND == kDX) {
+          dst_row = a.partial + ((uint64_t)x.id * 128 + row) * 512;
+          valid = true;
+        } else {
+          const uint32_t c = x.a_row + row;
+          dst_row = a.out + (uint64_t)c * 512;
+          valid = c < mw;
+        }
+#pragma unroll 1
+        for (uint32_t ch = 0; ch < 8; ++ch) {
+          const uint32_t col = h * 256 + ch * 32;
+          float v[32];
+          if (x.nk) {
+            tc::tmem_ld32(tb + col, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          }
+          if (valid) {
+            float4* d4 = reinterpret_cast<float4*>(dst_row + col);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              d4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+      }
+      if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tbase);
+  }
+}
+
+// ---- small fused kernels of the fast path ---------------------------------------------------
+
+// per-row softmax statistics from the GEMM-F tile partials: 32 rows x 32 tile groups per block,
+// each thread sums its tile group in order, then a fixed-order combine (deterministic)
+__global__ void k_rowreduce(const SelState* st, const float* __restrict__ partial,
+                            const float* __restrict__ labelterm, const int32_t* __restrict__ lcol,
+                            uint32_t B, uint32_t bpad, double* __restrict__ red) {
+  __shared__ double part[32][33];
+  const uint32_t nt = 2 * ((st->active_count + 255) / 256);
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // row in block, tile group
+  const uint32_t b = blockIdx.x * 32 + tx;
+  double s = 0.0;
+  if (b < B)
+    for (uint32_t t = ty; t < nt; t += 32) s += (double)partial[(uint64_t)t * bpad + b];
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && b < B) {
+    double tot = 0.0;
+    for (int g = 0; g < 32; ++g) tot += part[g][tx];
+    const int32_t c = lcol[b];
+    red[b] = tot;
+    red[B + b] = c >= 0 ? (double)labelterm[b] : 0.0;
+    red[2 * B + b] = c >= 0 ? 1.0 : 0.0;
+  }
+}
+
+// P~' = P~ - sum at the label column; X_hat' = bf16(x_hat * s / (B * sum)); pad rows zeroed
+template <int DV>
+__global__ void k_fixup(const double* __restrict__ red, const int32_t* __restrict__ lcol,
+                        const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
+                        uint32_t bpad, uint32_t d, float scale, __nv_bfloat16* __restrict__ Pt,
+                        uint64_t ldp, __nv_bfloat16* __restrict__ Xs) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < bpad;
+       b += (gridDim.x * blockDim.x) >> 5) {
+    uint2* dst = reinterpret_cast<uint2*>(Xs + (uint64_t)b * d);
+    if (b >= B) {
+#pragma unroll
+      for (int c = 0; c < DV; ++c) dst[lane + 32 * c] = make_uint2(0, 0);
+      continue;
+    }
+    const double denom = red[b];
+    const int32_t lc = lcol[b];
+    if (lane == 0 && lc >= 0) {
+      __nv_bfloat16* p = Pt + (uint64_t)b * ldp + lc;
+      *p = __float2bfloat16_rn(__bfloat162float(*p) - (float)denom);
+    }
+    const float inv = 1.0f / xnorm[b];
+    const float rs = (float)((double)scale / ((double)B * denom));
+    const float4* xp = reinterpret_cast<const float4*>(X + (uint64_t)b * d);
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
+      const float4 x = xp[lane + 32 * c];
+      dst[lane + 32 * c] = make_uint2(pack_bf16(__fmul_rn(x.x, inv) * rs, __fmul_rn(x.y, inv) * rs),
+                                      pack_bf16(__fmul_rn(x.z, inv) * rs, __fmul_rn(x.w, inv) * rs));
+    }
+  }
+}
+
+// dX[b][:] = s * r_b * sum_s partial[s][b][:] (fixed split order)
+__global__ void k_dx_reduce(const float* __restrict__ partial, const double* __restrict__ red,
+                            uint32_t B, uint32_t nbt, uint32_t splits, float scale,
+                            float* __restrict__ out) {
+  const uint64_t total = (uint64_t)B * 128;  // float4 units (D = 512)
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)(e / 128), c4 = (uint32_t)(e % 128);
+    const uint32_t bt = b / 128, row = b % 128;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t s = 0; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(
+          partial + ((uint64_t)(s * nbt + bt) * 128 + row) * 512)[c4];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const float rs = (float)((double)scale / ((double)B * red[b]));
+    reinterpret_cast<float4*>(out + (uint64_t)b * 512)[c4] =
+        make_float4(acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs);
+  }
+}
+
+__global__ void k_zero_rows_bf16(const SelState* st, __nv_bfloat16* W16, uint32_t cap_rows,
+                                 uint32_t d) {
+  // rows [count, round_up(count, 256)) of W_sub must be zero for the K loop of GEMM-dX
+  const uint32_t c = st->active_count;
+  const uint32_t e = min(cap_rows, (c + 255) / 256 * 256);
+  const uint64_t n = (uint64_t)(e - c) * d / 8;
+  uint4* p = reinterpret_cast<uint4*>(W16 + (uint64_t)c * d);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
+// ---- host-side tensor maps ------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct FastState {
+  uint32_t bpad = 0, nbt = 0, mwpad = 0, splits = 0;
+  float* partial_f = nullptr;   // [2 * mwpad/256][bpad]
+  float* labelterm = nullptr;   // [bpad]
+  float* partial_dx = nullptr;  // [nbt * splits][128][512]
+  CUtensorMap mF_A, mF_B, mDX_A, mDX_B, mDW_A, mDW_B;
+};
+
+xknn_status_t Layer::init_fast() {
+  auto* f = new FastState;
+  fast = f;
+  if (d != 512) return fail_msg(XKNN_ERR_UNSUPPORTED, "BF16 path is specialised for D = 512");
+  f->bpad = (uint32_t)((bmax + 127) / 128 * 128);
+  f->nbt = f->bpad / 128;
+  f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
+  ldp = f->mwpad;
+  // split-K of GEMM-dX: enough (batch tile, class range) units to fill the SMs in whole waves
+  {
+    uint32_t best = 1;
+    double best_eff = 0;
+    for (uint32_t s = 1; s <= 64; ++s) {
+      const uint32_t units = f->nbt * s;
+      const double eff = (double)units / (((units + kNumSMs - 1) / kNumSMs) * kNumSMs);
+      if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+      if (units >= 2 * kNumSMs) break;
+    }
+    f->splits = best;
+  }
+  XK_CUDA(dalloc(&Xhat16, (uint64_t)f->bpad * d));
+  XK_CUDA(dalloc(&Xs16, (uint64_t)f->bpad * d));
+  XK_CUDA(cudaMemsetAsync(Xhat16, 0, (uint64_t)f->bpad * d * 2, stream));
+  XK_CUDA(dalloc(&Wsub16, (uint64_t)f->mwpad * d));
+  XK_CUDA(cudaMemsetAsync(Wsub16, 0, (uint64_t)f->mwpad * d * 2, stream));
+  XK_CUDA(dalloc(&Pt, (uint64_t)f->bpad * ldp));
+  XK_CUDA(cudaMemsetAsync(Pt, 0, (uint64_t)f->bpad * ldp * 2, stream));
+  XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
+  XK_CUDA(dalloc(&f->labelterm, f->bpad));
+  XK_CUDA(dalloc(&f->partial_dx, (uint64_t)f->nbt * f->splits * 128 * 512));
+  XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
+  bool ok = true;
+  ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mF_B, Wsub16, d, f->mwpad, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  XK_CUDA(cudaFuncSetAttribute(k_gemm<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes<kF>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm<kDX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes<kDX>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm<kDW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes<kDW>()));
+  return XKNN_OK;
+}
+
+void Layer::free_fast() {
+  auto* f = static_cast<FastState*>(fast);
+  if (!f) return;
+  if (f->partial_f) cudaFree(f->partial_f);
+  if (f->labelterm) cudaFree(f->labelterm);
+  if (f->partial_dx) cudaFree(f->partial_dx);
+  delete f;
+  fast = nullptr;
+}
+
+xknn_status_t Layer::run_fast_core(uint64_t B) {
+  auto* f = static_cast<FastState*>(fast);
+  const uint32_t D = (uint32_t)d;
+  if (B > f->bpad) return XKNN_ERR_INVALID_ARGUMENT;
+  // (a) operands: X_hat (bf16) + norms; gathered, normalized active rows of W (bf16) + norms
+  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, nullptr, Xhat16, xnorm, err, stream));
+  ++launches;
+  XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, nullptr, Wsub16,
+                                wnorm, err, stream));
+  ++launches;
+  k_zero_rows_bf16<<<64, 256, 0, stream>>>(st, Wsub16, f->mwpad, D);
+  XK_LAUNCH();
+
+  mark(3);
+  GemmArgs ga{};
+  ga.st = st;
+  ga.B = (uint32_t)B;
+  ga.bpad = f->bpad;
+  ga.nbt = (uint32_t)((B + 127) / 128);
+  ga.splits = f->splits;
+  ga.dim = D;
+  ga.scale = cfg.scale;
+  ga.label_col = label_col;
+  ga.Pt = Pt;
+  ga.ldp = ldp;
+  ga.labelterm = f->labelterm;
+  // (b) GEMM-F with the fused exp/row-sum/label-logit epilogue
+  ga.partial = f->partial_f;
+  k_gemm<kF><<<kNumSMs, 384, smem_bytes<kF>(), stream>>>(f->mF_A, f->mF_B, ga);
+  XK_LAUNCH();
+  mark(4);
+  // (c) row statistics -> all-reduce over class shards -> loss
+  k_rowreduce<<<(unsigned)((B + 31) / 32), 1024, 0, stream>>>(st, f->partial_f, f->labelterm, label_col,
+                                                     (uint32_t)B, f->bpad, rowred);
+  XK_LAUNCH();
+  if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
+  XK_CUDA(launch_loss(rowred, B, loss_dev, st, err, stream));
+  ++launches;
+  // (d) label-column fix-up of P~ and the row-scaled X_hat'
+  k_fixup<4><<<grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream>>>(
+      rowred, label_col, X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16);
+  XK_LAUNCH();
+  mark(5);
+  // (e) GEMM-dW; with XKNN_FLAG_FUSED_UPDATE the normalize-backward + momentum-SGD update
+  //     runs in its epilogue (otherwise dW goes to HBM and k_update_rows applies it)
+  const bool fused = (cfg.flags & XKNN_FLAG_FUSED_UPDATE) != 0;
+  ga.out = fused ? nullptr : dW;
+  ga.W = W;
+  ga.V = V;
+  ga.active = active;
+  ga.begin = begin;
+  ga.wnorm = wnorm;
+  ga.lr = lr_dev;
+  ga.mu = cfg.momentum;
+  ga.wd = cfg.weight_decay;
+  ga.err = err;
+  k_gemm<kDW><<<kNumSMs, 384, smem_bytes<kDW>(), stream>>>(f->mDW_A, f->mDW_B, ga);
+  XK_LAUNCH();
+  mark(6);
+  // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
+  ga.partial = f->partial_dx;
+  ga.nbt = (uint32_t)((B + 127) / 128);
+  k_gemm<kDX><<<kNumSMs, 384, smem_bytes<kDX>(), stream>>>(f->mDX_A, f->mDX_B, ga);
+  XK_LAUNCH();
+  mark(7);
+  k_dx_reduce<<<grid_for(B * 128, 256), 256, 0, stream>>>(f->partial_dx, rowred, (uint32_t)B,
+                                                           ga.nbt, f->splits, cfg.scale, dXpart);
+  XK_LAUNCH();
+  const uint64_t bl = B / world;
+  if (world > 1)
+    XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
+  else
+    XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  return XKNN_OK;
 }
 
 }  // namespace xknn

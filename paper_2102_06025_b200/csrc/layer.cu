@@ -17,11 +17,15 @@ static xknn_status_t fail(xknn_status_t s, const std::string& msg) {
   return s;
 }
 
-xknn_status_t Layer::cuda_ok(cudaError_t e) {
+xknn_status_t fail_msg(xknn_status_t s, const char* msg) { return fail(s, msg); }
+
+xknn_status_t Layer::cuda_ok(cudaError_t e, const char* file, int line, const char* expr) {
   if (e == cudaSuccess) return XKNN_OK;
+  (void)cudaGetLastError();  // clear non-sticky errors so the caller's runtime stays clean
+  const std::string where = std::string(" at ") + file + ":" + std::to_string(line) + " " + expr;
   if (e == cudaErrorMemoryAllocation)
-    return fail(XKNN_ERR_OUT_OF_MEMORY, std::string("cuda: ") + cudaGetErrorString(e));
-  return fail(XKNN_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e));
+    return fail(XKNN_ERR_OUT_OF_MEMORY, std::string("cuda: ") + cudaGetErrorString(e) + where);
+  return fail(XKNN_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + where);
 }
 
 xknn_status_t Layer::nccl_ok(ncclResult_t r) {
@@ -29,11 +33,6 @@ xknn_status_t Layer::nccl_ok(ncclResult_t r) {
   return fail(XKNN_ERR_NCCL, std::string("nccl: ") + ncclGetErrorString(r));
 }
 
-template <typename T>
-static cudaError_t dalloc(T** p, uint64_t count) {
-  if (count == 0) count = 1;
-  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
-}
 
 xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
                           const xknn_config_t* cfg_, void* comm_, void* stream_) {
@@ -65,9 +64,10 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(dalloc(&sel_occ, nw));
   XK_CUDA(cudaMemsetAsync(sel_best, 0xff, nw * sizeof(uint32_t), stream));
   XK_CUDA(cudaMemsetAsync(sel_occ, 0, nw * sizeof(uint32_t), stream));
-  XK_CUDA(dalloc(&pool_bits, nwords));
-  XK_CUDA(dalloc(&act_bits, nwords));
-  XK_CUDA(dalloc(&lab_bits, nwords));
+  XK_CUDA(dalloc(&pool_bits, 3 * nwords));  // pool | act | labels, cleared by one memset
+  act_bits = pool_bits + nwords;
+  lab_bits = pool_bits + 2 * nwords;
+  XK_CUDA(dalloc(&pos_of, nw));
   XK_CUDA(dalloc(&pool_list, nw));
   XK_CUDA(dalloc(&active, mw_cap + 32));
   const uint64_t nblocks = (nwords + 255) / 256;
@@ -81,23 +81,18 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(dalloc(&pred, m));
   XK_CUDA(dalloc(&lw, m));
   XK_CUDA(dalloc(&labels_all, bmax));
-  XK_CUDA(dalloc(&labels_sorted, bmax));
-  XK_CUDA(dalloc(&labels_distinct, bmax));
-  XK_CUDA(dalloc(&n_distinct, 1));
   XK_CUDA(dalloc(&label_col, bmax));
-  XK_CUDA(dalloc(&pool_counts, world));
+  XK_CUDA(dalloc(&pool_counts, 2 * world));
   XK_CUDA(dalloc(&tie_counts, world));
   XK_CUDA(dalloc(&st, 1));
   XK_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), stream));
   XK_CUDA(dalloc(&err, 1));
   XK_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned long long), stream));
   XK_CUDA(dalloc(&loss_dev, 1));
+  XK_CUDA(dalloc(&lr_dev, 1));
 
   // cub temp: max over the sorts/scans/selects we run
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, b1, labels_all, labels_sorted, (int)bmax, 0, 32, stream);
-  cub::DeviceSelect::Unique(nullptr, b2, labels_sorted, labels_distinct, n_distinct, (int)bmax,
-                            stream);
   cub::DeviceScan::ExclusiveSum(nullptr, b3, blk_counts, blk_counts, (int)(nblocks + 1), stream);
   cub::DeviceRadixSort::SortPairs(nullptr, b4, pick_key, pick_key_s, pick_val, pick_val_s,
                                   (int)std::max<uint64_t>(m, 1), 0, 32, stream);
@@ -125,14 +120,18 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
 }
 
 void Layer::free_all() {
-  void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, act_bits, lab_bits,
+  void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, pos_of,
                   pool_list, active, blk_counts, mt_cache, pick_key, pick_val, pick_key_s,
-                  pick_val_s, pred, lw, labels_all, labels_sorted, labels_distinct, n_distinct,
-                  label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
+                  pick_val_s, pred, lw, labels_all, label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
                   Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
                   dXpart, loss_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto e : prof_ev) cudaEventDestroy(e);
+  prof_ev.clear();
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  graph_exec = nullptr;
+  if (lr_dev) cudaFree(lr_dev);
   free_fast();
 }
 
@@ -156,24 +155,59 @@ xknn_status_t Layer::ensure_mt_cache() {
   return XKNN_OK;
 }
 
-xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_local,
-                              uint64_t bl, float lr, double* loss_out, float* gfeat_local) {
-  const uint64_t B = bl * world;
-  const uint32_t D = (uint32_t)d;
-  last_b = B;
-  // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544)
-  if (world > 1) {
-    XK_NCCL(ncclGroupStart());
-    XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm, stream));
-    XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
-    XK_NCCL(ncclGroupEnd());
-  } else {
-    XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
-    XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
-                            stream));
+__global__ void k_set_f32(float* p, float v) { *p = v; }
+
+void Layer::mark(int i) {
+  if (!prof_on) return;
+  const uint64_t slot = graph_mode ? 0 : (prof_steps % kRing);
+  // inside a stream capture an External record becomes an event-record node fired on replay
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(prof_ev[slot * kMarks + i], stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(prof_ev[slot * kMarks + i], stream);
+}
+
+// Accumulates the phase durations of finished steps (all = wait for every recorded step).  In
+// graph mode the in-graph marks are fixed event nodes: the phases of the last replay count.
+void Layer::prof_collect(bool all) {
+  if (graph_mode) {
+    if (!all || prof_steps == 0) return;
+    cudaEvent_t* e = &prof_ev[0];
+    cudaEventSynchronize(e[kMarks - 1]);
+    prof_ms.assign(kMarks, 0.0);
+    for (int i = 0; i + 1 < kMarks; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] = ms;
+    }
+    prof_done = 1;
+    (void)cudaGetLastError();  // never leave a stale error for the caller's runtime
+    return;
   }
+  while (prof_done < prof_steps) {
+    if (!all && prof_steps - prof_done < kRing) break;
+    cudaEvent_t* e = &prof_ev[(prof_done % kRing) * kMarks];
+    cudaEventSynchronize(e[kMarks - 1]);
+    for (int i = 0; i + 1 < kMarks; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] += ms;
+    }
+    ++prof_done;
+  }
+  (void)cudaGetLastError();
+}
+
+// Everything between the input all-gather and the caller-facing outputs: selection, operands,
+// the three GEMMs with the distributed softmax, the feature-gradient reduce(-scatter) and the
+// sparse update.  Touches only layer-owned buffers, so it is captured once per batch size into
+// a CUDA graph and replayed (the learning rate is read from device memory).
+xknn_status_t Layer::run_core(uint64_t B) {
+  const uint32_t D = (uint32_t)d;
+  const uint64_t bl = B / world;
   // (1) Algorithm 1 selection -> this shard's sorted active rows
   XK_TRY(run_selection(B));
+  mark(2);
   unsigned int* cnt = &st->active_count;
   // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
   // whole shard as parallel.cpp:490-492 does -- row-wise identical)
@@ -185,9 +219,11 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
     ++launches;
     float* L = logits;
     float* G = logits + bmax * mw_cap;
+    mark(3);
     // (3) logits
     XK_CUDA(launch_logits_exact(Xhat, Wsub, B, cnt, mw_cap, D, cfg.scale, L, stream));
     ++launches;
+    mark(4);
     // (4) distributed softmax-CE: global row max, then [exp-sum, label term, owner] sums
     XK_CUDA(launch_rowmax(L, B, cnt, rowmax, stream));
     ++launches;
@@ -200,11 +236,14 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
     XK_CUDA(cudaMemcpyAsync(G, L, B * mw_cap * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     XK_CUDA(launch_softmax_grad(G, B, cnt, mw_cap, rowmax, rowred, label_col, stream));
     ++launches;
+    mark(5);
     // (5) weight side and feature side
     XK_CUDA(launch_dw_exact(G, Xhat, B, cnt, mw_cap, D, cfg.scale * 1.0f, dW, stream));
     ++launches;
+    mark(6);
     XK_CUDA(launch_dx_exact(G, Wsub, B, cnt, D, cfg.scale, dXpart, stream));
     ++launches;
+    mark(7);
     if (world > 1)
       XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
     else
@@ -212,16 +251,81 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   } else {
     XK_TRY(run_fast_core(B));
   }
+  // (8) normalize-backward + momentum SGD on the active rows only (parallel.cpp:649-667);
+  //     fused into the GEMM-dW epilogue in BF16 precision
+  mark(8);
+  if (cfg.precision == XKNN_PREC_FP32_EXACT || !(cfg.flags & XKNN_FLAG_FUSED_UPDATE)) {
+    XK_CUDA(launch_update_rows(W, V, dW, active, cnt, mw_cap, begin, D, wnorm, lr_dev,
+                               cfg.momentum, cfg.weight_decay, err, stream));
+    ++launches;
+  }
+  mark(9);
+  return XKNN_OK;
+}
+
+xknn_status_t Layer::ensure_graph(uint64_t B) {
+  if (graph_exec && graph_b == B && graph_prof == prof_on) return XKNN_OK;
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  graph_exec = nullptr;
+  XK_TRY(ensure_mt_cache());
+  const uint64_t l0 = launches;
+  cudaGraph_t g = nullptr;
+  XK_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  xknn_status_t s = run_core(B);
+  cudaError_t e = cudaStreamEndCapture(stream, &g);
+  if (s != XKNN_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  XK_CUDA(e);
+  e = cudaGraphInstantiate(&graph_exec, g, 0);
+  cudaGraphDestroy(g);
+  XK_CUDA(e);
+  graph_b = B;
+  graph_prof = prof_on;
+  graph_launches = launches - l0;
+  launches = l0;
+  return XKNN_OK;
+}
+
+xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_local,
+                              uint64_t bl, float lr, double* loss_out, float* gfeat_local) {
+  const uint64_t B = bl * world;
+  const uint32_t D = (uint32_t)d;
+  last_b = B;
+  graph_mode = !(cfg.flags & XKNN_FLAG_NO_GRAPH) && stream != nullptr;
+  if (prof_on) prof_collect(false);
+  mark(0);
+  // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544)
+  if (world > 1) {
+    XK_NCCL(ncclGroupStart());
+    XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm, stream));
+    XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
+    XK_NCCL(ncclGroupEnd());
+  } else {
+    XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                            stream));
+  }
+  // the learning rate travels through device memory so the captured core stays valid
+  k_set_f32<<<1, 1, 0, stream>>>(lr_dev, lr);
+  XK_LAUNCH();
+  mark(1);
+  if (graph_mode) {
+    XK_TRY(ensure_graph(B));
+    XK_CUDA(cudaGraphLaunch(graph_exec, stream));
+    launches += graph_launches;
+  } else {
+    XK_TRY(run_core(B));
+  }
   // (6) feature normalize-backward on this rank's rows (parallel.cpp:574-585)
   if (gfeat_local) {
     XK_CUDA(launch_feature_backward(X + (uint64_t)rank * bl * d, xnorm + (uint64_t)rank * bl, dX,
                                     bl, D, gfeat_local, stream));
     ++launches;
   }
-  // (8) normalize-backward + momentum SGD on the active rows only (parallel.cpp:649-667)
-  XK_CUDA(launch_update_rows(W, V, dW, active, cnt, mw_cap, begin, D, wnorm, lr, cfg.momentum,
-                             cfg.weight_decay, err, stream));
-  ++launches;
+  mark(10);
+  if (prof_on) ++prof_steps;
   if (loss_out)
     XK_CUDA(cudaMemcpyAsync(loss_out, loss_dev, sizeof(double), cudaMemcpyDeviceToDevice, stream));
   return XKNN_OK;
@@ -355,6 +459,9 @@ xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg) {
   L.cfg.momentum = cfg->momentum;
   L.cfg.weight_decay = cfg->weight_decay;
   L.cfg.rng_seed = cfg->rng_seed;
+  L.cfg.flags = cfg->flags;
+  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);
+  L.graph_exec = nullptr;
   return XKNN_OK;
 }
 
@@ -426,6 +533,8 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   L.g_off = nullptr;
   L.g_flat = nullptr;
   L.has_graph = false;
+  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);  // graph buffers are baked into the graph
+  L.graph_exec = nullptr;
   XK_CUDA_H(xknn::dalloc(&L.g_kpc, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_off, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_flat, flat_len));
@@ -547,5 +656,31 @@ xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out, uint64_t capac
 }
 
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h) { return h ? h->L.launches : 0; }
+
+xknn_status_t xknn_layer_profile(xknn_layer_t* h, int enable) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (enable && L.prof_ev.empty()) {
+    L.prof_ev.resize(Layer::kRing * Layer::kMarks);
+    for (auto& e : L.prof_ev) XK_CUDA_H(cudaEventCreate(&e));
+  }
+  L.prof_collect(true);
+  L.prof_on = enable != 0;
+  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);  // re-capture with/without the marks
+  L.graph_exec = nullptr;
+  L.prof_ms.assign(Layer::kMarks, 0.0);
+  L.prof_steps = L.prof_done = 0;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_phase_ms(xknn_layer_t* h, double* out, int n, uint64_t* steps) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  L.prof_collect(true);
+  for (int i = 0; i < n && i + 1 < Layer::kMarks; ++i)
+    out[i] = L.prof_ms.empty() ? 0.0 : L.prof_ms[i];
+  if (steps) *steps = L.prof_done;
+  return XKNN_OK;
+}
 
 }  // extern "C"

@@ -26,6 +26,8 @@
 
 namespace xknn {
 
+xknn_status_t fail_msg(xknn_status_t s, const char* msg);  // sets xknn_last_error_message
+
 struct SelState {
   unsigned long long pool_local;   // |pool ∩ shard|
   unsigned long long pool_total;   // |pool|
@@ -76,6 +78,7 @@ struct Layer {
   uint32_t* lab_bits = nullptr;
   uint64_t nwords = 0;
   uint32_t* pool_list = nullptr;      // sorted local pool (global ids), cap nw
+  uint32_t* pos_of = nullptr;         // local class -> position in `active` (valid if active)
   uint32_t* active = nullptr;         // sorted local active (global ids), cap mw_cap
   uint64_t mw_cap = 0;
   uint32_t* blk_counts = nullptr;     // compaction block counts / offsets
@@ -88,11 +91,8 @@ struct Layer {
   uint32_t* pred = nullptr;           // [M]
   uint32_t* lw = nullptr;             // [M]
   uint32_t* labels_all = nullptr;     // [B]
-  uint32_t* labels_sorted = nullptr;  // [B]
-  uint32_t* labels_distinct = nullptr;// [B]
-  uint32_t* n_distinct = nullptr;     // [1]
   int32_t* label_col = nullptr;       // [B] column of label in local active list, -1 if not local
-  unsigned long long* pool_counts = nullptr;  // [world]
+  unsigned long long* pool_counts = nullptr;  // [2*world]: pool size, distinct labels
   unsigned long long* tie_counts = nullptr;   // [world]
   uint32_t* hist = nullptr;           // over-full histograms [hist_len]
   uint64_t hist_len = 0;
@@ -122,6 +122,11 @@ struct Layer {
   float* dXpart = nullptr;            // split-K partials
   uint64_t dxpart_splits = 0;
   double* loss_dev = nullptr;         // [1]
+  float* lr_dev = nullptr;            // [1] learning rate of the current step
+  // CUDA graph of run_core per batch size
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_b = 0, graph_launches = 0;
+  bool graph_mode = false, graph_prof = false;
   uint64_t last_b = 0;
 
   std::string last_msg;
@@ -132,10 +137,24 @@ struct Layer {
   void free_all();
   xknn_status_t ensure_mt_cache();
   xknn_status_t run_selection(uint64_t batch);    // labels_all already on device
+  xknn_status_t run_core(uint64_t batch);
+  xknn_status_t ensure_graph(uint64_t batch);
   xknn_status_t run_step(const float* feats_local, const uint32_t* labels_local,
                          uint64_t batch_local, float lr, double* loss_out, float* gfeat_local);
   xknn_status_t nccl_ok(ncclResult_t r);
-  xknn_status_t cuda_ok(cudaError_t e);
+  xknn_status_t cuda_ok(cudaError_t e, const char* file = "", int line = 0,
+                        const char* expr = "");
+
+  // phase profiler: CUDA events recorded on the layer stream at phase boundaries (a ring of
+  // per-step event sets, read back lazily so the timed loop stays asynchronous)
+  static constexpr int kMarks = 11;
+  static constexpr int kRing = 64;
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<double> prof_ms;
+  uint64_t prof_steps = 0, prof_done = 0;
+  void mark(int i);
+  void prof_collect(bool all);
 
   // BF16 tensor-core path (fast.cu)
   void* fast = nullptr;
@@ -147,10 +166,10 @@ struct Layer {
 }  // namespace xknn
 
 // error helpers usable inside Layer methods
-#define XK_CUDA(expr)                                  \
-  do {                                                 \
-    cudaError_t _e = (expr);                           \
-    if (_e != cudaSuccess) return cuda_ok(_e);         \
+#define XK_CUDA(expr)                                                      \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) return cuda_ok(_e, __FILE__, __LINE__, #expr);  \
   } while (0)
 #define XK_NCCL(expr)                                  \
   do {                                                 \
@@ -162,10 +181,10 @@ struct Layer {
     xknn_status_t _s = (expr);                         \
     if (_s != XKNN_OK) return _s;                      \
   } while (0)
-#define XK_CUDA_H(expr)                                \
-  do {                                                 \
-    cudaError_t _e = (expr);                           \
-    if (_e != cudaSuccess) return h->L.cuda_ok(_e);    \
+#define XK_CUDA_H(expr)                                                        \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) return h->L.cuda_ok(_e, __FILE__, __LINE__, #expr); \
   } while (0)
 #define XK_LAUNCH() \
   do {              \

@@ -83,9 +83,10 @@ template <int DV>
 __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
                               const float* __restrict__ G, const uint32_t* __restrict__ active,
                               const unsigned int* count, uint64_t begin, uint32_t d,
-                              const float* __restrict__ wnorm, float lr, float mu, float wd,
-                              const unsigned long long* err) {
+                              const float* __restrict__ wnorm, const float* __restrict__ lr_dev,
+                              float mu, float wd, const unsigned long long* err) {
   if (*err) return;
+  const float lr = *lr_dev;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = *count;
   for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < nrows;
@@ -197,7 +198,7 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
 
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
-                               uint32_t d, const float* wnorm, float lr, float mu, float wd,
+                               uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
                                const unsigned long long* err, cudaStream_t s) {
   const unsigned grid = grid_for(max_rows * 32, 256);
   XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,

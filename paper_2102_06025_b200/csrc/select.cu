@@ -30,20 +30,27 @@ namespace {
 
 constexpr int kCompactBlock = 256;
 
-// ---- pool marking: one warp per batch label, lanes stride the label's slice
+// ---- pool marking: one warp per batch label, lanes stride the label's slice; lane 0 also
+// marks the label (distinct labels of this shard counted as newly set bits)
 __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch, uint64_t n,
                             uint64_t begin, uint64_t nw, const uint32_t* __restrict__ kpc,
                             const uint64_t* __restrict__ off, const uint32_t* __restrict__ flat,
-                            uint32_t* pool_bits, uint32_t* best, uint32_t* occ,
-                            unsigned long long* err, int reset) {
+                            uint32_t* pool_bits, uint32_t* lab_bits, uint32_t* best, uint32_t* occ,
+                            SelState* st, unsigned long long* err, int reset) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t newlab = 0;
   for (uint32_t i = warp; i < batch; i += nwarps) {
     const uint32_t y = labels[i];
     if (y >= n) {
       if (lane == 0 && !reset) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
       continue;
+    }
+    if (!reset && lane == 0 && y >= begin && y - begin < nw) {
+      const uint64_t lc = y - begin;
+      const uint32_t bit = 1u << (lc & 31);
+      if (!(atomicOr(&lab_bits[lc >> 5], bit) & bit)) ++newlab;
     }
     const uint32_t kk = kpc[y];
     const uint64_t o = off[y];
@@ -60,76 +67,90 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
       }
     }
   }
+  newlab = warp_sum(newlab);
+  if (lane == 0 && newlab) atomicAdd(&st->labels_local, newlab);
 }
 
-__global__ void k_label_bits(const uint32_t* __restrict__ distinct, const uint32_t* n_distinct,
-                             uint64_t begin, uint64_t end, uint32_t* lab_bits, SelState* st) {
-  const uint32_t nd = *n_distinct;
-  uint32_t local = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
-    const uint64_t y = distinct[i];
-    if (y >= begin && y < end) {
-      const uint64_t lc = y - begin;
-      atomicOr(&lab_bits[lc >> 5], 1u << (lc & 31));
-      ++local;
-    }
-  }
-  local = warp_sum(local);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&st->labels_local, local);
+// ---- bitmap -> sorted list compaction (one 32-bit word per thread, block scan, sorted by
+// construction).  mode 0: the pool bitmap.  mode 1: the final active set = act | pool (padding /
+// exact fit, knn_softmax.cpp:32-51) or act | labels (over-full, :52-72).
+__device__ __forceinline__ uint32_t final_word(int mode, const SelState* st, const uint32_t* act,
+                                               const uint32_t* pool, const uint32_t* lab,
+                                               uint64_t w) {
+  if (mode == 0) return pool[w];
+  return act[w] | (st->branch == kOverfull ? lab[w] : pool[w]);
 }
 
-// ---- bitmap -> sorted list compaction (ballot-free: one 32-bit word per thread)
-__global__ void k_bits_count(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+__global__ void k_bits_count(int mode, SelState* st, const uint32_t* __restrict__ act,
+                             const uint32_t* __restrict__ pool, const uint32_t* __restrict__ lab,
                              uint64_t nwords, uint32_t* blk_counts) {
   using BR = cub::BlockReduce<uint32_t, kCompactBlock>;
   __shared__ typename BR::TempStorage tmp;
+  __shared__ typename BR::TempStorage tmp2;
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
-  uint32_t word = 0;
-  if (w < nwords) word = a[w] | (b ? b[w] : 0u);
+  uint32_t word = 0, found = 0;
+  if (w < nwords) {
+    word = final_word(mode, st, act, pool, lab, w);
+    if (mode == 1) found = __popc(word & lab[w]);
+  }
   const uint32_t c = BR(tmp).Sum(__popc(word));
   if (threadIdx.x == 0) blk_counts[blockIdx.x] = c;
+  if (mode == 1) {
+    const uint32_t f = BR(tmp2).Sum(found);
+    if (threadIdx.x == 0 && f) atomicAdd(&st->labels_found, f);
+  }
 }
 
-__global__ void k_bits_write(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+__global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict__ act,
+                             const uint32_t* __restrict__ pool, const uint32_t* __restrict__ lab,
                              uint64_t nwords, const uint32_t* __restrict__ blk_off,
                              uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
-                             unsigned int* out_count) {
+                             uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
+                             int rank) {
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
   __shared__ typename BS::TempStorage tmp;
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
   uint32_t word = 0;
-  if (w < nwords) word = a[w] | (b ? b[w] : 0u);
+  if (w < nwords) word = final_word(mode, st, act, pool, lab, w);
   uint32_t pos;
   BS(tmp).ExclusiveSum(__popc(word), pos);
   pos += blk_off[blockIdx.x];
   while (word) {
     const uint32_t bit = __ffs(word) - 1;
-    out[pos++] = base + (uint32_t)(w * 32 + bit);
+    const uint32_t lc = (uint32_t)(w * 32 + bit);
+    out[pos] = base + lc;
+    if (pos_of) pos_of[lc] = pos;
+    ++pos;
     word &= word - 1;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *out_count = blk_off[nblocks];
-}
-
-__global__ void k_store_pool_count(SelState* st, unsigned long long* pool_counts, int rank) {
-  st->pool_local = st->pool_count;
-  pool_counts[rank] = st->pool_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t total = blk_off[nblocks];
+    if (mode == 0) {
+      st->pool_count = total;
+      st->pool_local = total;
+      pool_counts[2 * rank] = total;              // exchanged: [pool, distinct labels] per shard
+      pool_counts[2 * rank + 1] = st->labels_local;
+    } else {
+      st->active_count = total;
+    }
+  }
 }
 
 // ---- the plan: which branch, how many pads, which complement positions this shard owns
 __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int world, int rank,
                        uint64_t n, uint64_t m, uint64_t begin, uint64_t nw,
-                       const uint32_t* n_distinct, unsigned long long* err) {
-  unsigned long long total = 0, before = 0;
+                       unsigned long long* err) {
+  unsigned long long total = 0, before = 0, nd = 0;
   for (int s = 0; s < world; ++s) {
-    total += pool_counts[s];
-    if (s < rank) before += pool_counts[s];
+    total += pool_counts[2 * s];
+    nd += pool_counts[2 * s + 1];  // shards own disjoint class ranges
+    if (s < rank) before += pool_counts[2 * s];
   }
-  const unsigned long long nd = *n_distinct;
   st->pool_total = total;
   st->nd = nd;
   st->csize = n - total;
   st->cbase = begin - before;
-  st->compl_local = nw - pool_counts[rank];
+  st->compl_local = nw - pool_counts[2 * rank];
   st->first_rej = kNone;
   st->need = 0;
   st->take = 0;
@@ -195,27 +216,19 @@ __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, ui
   }
 }
 
-// pred[i] = last t < i with j_t == j_i (sorted runs are stable: ascending t)
-__global__ void k_pred(const SelState* st, const uint32_t* __restrict__ key_s,
-                       const uint32_t* __restrict__ val_s, uint32_t* __restrict__ pred) {
-  if (st->branch != kPad) return;
-  const uint64_t need = st->need;
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < need;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t j = key_s[q];
-    pred[val_s[q]] = (q > 0 && key_s[q - 1] == j) ? val_s[q - 1] : kNone;
-  }
-}
-
+// pred[i] = last t < i with j_t == j_i (sorted runs are stable: ascending t), and
 // lw[t] = last t' < t with j_t' == t (the swap that last moved a value into position t before
 // step t ran)
-__global__ void k_lastwriter(const SelState* st, const uint32_t* __restrict__ key_s,
-                             const uint32_t* __restrict__ val_s, uint32_t* __restrict__ lw) {
+__global__ void k_pred_lw(const SelState* st, const uint32_t* __restrict__ key_s,
+                          const uint32_t* __restrict__ val_s, uint32_t* __restrict__ pred,
+                          uint32_t* __restrict__ lw) {
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < need;
-       t += gridDim.x * blockDim.x) {
-    // upper_bound(t) over key_s[0, need)
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < need; q += gridDim.x * blockDim.x) {
+    const uint32_t j = key_s[q];
+    pred[val_s[q]] = (q > 0 && key_s[q - 1] == j) ? val_s[q - 1] : kNone;
+    // lw for position t = q: upper_bound(q) over key_s[0, need)
+    const uint32_t t = q;
     uint32_t lo = 0, hi = need;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
@@ -223,11 +236,11 @@ __global__ void k_lastwriter(const SelState* st, const uint32_t* __restrict__ ke
     }
     uint32_t r = kNone;
     if (lo > 0 && key_s[lo - 1] == t) {
-      uint32_t q = lo - 1;
-      if (val_s[q] == t) {
-        if (q > 0 && key_s[q - 1] == t) r = val_s[q - 1];
+      const uint32_t p = lo - 1;
+      if (val_s[p] == t) {
+        if (p > 0 && key_s[p - 1] == t) r = val_s[p - 1];
       } else {
-        r = val_s[q];
+        r = val_s[p];
       }
     }
     lw[t] = r;
@@ -375,47 +388,22 @@ __global__ void k_of_select(SelState* st, const uint32_t* __restrict__ pool_list
   }
 }
 
-__global__ void k_or_bits(const SelState* st, uint32_t* act, const uint32_t* __restrict__ lab,
-                          const uint32_t* __restrict__ pool, uint64_t nwords) {
-  const bool with_pool = st->branch != kOverfull;  // over-full: k_of_select marked its picks
-  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
-       w += (uint64_t)gridDim.x * blockDim.x)
-    act[w] |= lab[w] | (with_pool ? pool[w] : 0u);
-}
-
-// label -> column in this shard's active list (-1 if another shard owns it)
-__global__ void k_label_cols(SelState* st, const uint32_t* __restrict__ labels, uint32_t batch,
-                             const uint32_t* __restrict__ active, uint64_t begin, uint64_t end,
-                             int32_t* label_col, unsigned long long* err) {
+// label -> column in this shard's active list (-1 if another shard owns it or it is absent:
+// the softmax then reports LabelOutOfRange as distributed_softmax_xent_cols does, :157-161)
+__global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ labels,
+                             uint32_t batch, const uint32_t* __restrict__ active,
+                             const uint32_t* __restrict__ pos_of, uint64_t begin, uint64_t end,
+                             int32_t* label_col) {
   const uint32_t na = st->active_count;
-  uint32_t found = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += gridDim.x * blockDim.x) {
     const uint32_t y = labels[i];
     int32_t col = -1;
     if (y >= begin && y < end) {
-      const uint32_t p = lower_bound_u32(active, na, y);
+      const uint32_t p = pos_of[y - begin];
       if (p < na && active[p] == y) col = (int32_t)p;
-      else raise_error(err, XKNN_ERR_LABEL_NOT_ACTIVE, i);
     }
     label_col[i] = col;
   }
-  (void)found;
-}
-
-__global__ void k_labels_found(SelState* st, const uint32_t* __restrict__ distinct,
-                               const uint32_t* n_distinct, const uint32_t* __restrict__ active,
-                               uint64_t begin, uint64_t end) {
-  const uint32_t nd = *n_distinct, na = st->active_count;
-  uint32_t f = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
-    const uint32_t y = distinct[i];
-    if (y >= begin && y < end) {
-      const uint32_t p = lower_bound_u32(active, na, y);
-      f += (p < na && active[p] == y);
-    }
-  }
-  f = warp_sum(f);
-  if ((threadIdx.x & 31) == 0 && f) atomicAdd(&st->labels_found, f);
 }
 
 __global__ void k_zero_sel(SelState* st) {
@@ -427,61 +415,49 @@ __global__ void k_zero_sel(SelState* st) {
 
 }  // namespace
 
-// Compacts (a | b) over this shard's bitmap into sorted global ids.
-static xknn_status_t compact_bits(Layer& L, const uint32_t* a, const uint32_t* b, uint32_t* out,
-                                  unsigned int* out_count) {
+// Compacts this shard's bitmap (mode 0: pool, mode 1: final active set) into sorted global ids.
+static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* pos_of) {
   const uint32_t nblocks = (uint32_t)((L.nwords + kCompactBlock - 1) / kCompactBlock);
-  k_bits_count<<<nblocks, kCompactBlock, 0, L.stream>>>(a, b, L.nwords, L.blk_counts);
+  k_bits_count<<<nblocks, kCompactBlock, 0, L.stream>>>(mode, L.st, L.act_bits, L.pool_bits,
+                                                        L.lab_bits, L.nwords, L.blk_counts);
   ++L.launches;
   // blk_counts[nblocks] is kept 0, so the exclusive scan's last entry is the total
   size_t bytes = L.cub_tmp_bytes;
-  if (cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.blk_counts, L.blk_counts + nblocks + 1,
-                                    nblocks + 1, L.stream) != cudaSuccess)
-    return L.cuda_ok(cudaGetLastError());
-  k_bits_write<<<nblocks, kCompactBlock, 0, L.stream>>>(a, b, L.nwords, L.blk_counts + nblocks + 1,
-                                                        nblocks, (uint32_t)L.begin, out, out_count);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.blk_counts,
+                                                L.blk_counts + nblocks + 1, nblocks + 1, L.stream);
+  if (e != cudaSuccess) return L.cuda_ok(e, __FILE__, __LINE__, "DeviceScan");
   ++L.launches;
-  return L.cuda_ok(cudaGetLastError());
+  k_bits_write<<<nblocks, kCompactBlock, 0, L.stream>>>(
+      mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
+      nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank);
+  ++L.launches;
+  return L.cuda_ok(cudaGetLastError(), __FILE__, __LINE__, "k_bits_write");
 }
 
 xknn_status_t Layer::run_selection(uint64_t batch) {
   const uint32_t B = (uint32_t)batch;
   const uint64_t m = cfg.m_active;
   XK_TRY(ensure_mt_cache());
-  const size_t wbytes = nwords * sizeof(uint32_t);
-  XK_CUDA(cudaMemsetAsync(pool_bits, 0, wbytes, stream));
-  XK_CUDA(cudaMemsetAsync(act_bits, 0, wbytes, stream));
-  XK_CUDA(cudaMemsetAsync(lab_bits, 0, wbytes, stream));
+  // pool_bits, act_bits, lab_bits are one allocation
+  XK_CUDA(cudaMemsetAsync(pool_bits, 0, 3 * nwords * sizeof(uint32_t), stream));
   k_zero_sel<<<1, 1, 0, stream>>>(st);
   XK_LAUNCH();
 
-  // (1) pool of this shard: union of its slices for every batch label (knn_softmax.cpp:122-132)
+  // (1) pool of this shard: union of its slices for every batch label (knn_softmax.cpp:122-132),
+  //     candidate best rank / occurrences, and the labels this shard owns
   k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
-      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, sel_best, sel_occ, err, 0);
+      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
+      st, err, 0);
   XK_LAUNCH();
-  // (2) distinct labels (knn_softmax.cpp:20-23)
-  size_t bytes = cub_tmp_bytes;
-  XK_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, bytes, labels_all, labels_sorted, (int)B, 0, 32,
-                                         stream));
-  bytes = cub_tmp_bytes;
-  XK_CUDA(cub::DeviceSelect::Unique(cub_tmp, bytes, labels_sorted, labels_distinct, n_distinct,
-                                    (int)B, stream));
-  launches += 6;
-  k_label_bits<<<grid_for(B, 256), 256, 0, stream>>>(labels_distinct, n_distinct, begin, end,
-                                                      lab_bits, st);
-  XK_LAUNCH();
-  // (3) sorted local pool and the cross-shard pool counts
-  XK_TRY(compact_bits(*this, pool_bits, nullptr, pool_list, &st->pool_count));
-  k_store_pool_count<<<1, 1, 0, stream>>>(st, pool_counts, rank);
-  XK_LAUNCH();
+  // (2) sorted local pool; [pool size, distinct labels] exchanged between shards
+  XK_TRY(compact_bits(*this, 0, pool_list, nullptr));
   if (world > 1)
-    XK_NCCL(ncclAllGather(pool_counts + rank, pool_counts, 1, ncclUint64, comm, stream));
-  k_plan<<<1, 1, 0, stream>>>(st, pool_counts, world, rank, n, m, begin, nw, n_distinct, err);
+    XK_NCCL(ncclAllGather(pool_counts + 2 * rank, pool_counts, 2, ncclUint64, comm, stream));
+  k_plan<<<1, 1, 0, stream>>>(st, pool_counts, world, rank, n, m, begin, nw, err);
   XK_LAUNCH();
 
-  // (4a) padding branch
-  const bool pad_possible = m > 0;
-  if (pad_possible) {
+  // (3a) padding branch (|pool| < M): picks from the cached stream, Fisher-Yates chains
+  if (m > 0) {
     uint32_t bits = 1;
     while (bits < 32 && (1ull << bits) <= n) ++bits;
     if (bits < 32) ++bits;
@@ -490,19 +466,17 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
     XK_LAUNCH();
     k_picks_replay<<<1, 1, 0, stream>>>(st, mt_cache, mt_len, pick_key, err);
     XK_LAUNCH();
-    bytes = cub_tmp_bytes;
+    size_t bytes = cub_tmp_bytes;
     XK_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, pick_key, pick_key_s, pick_val,
                                             pick_val_s, (int)m, 0, (int)bits, stream));
-    launches += 4;
-    k_pred<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, pred);
-    XK_LAUNCH();
-    k_lastwriter<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, lw);
+    launches += 3;
+    k_pred_lw<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, pred, lw);
     XK_LAUNCH();
     k_pad_map<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pred, lw, pool_list, begin,
                                                      act_bits);
     XK_LAUNCH();
   }
-  // (4b) over-full branch: only reachable when B * k could exceed M
+  // (3b) over-full branch: only reachable when B * k could exceed M
   const bool overfull_possible = (uint64_t)B * g_kmax > m;
   if (overfull_possible) {
     const uint32_t nb_rank = g_kmax ? g_kmax : 1;
@@ -531,20 +505,15 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
                                         tie_counts, rank, nb_rank, act_bits);
     XK_LAUNCH();
   }
-  // (5) final ActiveSet slice: pool (padding / exact fit) or ranked picks, plus the labels
-  //     (always retained); sorted by construction
-  k_or_bits<<<grid_for(nwords, 256), 256, 0, stream>>>(st, act_bits, lab_bits, pool_bits, nwords);
+  // (4) this shard's ActiveSet slice, sorted by construction; label -> column map
+  XK_TRY(compact_bits(*this, 1, active, pos_of));
+  k_label_cols<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_all, B, active, pos_of, begin, end,
+                                                      label_col);
   XK_LAUNCH();
-  XK_TRY(compact_bits(*this, act_bits, nullptr, active, &st->active_count));
-  k_label_cols<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_all, B, active, begin, end,
-                                                      label_col, err);
-  XK_LAUNCH();
-  k_labels_found<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_distinct, n_distinct, active,
-                                                        begin, end);
-  XK_LAUNCH();
-  // (6) reset the candidate ranks touched this step
+  // (5) reset the candidate ranks touched this step
   k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
-      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, sel_best, sel_occ, err, 1);
+      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
+      st, err, 1);
   XK_LAUNCH();
   return XKNN_OK;
 }

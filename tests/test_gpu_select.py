@@ -20,7 +20,7 @@ def _check(n, k, b, m, seed, graph_seed, label_seed, trials=1):
     g = O.random_graph(n, k, graph_seed)
     shards = [O.compress(g, 1, 0)]
     w = np.ones((n, 128), np.float32)
-    layer = make_layer(n, 128, 1, 0, m, b, w, g, precision=X.PREC_BF16, seed=seed)
+    layer = make_layer(n, 128, 1, 0, m, b, w, g, precision=X.PREC_FP32_EXACT, seed=seed)
     rng = np.random.default_rng(label_seed)
     for _ in range(trials):
         lab = rng.integers(0, n, b).astype(np.uint32)
@@ -61,7 +61,7 @@ def test_select_exact_fit():
     pool = np.unique(g[lab].ravel())
     m = pool.size
     layer = make_layer(n, 128, 1, 0, m, b, np.ones((n, 128), np.float32), g,
-                       precision=X.PREC_BF16)
+                       precision=X.PREC_FP32_EXACT)
     got, _ = layer.select_active_classes(torch.from_numpy(lab.view(np.int32)).cuda())
     assert np.array_equal(got.cpu().numpy().view(np.uint32), pool.astype(np.uint32))
 
@@ -72,7 +72,7 @@ def test_select_errors():
     torch = torch_cuda()
     n, k, b = 1_000, 4, 32
     g = O.random_graph(n, k, 1)
-    layer = make_layer(n, 128, 1, 0, 8, b, np.ones((n, 128), np.float32), g, precision=X.PREC_BF16)
+    layer = make_layer(n, 128, 1, 0, 8, b, np.ones((n, 128), np.float32), g, precision=X.PREC_FP32_EXACT)
     lab = np.arange(b, dtype=np.uint32)
     with pytest.raises(X.MTooSmall):  # knn_softmax.cpp:24-27
         layer.select_active_classes(torch.from_numpy(lab.view(np.int32)).cuda())
@@ -93,6 +93,28 @@ def test_select_golden_p1(i):
     n, k, m = int(z["n"]), int(z["k"]), int(z["m"])
     g = O.random_graph(n, k, int(z["graph_seed"]))
     layer = make_layer(n, 128, 1, 0, m, int(z["b"]), np.ones((n, 128), np.float32), g,
-                       precision=X.PREC_BF16, seed=int(z["seed"]))
+                       precision=X.PREC_FP32_EXACT, seed=int(z["seed"]))
     got, ca = layer.select_active_classes(torch.from_numpy(z["labels"].view(np.int32)).cuda())
     assert np.array_equal(got.cpu().numpy().view(np.uint32), z["active"])
+
+
+@pytest.mark.parametrize("m", [600, 60])
+def test_select_not_self_first(m):
+    """Graphs whose lists omit the class itself: labels join the ActiveSet only in the over-full
+    branch (knn_softmax.cpp:52-54); contains_all_labels reports the difference."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    n, k, b = 2_000, 5, 40
+    rng = np.random.default_rng(3)
+    g = O.random_graph(n, k + 1, 9)[:, 1:].copy()  # drop self
+    shards = [O.compress(g, 1, 0)]
+    layer = make_layer(n, 128, 1, 0, m, b, np.ones((n, 128), np.float32), g,
+                       precision=X.PREC_FP32_EXACT, seed=5)
+    for _ in range(4):
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        rc, want, ca = O.select_shards("oracle", n, shards, lab, m, 5)
+        assert rc == 0
+        got, gca = layer.select_active_classes(torch.from_numpy(lab.view(np.int32)).cuda())
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), want)
+        assert gca == ca

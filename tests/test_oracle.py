@@ -156,3 +156,19 @@ def test_ref_graph_builders():
     rc, go = O.bruteforce_graph("oracle", wn, 10)
     rc2, gr = O.bruteforce_graph("ref", wn, 10)
     assert rc == rc2 == 0 and np.array_equal(go, gr)
+
+
+@pytest.mark.ref
+def test_ref_selection_not_self_first():
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        n = int(rng.integers(100, 3000))
+        k = int(rng.integers(2, 12))
+        g = O.random_graph(n, k + 1, trial)[:, 1:].copy()
+        p = int(rng.choice([1, 2, 4]))
+        shards = [O.compress(g, p, s) for s in range(p)]
+        lab = rng.integers(0, n, 30).astype(np.uint32)
+        m = int(rng.integers(30, n))
+        a = O.select_shards("oracle", n, shards, lab, m, trial)
+        r = O.select_shards("ref", n, shards, lab, m, trial)
+        assert a[0] == r[0] and np.array_equal(a[1], r[1]) and a[2] == r[2]
