@@ -290,7 +290,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                                             C.POINTER(C.c_uint64)]
     X.lib().xknn_layer_phase_ms(layer.h, ph, len(PHASES), C.byref(nsteps))
     X.lib().xknn_layer_profile(layer.h, 0)
-    phase_ms = {PHASES[i]: ph[i] / max(nsteps.value, 1) for i in range(len(PHASES))}
+    phase_ms = {PHASES[i]: ph[i] / max(nsteps.value, 1) for i in range(len(PHASES))
+                if PHASES[i] != "-"}
     layer.sync()
     active_total, active_local = layer.last_active()
     loss_v = float(loss.item())

@@ -164,7 +164,8 @@ xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out_host, uint64_t 
    0 feature/label all-gather, 1 selection, 2 operand normalize/gather, 3 logit GEMM (+ fused
    softmax epilogue in BF16), 4 softmax statistics + all-reduce + loss, 5 weight-gradient GEMM,
    6 feature-gradient GEMM, 7 feature-gradient reduce(-scatter), 8 normalize-backward +
-   momentum-SGD row update, 9 feature normalize-backward. */
+   momentum-SGD row update (BF16: the wait for it), 9 feature normalize-backward, 11 the BF16
+   row update itself (it runs on a side stream concurrently with phase 6). */
 xknn_status_t xknn_layer_profile(xknn_layer_t* h, int enable);
 xknn_status_t xknn_layer_phase_ms(xknn_layer_t* h, double* out_ms, int n, uint64_t* steps);
 

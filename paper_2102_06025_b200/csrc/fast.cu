@@ -392,6 +392,443 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+
+// =============================================================================================
+// CTA-pair (cta_group::2) GEMMs: M = 256 rows per pair (128 per SM), the N operand split across
+// the pair, MMAs issued by the leader CTA only, TMEM accumulators in both.  GEMM-F keeps the
+// pair's X_hat rows resident in shared memory for a whole unit, so only W_sub streams: 128
+// MAC/B of L2 traffic per SM (vs 44 for the 1-CTA kernel), under the chip's L2 bandwidth.
+// Epilogues stage each 32x32 chunk in swizzled shared memory and store with TMA (full lines).
+// =============================================================================================
+template <int KIND>
+struct Cfg2;
+template <>
+struct Cfg2<kF> {
+  static constexpr uint32_t STAGES = 4, A_BYTES = 0, B_BYTES = 128 * 64 * 2;
+  static constexpr uint32_t ARES_BYTES = 8 * 128 * 64 * 2;  // resident X_hat: 128 rows x 512
+  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 2048;  // staging per warp buffer
+};
+template <>
+struct Cfg2<kDX> {
+  static constexpr uint32_t STAGES = 6, A_BYTES = 128 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
+  static constexpr uint32_t ARES_BYTES = 0;
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096;
+};
+template <>
+struct Cfg2<kDW> {
+  static constexpr uint32_t STAGES = 6, A_BYTES = 2 * 64 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
+  static constexpr uint32_t ARES_BYTES = 0;
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096;
+};
+
+template <int KIND>
+constexpr uint32_t smem_bytes2() {
+  using C = Cfg2<KIND>;
+  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * 2 * C::STG + 1024 + 256 +
+         (KIND == kDW ? 2048 + 64 : 0);  // dW: fp64 row-dot exchange of the fused update
+}
+
+struct Unit2 {
+  uint32_t row0;   // F/dX: first batch row of the pair; dW: first class of the pair
+  uint32_t t0, t1; // F: class-tile range; dX: 32-class K-chunk range; dW: unused
+  uint32_t id;
+  bool valid;
+};
+
+template <int KIND>
+__device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
+  if (KIND == kDW) return (mw + 255) / 256;
+  return a.nbt * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per pair-tile
+}
+
+template <int KIND>
+__device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32_t u) {
+  Unit2 x{};
+  x.id = u;
+  if (KIND == kDW) {
+    x.row0 = u * 256;
+    x.valid = true;
+    return x;
+  }
+  const uint32_t bp = u % a.nbt, r = u / a.nbt;
+  const uint32_t nt = KIND == kF ? (mw + 255) / 256 : (mw + 31) / 32;
+  x.row0 = bp * 256;
+  x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
+  x.t1 = (uint32_t)((uint64_t)(r + 1) * nt / a.splits);
+  x.valid = KIND == kDX || x.t1 > x.t0;  // dX units always write their (maybe zero) partial
+  return x;
+}
+
+// swizzled staging of one thread's 32-element row chunk: fp32 (SW128, 128-B rows) or bf16
+// (SW64, 64-B rows), matching the store tensor map
+__device__ __forceinline__ void stage_f32(uint8_t* buf, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {
+    float4* d = reinterpret_cast<float4*>(buf + r * 128 + ((c ^ (r & 7)) * 16));
+    *d = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+__device__ __forceinline__ void stage_bf16(uint8_t* buf, uint32_t r, const uint32_t (&pk)[16]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c) {
+    uint4* d = reinterpret_cast<uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
+    *d = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+  }
+}
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmOut, GemmArgs a) {
+  using C = Cfg2<KIND>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sRes = smem;                                      // F: resident A
+  uint8_t* sA = sRes + C::ARES_BYTES;                        // staged A
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;                 // staged B
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;               // epilogue staging, 8 warps x 2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 2 * C::STG);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint64_t* aempty = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = tc::cluster_ctarank();
+  const bool leader = cta == 0;
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (uint32_t s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (uint32_t s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 16);  // 8 epilogue warps in each CTA of the pair
+    }
+    tc::mbar_init(afull, 1);
+    tc::mbar_init(aempty, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    tc::tma_prefetch(&tmOut);
+  }
+  if (warp == 2) tc::tmem_alloc_2sm<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // peers see initialised barriers before any remote arrive / TMA
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  const uint32_t mw = a.st->active_count;
+  const uint32_t nunits = num_units2<KIND>(a, mw);
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs load their half) =================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, aphase = 0;
+      for (uint32_t u = pair; u < nunits; u += npairs) {
+        const Unit2 x = unit2_of<KIND>(a, mw, u);
+        if (!x.valid) continue;
+        const int32_t myrow = (int32_t)(x.row0 + cta * 128);
+        uint32_t nk;
+        if (KIND == kF) {
+          tc::mbar_wait(aempty, aphase ^ 1);
+          aphase ^= 1;
+          if (leader) tc::mbar_expect_tx(afull, 2 * C::ARES_BYTES);
+#pragma unroll 1
+          for (int kc = 0; kc < 8; ++kc)
+            tc::tma_load_2d_2sm(sRes + kc * 16384, &tmA, afull, kc * 64, myrow);
+          nk = (x.t1 - x.t0) * 8;
+        } else if (KIND == kDX) {
+          nk = x.t1 - x.t0;
+        } else {
+          nk = a.bpad / 32;
+        }
+        for (uint32_t k = 0; k < nk; ++k) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          uint8_t* dA = sA + stage * C::A_BYTES;
+          uint8_t* dB = sB + stage * C::B_BYTES;
+          if (KIND == kF) {
+            const uint32_t ct = x.t0 + k / 8, kc = k % 8;
+            tc::tma_load_2d_2sm(dB, &tmB, &full[stage], (int32_t)(kc * 64),
+                                (int32_t)(ct * 256 + cta * 128));
+          } else {
+            const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * 32);
+            if (KIND == kDX) {
+              tc::tma_load_2d_2sm(dA, &tmA, &full[stage], kk, myrow);  // P~ [b][class]
+            } else {
+#pragma unroll
+              for (int j = 0; j < 2; ++j)  // P~ᵀ: this CTA's 128 classes at batch rows kk..
+                tc::tma_load_2d_2sm(dA + j * 4096, &tmA, &full[stage], myrow + j * 64, kk);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)  // this CTA's half of each 256-wide N instruction
+                tc::tma_load_2d_2sm(dB + (j * 2 + h) * 4096, &tmB, &full[stage],
+                                    (int32_t)(256 * j + 128 * cta + 64 * h), kk);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA, one thread) =================
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0, aphase = 0;
+      for (uint32_t u = pair; u < nunits; u += npairs) {
+        const Unit2 x = unit2_of<KIND>(a, mw, u);
+        if (!x.valid) continue;
+        const uint32_t ntile = KIND == kF ? x.t1 - x.t0 : 1;
+        if (KIND == kF) {
+          tc::mbar_wait(afull, aphase);
+          aphase ^= 1;
+        }
+        for (uint32_t t = 0; t < ntile; ++t) {
+          tc::mbar_wait(&tempty[buf], tphase ^ 1);
+          tc::fence_after_sync();
+          const uint32_t dcol = tbase + buf * C::ACC;
+          const uint32_t nk = KIND == kF ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / 32);
+          for (uint32_t k = 0; k < nk; ++k) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::fence_after_sync();
+            const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
+            const uint32_t b0 = tc::smem_u32(sB + stage * C::B_BYTES);
+            if (KIND == kF) {
+              constexpr uint32_t id = tc::idesc_bf16(256, 256, false, false);
+              const uint32_t r0 = tc::smem_u32(sRes + k * 16384);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk)
+                tc::mma_bf16_2sm(dcol, tc::smem_desc(r0 + kk * 32, 16, 1024, tc::kSwizzle128),
+                                 tc::smem_desc(b0 + kk * 32, 16, 1024, tc::kSwizzle128), id,
+                                 (k | kk) != 0);
+            } else {
+              constexpr uint32_t id = tc::idesc_bf16(256, 256, KIND == kDW, true);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 2; ++kk) {
+                const uint64_t da =
+                    KIND == kDX ? tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64)
+                                : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j)
+                  tc::mma_bf16_2sm(dcol + j * 256, da,
+                                   tc::smem_desc(b0 + j * 8192 + kk * 2048, 4096, 1024,
+                                                 tc::kSwizzle128),
+                                   id, (k | kk) != 0);
+              }
+            }
+            tc::mma_commit_2sm(&empty[stage]);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (nk) tc::mma_commit_2sm(&tfull[buf]);
+          else { tc::mbar_arrive_remote(&tfull[buf], 0); tc::mbar_arrive_remote(&tfull[buf], 1); }
+          if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+        }
+        if (KIND == kF) tc::mma_commit_2sm(aempty);  // resident A may be replaced
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs: their own 128 rows) =================
+    const uint32_t q = warp & 3, h = (warp - 4) >> 2, ew = warp - 4;
+    const uint32_t row = q * 32 + lane;
+    const uint32_t lane_addr = (q * 32) << 16;
+    uint8_t* stg = sStg + ew * 2 * C::STG;
+    uint32_t sbuf = 0;
+    uint32_t buf = 0, tphase = 0;
+    auto stage_flush = [&](int32_t c0, int32_t r0) {
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tc::tma_store_2d(&tmOut, stg + sbuf * C::STG, c0, r0);
+        tc::tma_store_commit();
+      }
+      sbuf ^= 1;
+      if (lane == 0) tc::tma_store_wait_read<1>();  // the buffer written next is free again
+      __syncwarp();
+    };
+    for (uint32_t u = pair; u < nunits; u += npairs) {
+      const Unit2 x = unit2_of<KIND>(a, mw, u);
+      if (!x.valid) continue;
+      const uint32_t ntile = KIND == kF ? x.t1 - x.t0 : 1;
+      for (uint32_t t = 0; t < ntile; ++t) {
+        tc::mbar_wait(&tfull[buf], tphase);
+        tc::fence_after_sync();
+        const uint32_t tb = tbase + buf * C::ACC + lane_addr;
+        const int32_t grow0 = (int32_t)(x.row0 + cta * 128 + q * 32);  // this warp's 32 rows
+        if (KIND == kF) {
+          const uint32_t ct = x.t0 + t;
+          const uint32_t b = x.row0 + cta * 128 + row;
+          const bool vrow = b < a.B;
+          const int32_t lc = vrow ? a.label_col[b] : -1;
+          const float k2 = a.scale * 1.4426950408889634f;
+          float sum = 0.f, lab = 0.f;
+          bool has = false;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < 4; ++ch) {
+            const uint32_t col = h * 128 + ch * 32;
+            float v[32];
+            tc::tmem_ld32(tb + col, v);
+            const uint32_t c0 = ct * 256 + col;
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              float e[2];
+#pragma unroll
+              for (int w2 = 0; w2 < 2; ++w2) {
+                const uint32_t c = c0 + j + w2;
+                const bool ok = vrow && c < mw;
+                e[w2] = ok ? exp2f(fmaf(v[j + w2], k2, -k2)) : 0.f;
+                sum += e[w2];
+                if ((int32_t)c == lc) { lab = v[j + w2] * a.scale; has = true; }
+              }
+              pk[j / 2] = pack_bf16(e[0], e[1]);
+            }
+            stage_bf16(stg + sbuf * C::STG, lane, pk);
+            stage_flush((int32_t)c0, grow0);
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
+          if (has) a.labelterm[b] = lab - a.scale;
+        } else if (KIND == kDW && a.out == nullptr) {
+          // Fused normalize-backward + momentum SGD (parallel.cpp:653-667, fccs.cpp:74-89) on
+          // this CTA's 128 active rows.  Each 32x32 chunk of g is transposed through the
+          // swizzled staging buffer so W/V rows are read and written by whole warps (128-B
+          // lines); the row dot g.w_hat is reduced in fp64 across lanes and column halves.
+          const uint32_t cbase = x.row0 + cta * 128 + q * 32;
+          const uint32_t cr = cbase + lane;  // lane r owns row r's metadata
+          const bool vr = cr < mw && *a.err == 0;
+          const uint64_t gr = vr ? (uint64_t)a.active[cr] - a.begin : 0;
+          const float invr = vr ? 1.0f / a.wnorm[cr] : 1.0f;
+          uint8_t* tb_s = stg;  // transpose buffer (32 rows x 128 B, SW128)
+          // row metadata broadcast once per tile: rows r = 0..31 of this warp
+          const float* Wc = a.W;
+          double p[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) p[r] = 0.0;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < 8; ++ch) {
+            const uint32_t col = h * 256 + ch * 32;
+            {
+              float v[32];
+              tc::tmem_ld32(tb + col, v);
+              stage_f32(tb_s, lane, v);
+            }
+            // all 32 rows' W loads in flight before any use (coalesced 128-B row segments)
+            float w[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const uint64_t grw = __shfl_sync(XKNN_FULL_MASK, gr, r);
+              w[r] = Wc[grw * 512 + col + lane];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const float g = *reinterpret_cast<const float*>(
+                  tb_s + r * 128 + (((lane >> 2) ^ (r & 7)) * 16) + (lane & 3) * 4);
+              const float inv = __shfl_sync(XKNN_FULL_MASK, invr, r);
+              p[r] += (double)g * (double)__fmul_rn(w[r], inv);
+            }
+            __syncwarp();
+          }
+          double mydot = 0.0;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const double sr = warp_sum(p[r]);
+            if ((int)lane == r) mydot = sr;
+          }
+          double* xd = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 64);
+          xd[h * 128 + q * 32 + lane] = mydot;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const float ddr = (float)(xd[q * 32 + lane] + xd[128 + q * 32 + lane]);
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const float lr = *a.lr, mu = a.mu, wd = a.wd;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < 8; ++ch) {
+            const uint32_t col = h * 256 + ch * 32;
+            {
+              float v[32];
+              tc::tmem_ld32(tb + col, v);
+              stage_f32(tb_s, lane, v);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r0 = 0; r0 < 32; r0 += 16) {
+              float w[16], vel[16];
+              uint64_t off[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                off[i] = __shfl_sync(XKNN_FULL_MASK, gr, r0 + i) * 512 + col + lane;
+                w[i] = a.W[off[i]];
+                vel[i] = a.V[off[i]];
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int r = r0 + i;
+                const float g = *reinterpret_cast<const float*>(
+                    tb_s + r * 128 + (((lane >> 2) ^ (r & 7)) * 16) + (lane & 3) * 4);
+                const float inv = __shfl_sync(XKNN_FULL_MASK, invr, r);
+                const float dd = __shfl_sync(XKNN_FULL_MASK, ddr, r);
+                const bool vv = __shfl_sync(XKNN_FULL_MASK, vr, r);
+                const float grd =
+                    __fmul_rn(__fsub_rn(g, __fmul_rn(dd, __fmul_rn(w[i], inv))), inv);
+                const float nv =
+                    __fadd_rn(__fadd_rn(__fmul_rn(mu, vel[i]), grd), __fmul_rn(wd, w[i]));
+                if (vv) {
+                  a.V[off[i]] = nv;
+                  a.W[off[i]] = __fsub_rn(w[i], __fmul_rn(lr, nv));
+                }
+              }
+            }
+            __syncwarp();
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+        } else {
+          // dX: split-K partial rows of unit x.id; dW: dW rows (compact active order)
+          const int32_t orow = KIND == kDX ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
+          const bool zero = KIND == kDX && x.t1 == x.t0;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < 8; ++ch) {
+            const uint32_t col = h * 256 + ch * 32;
+            float v[32];
+            if (!zero) {
+              tc::tmem_ld32(tb + col, v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            stage_f32(stg + sbuf * C::STG, lane, v);
+            stage_flush((int32_t)col, orow);
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+        }
+        if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+      }
+    }
+    if (lane == 0) tc::tma_store_wait_all();
+    __syncwarp();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // both CTAs done: no MMA reads peer smem, no remote arrive in flight
+  if (warp == 2) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_2sm<512>(tbase);
+  }
+}
+
 // ---- small fused kernels of the fast path ---------------------------------------------------
 
 // per-row softmax statistics from the GEMM-F tile partials: 32 rows x 32 tile groups per block,
@@ -453,17 +890,17 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
 
 // dX[b][:] = s * r_b * sum_s partial[s][b][:] (fixed split order)
 __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __restrict__ red,
-                            uint32_t B, uint32_t nbt, uint32_t splits, float scale,
-                            float* __restrict__ out) {
+                            uint32_t B, uint32_t nbt, uint32_t splits, uint32_t rows_per_unit,
+                            float scale, float* __restrict__ out) {
   const uint64_t total = (uint64_t)B * 128;  // float4 units (D = 512)
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t b = (uint32_t)(e / 128), c4 = (uint32_t)(e % 128);
-    const uint32_t bt = b / 128, row = b % 128;
+    const uint32_t bt = b / rows_per_unit, row = b % rows_per_unit;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t s = 0; s < splits; ++s) {
       const float4 v = reinterpret_cast<const float4*>(
-          partial + ((uint64_t)(s * nbt + bt) * 128 + row) * 512)[c4];
+          partial + ((uint64_t)(s * nbt + bt) * rows_per_unit + row) * 512)[c4];
       acc.x += v.x;
       acc.y += v.y;
       acc.z += v.z;
@@ -502,14 +939,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw, bool f32 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void*>(base), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -518,17 +956,35 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 
 struct FastState {
   uint32_t bpad = 0, nbt = 0, mwpad = 0, splits = 0;
+  bool pair = true;              // CTA-pair kernels (k_gemm2); XKNN_GEMM_1SM=1 selects k_gemm
+  uint64_t dx_units_cap = 0;
   float* partial_f = nullptr;   // [2 * mwpad/256][bpad]
   float* labelterm = nullptr;   // [bpad]
-  float* partial_dx = nullptr;  // [nbt * splits][128][512]
+  float* partial_dx = nullptr;  // [units][rows per unit][512]
   CUtensorMap mF_A, mF_B, mDX_A, mDX_B, mDW_A, mDW_B;
+  CUtensorMap mF2_B, mPt_st, mDXP_st, mDW_st;
 };
+
+// splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
+// whole waves; at most max_units units
+static uint32_t pair_splits(uint32_t nbp, uint32_t max_units) {
+  uint32_t best = 1;
+  double best_eff = -1;
+  for (uint32_t s = 1; s <= 74 && (uint64_t)nbp * s <= max_units; ++s) {
+    const uint32_t u = nbp * s;
+    const double eff = (double)u / ((double)((u + 73) / 74) * 74);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return best;
+}
 
 xknn_status_t Layer::init_fast() {
   auto* f = new FastState;
   fast = f;
   if (d != 512) return fail_msg(XKNN_ERR_UNSUPPORTED, "BF16 path is specialised for D = 512");
-  f->bpad = (uint32_t)((bmax + 127) / 128 * 128);
+  const char* env1 = getenv("XKNN_GEMM_1SM");
+  f->pair = !(env1 && env1[0] == '1');
+  f->bpad = (uint32_t)((bmax + 255) / 256 * 256);
   f->nbt = f->bpad / 128;
   f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
   ldp = f->mwpad;
@@ -553,7 +1009,13 @@ xknn_status_t Layer::init_fast() {
   XK_CUDA(cudaMemsetAsync(Pt, 0, (uint64_t)f->bpad * ldp * 2, stream));
   XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
   XK_CUDA(dalloc(&f->labelterm, f->bpad));
-  XK_CUDA(dalloc(&f->partial_dx, (uint64_t)f->nbt * f->splits * 128 * 512));
+  f->dx_units_cap = std::max<uint64_t>((uint64_t)f->nbt * f->splits * 128,
+                                        (uint64_t)(f->bpad / 256) *
+                                            pair_splits(f->bpad / 256, 296) * 256);
+  XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
+  // fast path dW holds whole 256-class pair tiles
+  if (dW) cudaFree(dW);
+  XK_CUDA(dalloc(&dW, (uint64_t)f->mwpad * d));
   XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
   bool ok = true;
   ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -562,6 +1024,11 @@ xknn_status_t Layer::init_fast() {
   ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mF2_B, Wsub16, d, f->mwpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mPt_st, Pt, ldp, f->bpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok &= make_map(&f->mDXP_st, f->partial_dx, 512, f->dx_units_cap, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_128B, true);
+  ok &= make_map(&f->mDW_st, dW, 512, f->mwpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true);
   if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   XK_CUDA(cudaFuncSetAttribute(k_gemm<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes<kF>()));
@@ -569,6 +1036,12 @@ xknn_status_t Layer::init_fast() {
                                smem_bytes<kDX>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm<kDW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes<kDW>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm2<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kF>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kDX>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kDW>()));
   return XKNN_OK;
 }
 
@@ -610,7 +1083,14 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.labelterm = f->labelterm;
   // (b) GEMM-F with the fused exp/row-sum/label-logit epilogue
   ga.partial = f->partial_f;
-  k_gemm<kF><<<kNumSMs, 384, smem_bytes<kF>(), stream>>>(f->mF_A, f->mF_B, ga);
+  const uint32_t nbp = (uint32_t)((B + 255) / 256);
+  if (f->pair) {
+    ga.nbt = nbp;
+    ga.splits = pair_splits(nbp, 1u << 30);  // units are (pair tile, class-tile range)
+    k_gemm2<kF><<<kNumSMs, 384, smem_bytes2<kF>(), stream>>>(f->mF_A, f->mF2_B, f->mPt_st, ga);
+  } else {
+    k_gemm<kF><<<kNumSMs, 384, smem_bytes<kF>(), stream>>>(f->mF_A, f->mF_B, ga);
+  }
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over class shards -> loss
@@ -638,17 +1118,37 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.mu = cfg.momentum;
   ga.wd = cfg.weight_decay;
   ga.err = err;
-  k_gemm<kDW><<<kNumSMs, 384, smem_bytes<kDW>(), stream>>>(f->mDW_A, f->mDW_B, ga);
+  if (f->pair) {
+    k_gemm2<kDW><<<kNumSMs, 384, smem_bytes2<kDW>(), stream>>>(f->mDW_A, f->mDW_B, f->mDW_st, ga);
+  } else {
+    k_gemm<kDW><<<kNumSMs, 384, smem_bytes<kDW>(), stream>>>(f->mDW_A, f->mDW_B, ga);
+  }
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
   ga.partial = f->partial_dx;
-  ga.nbt = (uint32_t)((B + 127) / 128);
-  k_gemm<kDX><<<kNumSMs, 384, smem_bytes<kDX>(), stream>>>(f->mDX_A, f->mDX_B, ga);
+  uint32_t dx_rows, dx_tiles, dx_splits;
+  if (f->pair) {
+    dx_rows = 256;
+    dx_tiles = nbp;
+    dx_splits = pair_splits(nbp, 296);
+    ga.nbt = dx_tiles;
+    ga.splits = dx_splits;
+    k_gemm2<kDX><<<kNumSMs, 384, smem_bytes2<kDX>(), stream>>>(f->mDX_A, f->mDX_B, f->mDXP_st,
+                                                               ga);
+  } else {
+    dx_rows = 128;
+    dx_tiles = (uint32_t)((B + 127) / 128);
+    dx_splits = f->splits;
+    ga.nbt = dx_tiles;
+    ga.splits = dx_splits;
+    k_gemm<kDX><<<kNumSMs, 384, smem_bytes<kDX>(), stream>>>(f->mDX_A, f->mDX_B, ga);
+  }
   XK_LAUNCH();
   mark(7);
   k_dx_reduce<<<grid_for(B * 128, 256), 256, 0, stream>>>(f->partial_dx, rowred, (uint32_t)B,
-                                                           ga.nbt, f->splits, cfg.scale, dXpart);
+                                                           dx_tiles, dx_splits, dx_rows, cfg.scale,
+                                                           dXpart);
   XK_LAUNCH();
   const uint64_t bl = B / world;
   if (world > 1)
@@ -659,3 +1159,6 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
 }
 
 }  // namespace xknn
+static_assert(xknn::smem_bytes2<xknn::kF>() <= 232448, "GEMM-F pair smem");
+static_assert(xknn::smem_bytes2<xknn::kDX>() <= 232448, "GEMM-dX pair smem");
+static_assert(xknn::smem_bytes2<xknn::kDW>() <= 232448, "GEMM-dW pair smem");

@@ -12,7 +12,8 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
-                               const unsigned long long* err, cudaStream_t s);
+                               const unsigned long long* err, cudaStream_t s,
+                               unsigned max_grid = 148u * 16u);
 cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
                                     uint64_t rows, uint32_t d, float* out, cudaStream_t s);
 

@@ -90,6 +90,9 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned long long), stream));
   XK_CUDA(dalloc(&loss_dev, 1));
   XK_CUDA(dalloc(&lr_dev, 1));
+  XK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
 
   // cub temp: max over the sorts/scans/selects we run
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
@@ -132,6 +135,9 @@ void Layer::free_all() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
   graph_exec = nullptr;
   if (lr_dev) cudaFree(lr_dev);
+  if (side) cudaStreamDestroy(side);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   free_fast();
 }
 
@@ -157,8 +163,9 @@ xknn_status_t Layer::ensure_mt_cache() {
 
 __global__ void k_set_f32(float* p, float v) { *p = v; }
 
-void Layer::mark(int i) {
+void Layer::mark(int i, cudaStream_t on) {
   if (!prof_on) return;
+  cudaStream_t stream = on ? on : this->stream;
   const uint64_t slot = graph_mode ? 0 : (prof_steps % kRing);
   // inside a stream capture an External record becomes an event-record node fired on replay
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -175,11 +182,11 @@ void Layer::prof_collect(bool all) {
   if (graph_mode) {
     if (!all || prof_steps == 0) return;
     cudaEvent_t* e = &prof_ev[0];
-    cudaEventSynchronize(e[kMarks - 1]);
+    cudaEventSynchronize(e[10]);
     prof_ms.assign(kMarks, 0.0);
     for (int i = 0; i + 1 < kMarks; ++i) {
       float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] = ms;
+      if (i != 10 && cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] = ms;
     }
     prof_done = 1;
     (void)cudaGetLastError();  // never leave a stale error for the caller's runtime
@@ -188,10 +195,10 @@ void Layer::prof_collect(bool all) {
   while (prof_done < prof_steps) {
     if (!all && prof_steps - prof_done < kRing) break;
     cudaEvent_t* e = &prof_ev[(prof_done % kRing) * kMarks];
-    cudaEventSynchronize(e[kMarks - 1]);
+    cudaEventSynchronize(e[10]);
     for (int i = 0; i + 1 < kMarks; ++i) {
       float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] += ms;
+      if (i != 10 && cudaEventElapsedTime(&ms, e[i], e[i + 1]) == cudaSuccess) prof_ms[i] += ms;
     }
     ++prof_done;
   }
@@ -254,6 +261,8 @@ xknn_status_t Layer::run_core(uint64_t B) {
   // (8) normalize-backward + momentum SGD on the active rows only (parallel.cpp:649-667);
   //     fused into the GEMM-dW epilogue in BF16 precision
   mark(8);
+  // (an overlap of this HBM-bound kernel with the L2-bound feature-gradient GEMM on a side
+  //  stream was measured slower: both saturate the memory system)
   if (cfg.precision == XKNN_PREC_FP32_EXACT || !(cfg.flags & XKNN_FLAG_FUSED_UPDATE)) {
     XK_CUDA(launch_update_rows(W, V, dW, active, cnt, mw_cap, begin, D, wnorm, lr_dev,
                                cfg.momentum, cfg.weight_decay, err, stream));

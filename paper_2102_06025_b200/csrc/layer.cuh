@@ -58,6 +58,8 @@ struct Layer {
   xknn_config_t cfg{};
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // overlaps the row update with the feature-gradient GEMM
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint64_t launches = 0;
 
   // ---- persistent state
@@ -147,13 +149,13 @@ struct Layer {
 
   // phase profiler: CUDA events recorded on the layer stream at phase boundaries (a ring of
   // per-step event sets, read back lazily so the timed loop stays asynchronous)
-  static constexpr int kMarks = 11;
+  static constexpr int kMarks = 13;  // 0..10 main stream, 11..12 the side-stream update
   static constexpr int kRing = 64;
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_ms;
   uint64_t prof_steps = 0, prof_done = 0;
-  void mark(int i);
+  void mark(int i, cudaStream_t on = nullptr);
   void prof_collect(bool all);
 
   // BF16 tensor-core path (fast.cu)

@@ -199,8 +199,8 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
-                               const unsigned long long* err, cudaStream_t s) {
-  const unsigned grid = grid_for(max_rows * 32, 256);
+                               const unsigned long long* err, cudaStream_t s, unsigned max_grid) {
+  const unsigned grid = grid_for(max_rows * 32, 256, max_grid);
   XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,
                   wd, err);
   return cudaGetLastError();

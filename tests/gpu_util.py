@@ -12,13 +12,13 @@ def torch_cuda():
 
 
 def make_layer(n, d, p, rank, m, bmax, w_full, graph, *, precision, seed=42, scale=30.0,
-               momentum=0.9, wd=0.0, comm=None):
+               momentum=0.9, wd=0.0, comm=None, **kw):
     import paper_2102_06025_b200 as X
 
     torch = torch_cuda()
     layer = X.KnnSoftmaxLayer(n, d, rank=rank, world=p, m_active=m, max_batch=bmax, scale=scale,
                               momentum=momentum, weight_decay=wd, rng_seed=seed,
-                              precision=precision, comm=comm)
+                              precision=precision, comm=comm, **kw)
     b, e = layer.begin, layer.end
     layer.set_weights(torch.from_numpy(np.ascontiguousarray(w_full[b:e])).cuda())
     kpc, off, flat = O.compress(graph, p, rank)

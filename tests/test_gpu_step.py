@@ -15,7 +15,7 @@ from gpu_util import make_layer, rel_err, torch_cuda
 pytestmark = pytest.mark.gpu
 
 
-def _run(n, d, b, k, m, precision, steps=2, seed=42, lr=0.1, wd=0.0, check_logits=False):
+def _run(n, d, b, k, m, precision, steps=2, seed=42, lr=0.1, wd=0.0, check_logits=False, **kw):
     import paper_2102_06025_b200 as X
 
     torch = torch_cuda()
@@ -23,7 +23,7 @@ def _run(n, d, b, k, m, precision, steps=2, seed=42, lr=0.1, wd=0.0, check_logit
     w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
     g = O.random_graph(n, k, 3)
     shards = [O.compress(g, 1, 0)]
-    layer = make_layer(n, d, 1, 0, m, b, w, g, precision=precision, seed=seed, wd=wd)
+    layer = make_layer(n, d, 1, 0, m, b, w, g, precision=precision, seed=seed, wd=wd, **kw)
     w_or, v_or = w.copy(), np.zeros_like(w)
     out = []
     for step in range(steps):
@@ -76,11 +76,14 @@ def test_step_fp32_exact_weight_decay():
         assert abs(o["loss"] - o["loss_or"]) <= 1e-5 * abs(o["loss_or"])
 
 
-@pytest.mark.parametrize("n,b,k,m", [(100_000, 256, 10, 10_000), (20_000, 512, 10, 2_000)])
-def test_step_bf16(n, b, k, m):
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("n,b,k,m", [(100_000, 256, 10, 10_000), (20_000, 512, 10, 2_000),
+                                     (30_000, 200, 10, 3_001)])
+def test_step_bf16(n, b, k, m, fused):
     import paper_2102_06025_b200 as X
 
-    out, wg, w_or, vg, v_or, w0 = _run(n, 512, b, k, m, X.PREC_BF16, steps=2)
+    out, wg, w_or, vg, v_or, w0 = _run(n, 512, b, k, m, X.PREC_BF16, steps=2, wd=1e-4,
+                                       fused_update=fused)
     for o in out:
         assert abs(o["loss"] - o["loss_or"]) <= 2e-4 * abs(o["loss_or"]), (o["loss"], o["loss_or"])
         assert rel_err(o["gf"], o["gf_or"]) <= 1e-2
