@@ -1,0 +1,63 @@
+"""Class-sharded layer over NCCL on P GPUs vs the oracle at the same shard count P.
+
+Selection is bit-exact per shard (the rank-order concatenation is the reference ActiveSet);
+loss, weights and feature gradients within the precision's bound (test_gpu_step.py)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from gpu_util import rel_err
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ngpus():
+    import torch
+
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("m", [4_000, 400])  # padding branch / over-full ranking branch
+@pytest.mark.parametrize("precision,tol_loss,tol_g", [("fp32", 1e-5, 1e-5), ("bf16", 2e-4, 1e-2)])
+def test_multi_gpu_step(p, m, precision, tol_loss, tol_g, tmp_path):
+    if _ngpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    n, b, k, steps = 40_000, 256, 10, 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + p + (m % 97)}",
+           os.path.join(HERE, "mp_worker.py"), "--out", str(tmp_path), "--num-classes", str(n), "--batch",
+           str(b), "--knn", str(k), "--m-active", str(m), "--steps", str(steps), "--precision", precision]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{i}.npz")) for i in range(p)]
+
+    from mp_worker import problem
+
+    w, g = problem(n, 512, k, 7)
+    shards = [O.compress(g, p, s) for s in range(p)]
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    rng = np.random.default_rng(99)
+    for s in range(steps):
+        x = rng.standard_normal((b, 512)).astype(np.float32)
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        rc, want, ca = O.select_shards("oracle", n, shards, lab, m, 42)
+        assert rc == 0
+        got = np.concatenate([r[f"active_{s}"] for r in res])
+        assert np.array_equal(got, want)  # bit-exact ActiveSet across shards
+        assert all(bool(r[f"contains_{s}"]) for r in res) == ca
+        rc, loss_or, act, gf_or, _ = O.fc_train_step(w_or, v_or, x, lab, shards, m, 42)
+        assert rc == 0 and np.array_equal(act, want)
+        for r in res:
+            assert abs(float(r[f"loss_{s}"]) - loss_or) <= tol_loss * abs(loss_or)
+        gf = np.concatenate([r[f"gf_{s}"] for r in res])
+        assert rel_err(gf, gf_or) <= tol_g
+    wg = np.concatenate([r["w"] for r in res])
+    assert rel_err(wg - w, w_or - w) <= tol_g
+    untouched = np.all(w_or == w, axis=1)
+    assert np.array_equal(wg[untouched], w[untouched])
