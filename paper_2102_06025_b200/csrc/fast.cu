@@ -113,6 +113,13 @@ __device__ __forceinline__ Tile tile_of(const GemmArgs& a, uint32_t mw, uint32_t
   return x;
 }
 
+// 2^x on the MUFU pipe; arguments here lie in [-2s log2 e, 0] (no denormal results for s <= 40)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -677,18 +684,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             tc::tmem_ld32(tb + col, v);
             const uint32_t c0 = ct * 256 + col;
             uint32_t pk[16];
+            if (vrow && c0 + 32 <= mw) {  // interior chunk: 1 FFMA + 1 MUFU.EX2 + 1 FADD each
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              float e[2];
-#pragma unroll
-              for (int w2 = 0; w2 < 2; ++w2) {
-                const uint32_t c = c0 + j + w2;
-                const bool ok = vrow && c < mw;
-                e[w2] = ok ? exp2f(fmaf(v[j + w2], k2, -k2)) : 0.f;
-                sum += e[w2];
-                if ((int32_t)c == lc) { lab = v[j + w2] * a.scale; has = true; }
+              for (int j = 0; j < 32; j += 2) {
+                const float e0 = ex2_approx(fmaf(v[j], k2, -k2));
+                const float e1 = ex2_approx(fmaf(v[j + 1], k2, -k2));
+                sum += e0;
+                sum += e1;
+                pk[j / 2] = pack_bf16(e0, e1);
               }
-              pk[j / 2] = pack_bf16(e[0], e[1]);
+            } else {  // ragged edge: padded classes / batch rows contribute exact zeros
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const bool ok0 = vrow && c0 + j < mw, ok1 = vrow && c0 + j + 1 < mw;
+                const float e0 = ok0 ? ex2_approx(fmaf(v[j], k2, -k2)) : 0.f;
+                const float e1 = ok1 ? ex2_approx(fmaf(v[j + 1], k2, -k2)) : 0.f;
+                sum += e0;
+                sum += e1;
+                pk[j / 2] = pack_bf16(e0, e1);
+              }
+            }
+            if (lc >= (int32_t)c0 && lc < (int32_t)c0 + 32) {  // at most once per row
+              const int32_t idx = lc - (int32_t)c0;
+              float sel = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sel = (j == idx) ? v[j] : sel;
+              lab = sel * a.scale;
+              has = true;
             }
             stage_bf16(stg + sbuf * C::STG, lane, pk);
             stage_flush((int32_t)c0, grow0);
@@ -966,13 +988,15 @@ struct FastState {
 };
 
 // splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
-// whole waves; at most max_units units
+// whole waves: the fewest splits with >= 95% wave efficiency (else the most efficient), at most
+// max_units units
 static uint32_t pair_splits(uint32_t nbp, uint32_t max_units) {
   uint32_t best = 1;
   double best_eff = -1;
   for (uint32_t s = 1; s <= 74 && (uint64_t)nbp * s <= max_units; ++s) {
     const uint32_t u = nbp * s;
     const double eff = (double)u / ((double)((u + 73) / 74) * 74);
+    if (eff >= 0.95) return s;
     if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
   }
   return best;
@@ -1131,7 +1155,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   if (f->pair) {
     dx_rows = 256;
     dx_tiles = nbp;
-    dx_splits = pair_splits(nbp, 296);
+    dx_splits = pair_splits(nbp, 148);
     ga.nbt = dx_tiles;
     ga.splits = dx_splits;
     k_gemm2<kDX><<<kNumSMs, 384, smem_bytes2<kDX>(), stream>>>(f->mDX_A, f->mDX_B, f->mDXP_st,

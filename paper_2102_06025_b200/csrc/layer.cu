@@ -76,8 +76,8 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   const uint64_t m = cfg.m_active;
   XK_CUDA(dalloc(&pick_key, m));
   XK_CUDA(dalloc(&pick_val, m));
-  XK_CUDA(dalloc(&pick_key_s, m));
-  XK_CUDA(dalloc(&pick_val_s, m));
+  XK_CUDA(dalloc(&pick_head, n));  // per complement position, kNone between steps
+  XK_CUDA(cudaMemsetAsync(pick_head, 0xff, n * sizeof(uint32_t), stream));
   XK_CUDA(dalloc(&pred, m));
   XK_CUDA(dalloc(&lw, m));
   XK_CUDA(dalloc(&labels_all, bmax));
@@ -97,8 +97,6 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   // cub temp: max over the sorts/scans/selects we run
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b3, blk_counts, blk_counts, (int)(nblocks + 1), stream);
-  cub::DeviceRadixSort::SortPairs(nullptr, b4, pick_key, pick_key_s, pick_val, pick_val_s,
-                                  (int)std::max<uint64_t>(m, 1), 0, 32, stream);
   cub_tmp_bytes = std::max(std::max(b1, b2), std::max(b3, b4)) + 256;
   XK_CUDA(cudaMalloc(&cub_tmp, cub_tmp_bytes));
 
@@ -124,8 +122,8 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
 
 void Layer::free_all() {
   void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, pos_of,
-                  pool_list, active, blk_counts, mt_cache, pick_key, pick_val, pick_key_s,
-                  pick_val_s, pred, lw, labels_all, label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
+                  pool_list, active, blk_counts, mt_cache, pick_key, pick_val, pick_head,
+                  pred, lw, labels_all, label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
                   Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
                   dXpart, loss_dev};
   for (void* p : ptrs)

@@ -87,9 +87,8 @@ struct Layer {
   uint64_t* mt_cache = nullptr;       // u64[m_active + 64]
   uint64_t mt_len = 0, mt_seed = 0;
   uint32_t* pick_key = nullptr;       // j_i        [M]
-  uint32_t* pick_val = nullptr;       // i          [M]
-  uint32_t* pick_key_s = nullptr;     // sorted     [M]
-  uint32_t* pick_val_s = nullptr;     // sorted     [M]
+  uint32_t* pick_val = nullptr;       // next-in-group links [M]
+  uint32_t* pick_head = nullptr;      // [N] group heads per complement position
   uint32_t* pred = nullptr;           // [M]
   uint32_t* lw = nullptr;             // [M]
   uint32_t* labels_all = nullptr;     // [B]

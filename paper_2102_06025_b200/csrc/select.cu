@@ -81,6 +81,25 @@ __device__ __forceinline__ uint32_t final_word(int mode, const SelState* st, con
   return act[w] | (st->branch == kOverfull ? lab[w] : pool[w]);
 }
 
+// exclusive scan of the per-block counts (nblocks + 1 entries, last is the total), one CTA
+__global__ void k_scan_blocks(const uint32_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
+  using BS = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < n ? in[i] : 0;
+    uint32_t x, tot;
+    BS(tmp).ExclusiveSum(v, x, tot);
+    if (i < n) out[i] = carry + x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
 __global__ void k_bits_count(int mode, SelState* st, const uint32_t* __restrict__ act,
                              const uint32_t* __restrict__ pool, const uint32_t* __restrict__ lab,
                              uint64_t nwords, uint32_t* blk_counts) {
@@ -169,26 +188,19 @@ __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int 
 }
 
 // ---- padding: Lemire draws from the cached mt19937_64 stream
-__global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint64_t m,
-                        uint32_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t sentinel) {
-  const bool pad = st->branch == kPad;
-  const uint64_t need = pad ? st->need : 0;
-  const uint64_t csize = st->csize;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+__global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint32_t* __restrict__ key) {
+  if (st->branch != kPad) return;
+  const uint64_t need = st->need, csize = st->csize;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < need;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    if (i < need) {
-      const uint64_t range = csize - i;  // __uerange = (csize-1) - i + 1
-      const uint64_t u = mt[i];
-      const uint64_t lo = u * range;
-      if (lo < range) {
-        const uint64_t thr = (0ull - range) % range;
-        if (lo < thr) atomicMin(&st->first_rej, (unsigned)i);
-      }
-      key[i] = (uint32_t)(i + __umul64hi(u, range));
-    } else {
-      key[i] = sentinel;
+    const uint64_t range = csize - i;  // __uerange = (csize-1) - i + 1
+    const uint64_t u = mt[i];
+    const uint64_t lo = u * range;
+    if (lo < range) {
+      const uint64_t thr = (0ull - range) % range;
+      if (lo < thr) atomicMin(&st->first_rej, (unsigned)i);
     }
-    val[i] = (uint32_t)i;
+    key[i] = (uint32_t)(i + __umul64hi(u, range));
   }
 }
 
@@ -216,34 +228,39 @@ __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, ui
   }
 }
 
-// pred[i] = last t < i with j_t == j_i (sorted runs are stable: ascending t), and
-// lw[t] = last t' < t with j_t' == t (the swap that last moved a value into position t before
-// step t ran)
-__global__ void k_pred_lw(const SelState* st, const uint32_t* __restrict__ key_s,
-                          const uint32_t* __restrict__ val_s, uint32_t* __restrict__ pred,
-                          uint32_t* __restrict__ lw) {
+// Group the picks by complement position: a singly linked list per position (arbitrary order),
+// heads in a dense u32[N] table that is all-kNone between steps.  Uniform picks collide rarely
+// (~need^2 / 2|C| pairs), so groups have one or two members.
+__global__ void k_link(const SelState* st, const uint32_t* __restrict__ key, uint32_t* head,
+                       uint32_t* __restrict__ nxt, uint32_t* __restrict__ lw) {
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < need; q += gridDim.x * blockDim.x) {
-    const uint32_t j = key_s[q];
-    pred[val_s[q]] = (q > 0 && key_s[q - 1] == j) ? val_s[q - 1] : kNone;
-    // lw for position t = q: upper_bound(q) over key_s[0, need)
-    const uint32_t t = q;
-    uint32_t lo = 0, hi = need;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (key_s[mid] <= t) lo = mid + 1; else hi = mid;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
+    nxt[i] = atomicExch(&head[key[i]], i);
+    lw[i] = kNone;
+  }
+}
+
+// One thread per group (the current list head): within the group of position j,
+//   pred[t] = largest member below t   (the swap that last wrote position j before step t)
+//   lw[j]   = largest member below j   (the last value moved into position j before step j)
+__global__ void k_resolve(const SelState* st, const uint32_t* __restrict__ key,
+                          const uint32_t* __restrict__ head, const uint32_t* __restrict__ nxt,
+                          uint32_t* __restrict__ pred, uint32_t* __restrict__ lw) {
+  if (st->branch != kPad) return;
+  const uint32_t need = (uint32_t)st->need;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
+    const uint32_t j = key[i];
+    if (head[j] != i) continue;
+    uint32_t lwj = kNone;
+    for (uint32_t a = i; a != kNone; a = nxt[a]) {
+      uint32_t p = kNone;
+      for (uint32_t b = i; b != kNone; b = nxt[b])
+        if (b < a && (p == kNone || b > p)) p = b;
+      pred[a] = p;
+      if (a < j && (lwj == kNone || a > lwj)) lwj = a;
     }
-    uint32_t r = kNone;
-    if (lo > 0 && key_s[lo - 1] == t) {
-      const uint32_t p = lo - 1;
-      if (val_s[p] == t) {
-        if (p > 0 && key_s[p - 1] == t) r = val_s[p - 1];
-      } else {
-        r = val_s[p];
-      }
-    }
-    lw[t] = r;
+    if (j < need) lw[j] = lwj;
   }
 }
 
@@ -251,13 +268,14 @@ __global__ void k_pred_lw(const SelState* st, const uint32_t* __restrict__ key_s
 __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ pred, const uint32_t* __restrict__ lw,
                           const uint32_t* __restrict__ pool_list, uint64_t begin,
-                          uint32_t* act_bits) {
+                          uint32_t* act_bits, uint32_t* head) {
   if (st->branch != kPad) return;
   const uint64_t need = st->need, cbase = st->cbase, cl = st->compl_local;
   const uint32_t npool = st->pool_count;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < need;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t src;
+    head[key[i]] = kNone;  // leave the group table clean for the next step
     uint32_t t = pred[i];
     if (t != kNone) {
       while (lw[t] != kNone) t = lw[t];
@@ -393,8 +411,15 @@ __global__ void k_of_select(SelState* st, const uint32_t* __restrict__ pool_list
 __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ labels,
                              uint32_t batch, const uint32_t* __restrict__ active,
                              const uint32_t* __restrict__ pos_of, uint64_t begin, uint64_t end,
-                             int32_t* label_col) {
-  const uint32_t na = st->active_count;
+                             int32_t* label_col, const uint32_t* __restrict__ pool_list,
+                             uint32_t* best, uint32_t* occ) {
+  const uint32_t na = st->active_count, np = st->pool_count;
+  // reset the candidate ranks of this step's pool (every touched class is in the pool)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const uint32_t lc = pool_list[i] - (uint32_t)begin;
+    best[lc] = kNone;
+    occ[lc] = 0;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += gridDim.x * blockDim.x) {
     const uint32_t y = labels[i];
     int32_t col = -1;
@@ -422,10 +447,7 @@ static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* p
                                                         L.lab_bits, L.nwords, L.blk_counts);
   ++L.launches;
   // blk_counts[nblocks] is kept 0, so the exclusive scan's last entry is the total
-  size_t bytes = L.cub_tmp_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(L.cub_tmp, bytes, L.blk_counts,
-                                                L.blk_counts + nblocks + 1, nblocks + 1, L.stream);
-  if (e != cudaSuccess) return L.cuda_ok(e, __FILE__, __LINE__, "DeviceScan");
+  k_scan_blocks<<<1, 1024, 0, L.stream>>>(L.blk_counts, nblocks + 1, L.blk_counts + nblocks + 1);
   ++L.launches;
   k_bits_write<<<nblocks, kCompactBlock, 0, L.stream>>>(
       mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
@@ -458,22 +480,16 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
 
   // (3a) padding branch (|pool| < M): picks from the cached stream, Fisher-Yates chains
   if (m > 0) {
-    uint32_t bits = 1;
-    while (bits < 32 && (1ull << bits) <= n) ++bits;
-    if (bits < 32) ++bits;
-    const uint32_t sentinel = bits >= 32 ? 0xffffffffu : (uint32_t)((1ull << bits) - 1);
-    k_picks<<<grid_for(m, 256), 256, 0, stream>>>(st, mt_cache, m, pick_key, pick_val, sentinel);
+    k_picks<<<grid_for(m, 256), 256, 0, stream>>>(st, mt_cache, pick_key);
     XK_LAUNCH();
     k_picks_replay<<<1, 1, 0, stream>>>(st, mt_cache, mt_len, pick_key, err);
     XK_LAUNCH();
-    size_t bytes = cub_tmp_bytes;
-    XK_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, pick_key, pick_key_s, pick_val,
-                                            pick_val_s, (int)m, 0, (int)bits, stream));
-    launches += 3;
-    k_pred_lw<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key_s, pick_val_s, pred, lw);
+    k_link<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pick_head, pick_val, lw);
+    XK_LAUNCH();
+    k_resolve<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pick_head, pick_val, pred, lw);
     XK_LAUNCH();
     k_pad_map<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pred, lw, pool_list, begin,
-                                                     act_bits);
+                                                     act_bits, pick_head);
     XK_LAUNCH();
   }
   // (3b) over-full branch: only reachable when B * k could exceed M
@@ -507,13 +523,8 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
   }
   // (4) this shard's ActiveSet slice, sorted by construction; label -> column map
   XK_TRY(compact_bits(*this, 1, active, pos_of));
-  k_label_cols<<<grid_for(B, 256), 256, 0, stream>>>(st, labels_all, B, active, pos_of, begin, end,
-                                                      label_col);
-  XK_LAUNCH();
-  // (5) reset the candidate ranks touched this step
-  k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
-      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
-      st, err, 1);
+  k_label_cols<<<grid_for(std::max<uint64_t>(B, (uint64_t)B * g_kmax), 256), 256, 0, stream>>>(
+      st, labels_all, B, active, pos_of, begin, end, label_col, pool_list, sel_best, sel_occ);
   XK_LAUNCH();
   return XKNN_OK;
 }
