@@ -169,6 +169,16 @@ xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out_host, uint64_t 
 xknn_status_t xknn_layer_profile(xknn_layer_t* h, int enable);
 xknn_status_t xknn_layer_phase_ms(xknn_layer_t* h, double* out_ms, int n, uint64_t* steps);
 
+/* build_graph_bruteforce (knn_graph.cpp:124-145): the exact KNN graph of the normalized class
+   weights w_norm_dev (num_classes x dim fp32, device), k neighbours per class, self first, then
+   descending inner product (the reference's fp32 ascending-d sum), ties to the lower index.
+   Bit-exact: a bf16 tensor-core pass keeps the top kprime candidates per row, candidates are
+   re-scored exactly, and rows whose certificate fails are recomputed by an exact scan
+   (*uncertified_rows counts them).  out_dev: num_classes x k u32.  Synchronizes `stream`. */
+xknn_status_t xknn_graph_bruteforce(const float* w_norm_dev, uint64_t num_classes, uint64_t dim,
+                                    uint32_t k, uint32_t kprime, uint32_t* out_dev, void* stream,
+                                    uint64_t* uncertified_rows);
+
 /* Kernel launch counter (all kernels this library launched on this layer since creation). */
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);
 

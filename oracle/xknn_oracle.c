@@ -535,6 +535,34 @@ int or_build_graph_bruteforce(uint64_t n, uint64_t d, const float* w, uint64_t k
   return OR_OK;
 }
 
+/* One row of build_graph_bruteforce: the exact k neighbours of class j (same arithmetic and
+   ordering), for sampled-row checks at sizes where the full O(N^2 D) oracle is too slow. */
+int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k, uint32_t* out) {
+  if (k > n) return OR_ERR_K_TOO_LARGE;
+  if (k == 0) return OR_ERR_INVALID_ARGUMENT;
+  float* sc = (float*)malloc(k * sizeof(float));
+  uint32_t* ix = (uint32_t*)malloc(k * sizeof(uint32_t));
+  uint64_t sz = 0;
+  const float* wj = w + j * d;
+  for (uint64_t i = 0; i < n; ++i) {
+    const float* wi = w + i * d;
+    float dot = 0.0f;
+    for (uint64_t t = 0; t < d; ++t) dot += wj[t] * wi[t];
+    if (sz == k && !better(dot, (uint32_t)i, sc[sz - 1], ix[sz - 1], (uint32_t)j)) continue;
+    uint64_t pos = 0;
+    while (pos < sz && better(sc[pos], ix[pos], dot, (uint32_t)i, (uint32_t)j)) ++pos;
+    uint64_t last = sz < k ? sz : k - 1;
+    for (uint64_t q = last; q > pos; --q) { sc[q] = sc[q - 1]; ix[q] = ix[q - 1]; }
+    sc[pos] = dot;
+    ix[pos] = (uint32_t)i;
+    if (sz < k) ++sz;
+  }
+  memcpy(out, ix, k * sizeof(uint32_t));
+  free(sc);
+  free(ix);
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* The fc half of HybridSim::train_step in kKnn mode with one micro-batch    */
 /* (parallel.cpp:455-572, :638-668), the composite the device layer replaces. */

@@ -104,6 +104,7 @@ for _name, _args in {
     "xknn_layer_sync": [VP],
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_last_logits": [VP, VP, U64],
+    "xknn_graph_bruteforce": [VP, U64, U64, C.c_uint32, C.c_uint32, VP, VP, C.POINTER(U64)],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
@@ -149,6 +150,20 @@ def nccl_comm_init(uid: bytes, world: int, rank: int) -> int:
 
 def nccl_comm_destroy(comm) -> None:
     _check(_lib.xknn_nccl_comm_destroy(comm))
+
+
+def graph_bruteforce(w_norm, k: int, kprime: int = 0):
+    """build_graph_bruteforce(w_norm, k) (knn_graph.cpp:124-145) on device, bit-exact.
+    w_norm: (N, D) fp32 CUDA tensor of unit rows.  Returns ((N, k) int32 tensor, uncertified)."""
+    import torch
+
+    w = w_norm.contiguous()
+    n, d = w.shape
+    out = torch.empty(n, k, dtype=torch.int32, device=w.device)
+    unc = U64()
+    _check(_lib.xknn_graph_bruteforce(w.data_ptr(), n, d, k, kprime, out.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream, C.byref(unc)))
+    return out, unc.value
 
 
 def _ptr(t) -> int:

@@ -22,7 +22,7 @@ namespace xknn {
 
 namespace {
 
-enum Kind : int { kF = 0, kDX = 1, kDW = 2 };
+enum Kind : int { kF = 0, kDX = 1, kDW = 2, kG = 3 };
 
 template <int KIND>
 struct Cfg;
@@ -73,6 +73,11 @@ struct GemmArgs {
   const float* lr;
   float mu, wd;
   const unsigned long long* err;
+  // graph build (kG): candidate regions [row][half][ch] of (approx score, column)
+  float2* cand;
+  uint32_t* cnt;
+  float* tau;
+  uint32_t ch, kprime, nrows;
 };
 
 struct Tile {
@@ -428,6 +433,13 @@ struct Cfg2<kDW> {
   static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096;
 };
 
+template <>
+struct Cfg2<kG> {
+  static constexpr uint32_t STAGES = 6, A_BYTES = 0, B_BYTES = 128 * 64 * 2;
+  static constexpr uint32_t ARES_BYTES = 8 * 128 * 64 * 2;
+  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 0;
+};
+
 template <int KIND>
 constexpr uint32_t smem_bytes2() {
   using C = Cfg2<KIND>;
@@ -445,6 +457,7 @@ struct Unit2 {
 template <int KIND>
 __device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
   if (KIND == kDW) return (mw + 255) / 256;
+  if (KIND == kG) return (a.nrows + 255) / 256;
   return a.nbt * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per pair-tile
 }
 
@@ -454,6 +467,13 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
   x.id = u;
   if (KIND == kDW) {
     x.row0 = u * 256;
+    x.valid = true;
+    return x;
+  }
+  if (KIND == kG) {  // one 256-row query block against every 256-column tile
+    x.row0 = u * 256;
+    x.t0 = 0;
+    x.t1 = (a.nrows + 255) / 256;
     x.valid = true;
     return x;
   }
@@ -483,6 +503,17 @@ __device__ __forceinline__ void stage_bf16(uint8_t* buf, uint32_t r, const uint3
   }
 }
 
+// order-preserving float -> uint32 key (larger score, larger key)
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Region full: the new cut is the kprime-th largest score; keep the entries strictly above it.
+// Every dropped (and every later rejected) column has approx score <= the returned cut.
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -532,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
 
-  const uint32_t mw = a.st->active_count;
+  const uint32_t mw = KIND == kG ? a.nrows : a.st->active_count;
   const uint32_t nunits = num_units2<KIND>(a, mw);
 
   if (warp == 0) {
@@ -544,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (!x.valid) continue;
         const int32_t myrow = (int32_t)(x.row0 + cta * 128);
         uint32_t nk;
-        if (KIND == kF) {
+        if (KIND == kF || KIND == kG) {
           tc::mbar_wait(aempty, aphase ^ 1);
           aphase ^= 1;
           if (leader) tc::mbar_expect_tx(afull, 2 * C::ARES_BYTES);
@@ -562,7 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
           uint8_t* dA = sA + stage * C::A_BYTES;
           uint8_t* dB = sB + stage * C::B_BYTES;
-          if (KIND == kF) {
+          if (KIND == kF || KIND == kG) {
             const uint32_t ct = x.t0 + k / 8, kc = k % 8;
             tc::tma_load_2d_2sm(dB, &tmB, &full[stage], (int32_t)(kc * 64),
                                 (int32_t)(ct * 256 + cta * 128));
@@ -593,8 +624,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (uint32_t u = pair; u < nunits; u += npairs) {
         const Unit2 x = unit2_of<KIND>(a, mw, u);
         if (!x.valid) continue;
-        const uint32_t ntile = KIND == kF ? x.t1 - x.t0 : 1;
-        if (KIND == kF) {
+        const uint32_t ntile = (KIND == kF || KIND == kG) ? x.t1 - x.t0 : 1;
+        if (KIND == kF || KIND == kG) {
           tc::mbar_wait(afull, aphase);
           aphase ^= 1;
         }
@@ -602,13 +633,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           tc::mbar_wait(&tempty[buf], tphase ^ 1);
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
-          const uint32_t nk = KIND == kF ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / 32);
+          const uint32_t nk =
+              (KIND == kF || KIND == kG) ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / 32);
           for (uint32_t k = 0; k < nk; ++k) {
             tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
             const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
             const uint32_t b0 = tc::smem_u32(sB + stage * C::B_BYTES);
-            if (KIND == kF) {
+            if (KIND == kF || KIND == kG) {
               constexpr uint32_t id = tc::idesc_bf16(256, 256, false, false);
               const uint32_t r0 = tc::smem_u32(sRes + k * 16384);
 #pragma unroll
@@ -638,7 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           else { tc::mbar_arrive_remote(&tfull[buf], 0); tc::mbar_arrive_remote(&tfull[buf], 1); }
           if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
         }
-        if (KIND == kF) tc::mma_commit_2sm(aempty);  // resident A may be replaced
+        if (KIND == kF || KIND == kG) tc::mma_commit_2sm(aempty);  // resident A may be replaced
       }
     }
   } else if (warp >= 4) {
@@ -663,13 +695,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     for (uint32_t u = pair; u < nunits; u += npairs) {
       const Unit2 x = unit2_of<KIND>(a, mw, u);
       if (!x.valid) continue;
-      const uint32_t ntile = KIND == kF ? x.t1 - x.t0 : 1;
+      const uint32_t ntile = (KIND == kF || KIND == kG) ? x.t1 - x.t0 : 1;
+      // kG: this thread's (row, column half) candidate region state for the whole unit
+      const uint32_t grow = x.row0 + cta * 128 + row;
+      float2* creg = KIND == kG ? a.cand + ((uint64_t)grow * 2 + h) * a.ch : nullptr;
+      uint32_t ccnt = 0;
+      float ctau = -INFINITY;
       for (uint32_t t = 0; t < ntile; ++t) {
         tc::mbar_wait(&tfull[buf], tphase);
         tc::fence_after_sync();
         const uint32_t tb = tbase + buf * C::ACC + lane_addr;
         const int32_t grow0 = (int32_t)(x.row0 + cta * 128 + q * 32);  // this warp's 32 rows
-        if (KIND == kF) {
+        if (KIND == kG) {
+          // threshold top-k' of approximate scores: insert columns above the current cut;
+          // when the region fills, raise the cut to its kprime-th largest score and compact
+          const bool vrow = grow < a.nrows;
+          const uint32_t cap = a.ch, kp = a.kprime;
+#pragma unroll 1
+          for (uint32_t chk = 0; chk < 4; ++chk) {
+            const uint32_t col = h * 128 + chk * 32;
+            float v[32];
+            tc::tmem_ld32(tb + col, v);
+            const uint32_t c0 = t * 256 + col;
+            uint32_t mask = 0;  // columns of this chunk above the current cut
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const uint32_t c = c0 + j;
+              if (vrow && v[j] > ctau && c < a.nrows && c != grow) mask |= 1u << j;
+            }
+            float sc[32];  // spill-friendly copy for the (rare) dynamic-index inserts
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sc[j] = v[j];
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              if (!(sc[j] > ctau)) continue;  // the cut may have risen since the mask
+              if (ccnt >= cap) {
+                // region full: new cut = kprime-th largest score; keep entries above it
+                uint32_t lo = 0, hi = 0xffffffffu;
+#pragma unroll 1
+                while (lo < hi) {
+                  const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
+                  uint32_t cntge = 0;
+#pragma unroll 1
+                  for (uint32_t i = 0; i < ccnt; ++i) cntge += fkey(creg[i].x) >= mid;
+                  if (cntge >= kp) lo = mid; else hi = mid - 1;
+                }
+                ctau = funkey(lo);
+                uint32_t w = 0;
+#pragma unroll 1
+                for (uint32_t i = 0; i < ccnt; ++i)
+                  if (creg[i].x > ctau) creg[w++] = creg[i];
+                ccnt = w;
+                if (!(sc[j] > ctau)) continue;
+              }
+              creg[ccnt++] = make_float2(sc[j], __uint_as_float(c0 + j));
+            }
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          if (t + 1 == ntile && vrow) {
+            a.cnt[grow * 2 + h] = ccnt;
+            a.tau[grow * 2 + h] = ctau;
+          }
+        } else if (KIND == kF) {
           const uint32_t ct = x.t0 + t;
           const uint32_t b = x.row0 + cta * 128 + row;
           const bool vrow = b < a.B;
@@ -1186,3 +1276,36 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
 static_assert(xknn::smem_bytes2<xknn::kF>() <= 232448, "GEMM-F pair smem");
 static_assert(xknn::smem_bytes2<xknn::kDX>() <= 232448, "GEMM-dX pair smem");
 static_assert(xknn::smem_bytes2<xknn::kDW>() <= 232448, "GEMM-dW pair smem");
+static_assert(xknn::smem_bytes2<xknn::kG>() <= 232448, "graph GEMM pair smem");
+
+namespace xknn {
+
+// GEMM + threshold top-k' candidate pass of the graph build (graph.cu): Wb is the bf16 copy of
+// the normalized class weights (npad x 512, zero pad rows).
+cudaError_t launch_graph_candidates(const __nv_bfloat16* Wb, uint32_t n, uint32_t npad,
+                                    float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
+                                    uint32_t kprime, cudaStream_t s) {
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, Wb, 512, npad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mB, Wb, 512, npad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm2<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem_bytes2<kG>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  GemmArgs ga{};
+  ga.nrows = n;
+  ga.cand = cand;
+  ga.cnt = cnt;
+  ga.tau = tau;
+  ga.ch = ch;
+  ga.kprime = kprime;
+  ga.dim = 512;
+  k_gemm2<kG><<<kNumSMs, 384, smem_bytes2<kG>(), s>>>(mA, mB, mA, ga);
+  return cudaGetLastError();
+}
+
+}  // namespace xknn

@@ -198,6 +198,16 @@ def bruteforce_graph(lib_kind: str, w_norm: np.ndarray, k: int):
     return rc, out
 
 
+def graph_row(w_norm: np.ndarray, j: int, k: int) -> np.ndarray:
+    n, d = w_norm.shape
+    out = np.zeros(k, np.uint32)
+    fn = oracle().or_graph_row
+    fn.restype = C.c_int
+    fn.argtypes = [U64, U64, f32p, U64, U64, u32p]
+    assert fn(n, d, np.ascontiguousarray(w_norm, np.float32), j, k, out) == 0
+    return out
+
+
 def l2_normalize(x: np.ndarray):
     x = np.ascontiguousarray(x, np.float32)
     r, c = x.shape
