@@ -701,6 +701,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       float2* creg = KIND == kG ? a.cand + ((uint64_t)grow * 2 + h) * a.ch : nullptr;
       uint32_t ccnt = 0;
       float ctau = -INFINITY;
+      if (KIND == kDW && a.out == nullptr && grow < mw) {
+        // fused update: pull this thread's W and V row halves into L2 while the MMA runs
+        const uint64_t off = ((uint64_t)a.active[grow] - a.begin) * 512 + h * 256;
+        tc::prefetch_l2_bulk(a.W + off, 1024);
+        tc::prefetch_l2_bulk(a.V + off, 1024);
+      }
       for (uint32_t t = 0; t < ntile; ++t) {
         tc::mbar_wait(&tfull[buf], tphase);
         tc::fence_after_sync();
@@ -812,20 +818,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (has) a.labelterm[b] = lab - a.scale;
         } else if (KIND == kDW && a.out == nullptr) {
           // Fused normalize-backward + momentum SGD (parallel.cpp:653-667, fccs.cpp:74-89) on
-          // this CTA's 128 active rows.  Each 32x32 chunk of g is transposed through the
-          // swizzled staging buffer so W/V rows are read and written by whole warps (128-B
-          // lines); the row dot g.w_hat is reduced in fp64 across lanes and column halves.
-          const uint32_t cbase = x.row0 + cta * 128 + q * 32;
-          const uint32_t cr = cbase + lane;  // lane r owns row r's metadata
+          // this CTA's 128 active rows; this warp owns rows q*32.. and column half h.  Each
+          // 32x32 chunk of g is transposed through the swizzled staging buffer, then lane l
+          // works on row 4*i + l/8, columns 4*(l%8).. of the chunk: float4 accesses, four
+          // 128-B row segments per instruction.  W/V were prefetched into L2 above.
+          const uint32_t cr = x.row0 + cta * 128 + row;  // lane r owns row r's metadata
           const bool vr = cr < mw && *a.err == 0;
-          const uint64_t gr = vr ? (uint64_t)a.active[cr] - a.begin : 0;
+          const uint32_t gr = vr ? a.active[cr] - (uint32_t)a.begin : 0;
           const float invr = vr ? 1.0f / a.wnorm[cr] : 1.0f;
+          const uint32_t sub = lane >> 3, c4 = lane & 7;
           uint8_t* tb_s = stg;  // transpose buffer (32 rows x 128 B, SW128)
-          // row metadata broadcast once per tile: rows r = 0..31 of this warp
-          const float* Wc = a.W;
-          double p[32];
+          uint32_t rg[8];
+          float rinv[8];
+          bool rv[8];
 #pragma unroll
-          for (int r = 0; r < 32; ++r) p[r] = 0.0;
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t r = 4 * i + sub;
+            rg[i] = __shfl_sync(XKNN_FULL_MASK, gr, r);
+            rinv[i] = __shfl_sync(XKNN_FULL_MASK, invr, r);
+            rv[i] = __shfl_sync(XKNN_FULL_MASK, vr, r);
+          }
+          double p[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) p[i] = 0.0;
 #pragma unroll 1
           for (uint32_t ch = 0; ch < 8; ++ch) {
             const uint32_t col = h * 256 + ch * 32;
@@ -834,33 +849,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               tc::tmem_ld32(tb + col, v);
               stage_f32(tb_s, lane, v);
             }
-            // all 32 rows' W loads in flight before any use (coalesced 128-B row segments)
-            float w[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-              const uint64_t grw = __shfl_sync(XKNN_FULL_MASK, gr, r);
-              w[r] = Wc[grw * 512 + col + lane];
-            }
             __syncwarp();
+            float4 w4[8];
 #pragma unroll
-            for (int r = 0; r < 32; ++r) {
-              const float g = *reinterpret_cast<const float*>(
-                  tb_s + r * 128 + (((lane >> 2) ^ (r & 7)) * 16) + (lane & 3) * 4);
-              const float inv = __shfl_sync(XKNN_FULL_MASK, invr, r);
-              p[r] += (double)g * (double)__fmul_rn(w[r], inv);
+            for (int i = 0; i < 8; ++i)
+              w4[i] = rv[i] ? *reinterpret_cast<const float4*>(a.W + (uint64_t)rg[i] * 512 + col +
+                                                               c4 * 4)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t r = 4 * i + sub;
+              const float4 g = *reinterpret_cast<const float4*>(tb_s + r * 128 +
+                                                                ((c4 ^ (r & 7)) * 16));
+              p[i] += (double)g.x * (double)__fmul_rn(w4[i].x, rinv[i]);
+              p[i] += (double)g.y * (double)__fmul_rn(w4[i].y, rinv[i]);
+              p[i] += (double)g.z * (double)__fmul_rn(w4[i].z, rinv[i]);
+              p[i] += (double)g.w * (double)__fmul_rn(w4[i].w, rinv[i]);
             }
             __syncwarp();
           }
-          double mydot = 0.0;
+          // row dots: the 8 lanes of a row, then the two column halves
 #pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            const double sr = warp_sum(p[r]);
-            if ((int)lane == r) mydot = sr;
+          for (int i = 0; i < 8; ++i) {
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) p[i] += __shfl_xor_sync(XKNN_FULL_MASK, p[i], o);
           }
           double* xd = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 64);
-          xd[h * 128 + q * 32 + lane] = mydot;
+          if (c4 == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xd[h * 128 + q * 32 + 4 * i + sub] = p[i];
+          }
           asm volatile("bar.sync 1, 256;" ::: "memory");
-          const float ddr = (float)(xd[q * 32 + lane] + xd[128 + q * 32 + lane]);
+          float rdd[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t r = q * 32 + 4 * i + sub;
+            rdd[i] = (float)(xd[r] + xd[128 + r]);
+          }
           asm volatile("bar.sync 1, 256;" ::: "memory");
           const float lr = *a.lr, mu = a.mu, wd = a.wd;
 #pragma unroll 1
@@ -872,33 +897,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               stage_f32(tb_s, lane, v);
             }
             __syncwarp();
+            float4 w4[8], v4[8];
 #pragma unroll
-            for (int r0 = 0; r0 < 32; r0 += 16) {
-              float w[16], vel[16];
-              uint64_t off[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                off[i] = __shfl_sync(XKNN_FULL_MASK, gr, r0 + i) * 512 + col + lane;
-                w[i] = a.W[off[i]];
-                vel[i] = a.V[off[i]];
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t off = (uint64_t)rg[i] * 512 + col + c4 * 4;
+              if (rv[i]) {
+                w4[i] = *reinterpret_cast<const float4*>(a.W + off);
+                v4[i] = *reinterpret_cast<const float4*>(a.V + off);
               }
+            }
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const int r = r0 + i;
-                const float g = *reinterpret_cast<const float*>(
-                    tb_s + r * 128 + (((lane >> 2) ^ (r & 7)) * 16) + (lane & 3) * 4);
-                const float inv = __shfl_sync(XKNN_FULL_MASK, invr, r);
-                const float dd = __shfl_sync(XKNN_FULL_MASK, ddr, r);
-                const bool vv = __shfl_sync(XKNN_FULL_MASK, vr, r);
-                const float grd =
-                    __fmul_rn(__fsub_rn(g, __fmul_rn(dd, __fmul_rn(w[i], inv))), inv);
-                const float nv =
-                    __fadd_rn(__fadd_rn(__fmul_rn(mu, vel[i]), grd), __fmul_rn(wd, w[i]));
-                if (vv) {
-                  a.V[off[i]] = nv;
-                  a.W[off[i]] = __fsub_rn(w[i], __fmul_rn(lr, nv));
-                }
-              }
+            for (int i = 0; i < 8; ++i) {
+              if (!rv[i]) continue;
+              const uint32_t r = 4 * i + sub;
+              const float4 g = *reinterpret_cast<const float4*>(tb_s + r * 128 +
+                                                                ((c4 ^ (r & 7)) * 16));
+              const float inv = rinv[i], dd = rdd[i];
+              float4 w = w4[i], v = v4[i];
+#define XKNN_FUPD(c)                                                                         \
+  {                                                                                          \
+    const float grd = __fmul_rn(__fsub_rn(g.c, __fmul_rn(dd, __fmul_rn(w.c, inv))), inv);    \
+    v.c = __fadd_rn(__fadd_rn(__fmul_rn(mu, v.c), grd), __fmul_rn(wd, w.c));                 \
+    w.c = __fsub_rn(w.c, __fmul_rn(lr, v.c));                                                \
+  }
+              XKNN_FUPD(x) XKNN_FUPD(y) XKNN_FUPD(z) XKNN_FUPD(w)
+#undef XKNN_FUPD
+              const uint64_t off = (uint64_t)rg[i] * 512 + col + c4 * 4;
+              *reinterpret_cast<float4*>(a.V + off) = v;
+              *reinterpret_cast<float4*>(a.W + off) = w;
             }
             __syncwarp();
           }
