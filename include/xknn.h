@@ -172,12 +172,45 @@ xknn_status_t xknn_layer_phase_ms(xknn_layer_t* h, double* out_ms, int n, uint64
 /* build_graph_bruteforce (knn_graph.cpp:124-145): the exact KNN graph of the normalized class
    weights w_norm_dev (num_classes x dim fp32, device), k neighbours per class, self first, then
    descending inner product (the reference's fp32 ascending-d sum), ties to the lower index.
-   Bit-exact: a bf16 tensor-core pass keeps the top kprime candidates per row, candidates are
-   re-scored exactly, and rows whose certificate fails are recomputed by an exact scan
-   (*uncertified_rows counts them).  out_dev: num_classes x k u32.  Synchronizes `stream`. */
+   Bit-exact: an fp16 tensor-core pass keeps up to kprime candidates per row (0 = default,
+   max(2k, k+32)) above a cut, the window that can reach the top k is re-scored exactly, and
+   rows whose certificate fails are recomputed by an exact scan (*uncertified_rows counts them).  out_dev: num_classes x k u32.  Synchronizes `stream`. */
 xknn_status_t xknn_graph_bruteforce(const float* w_norm_dev, uint64_t num_classes, uint64_t dim,
                                     uint32_t k, uint32_t kprime, uint32_t* out_dev, void* stream,
                                     uint64_t* uncertified_rows);
+
+/* build_graph_ring (knn_graph.cpp:147-233) over the class blocks of `world` ranks, one process
+   per GPU: w_norm_local_dev holds this rank's block of the ShardLayout(num_classes, world)
+   (knn_graph.cpp:94-115) -- its normalized class weights, (end - begin) x dim fp32, device.
+   The blocks travel around the ring over `comm` (ncclComm_t; rank -> rank+1, world-1 hops,
+   RingBuildStats::transfer_steps) while every rank scores its own rows against them.  Writes
+   rows [begin, end) of the graph (x k u32, global ids) to out_rows_dev; identical to
+   build_graph_bruteforce on the concatenated blocks (bit-exact, see xknn_graph_bruteforce).
+   k' >= k (else InvalidArgument, as the reference); it only sizes the candidate lists here.
+   Collective: every rank calls it.  dim must be 512 when world > 1.  Synchronizes `stream`. */
+xknn_status_t xknn_graph_ring(const float* w_norm_local_dev, uint64_t num_classes, uint64_t dim,
+                             uint32_t k, uint32_t kprime, int rank, int world, void* comm,
+                             void* stream, uint32_t* out_rows_dev, uint64_t* uncertified_rows,
+                             uint64_t* transfer_steps);
+
+/* compress_graph (knn_graph.cpp:235-266) + HybridSim::set_shard_graphs (parallel.cpp:381-388)
+   from the row-distributed full graph: every rank passes its rows [begin, end) x k (global ids,
+   device), entries are exchanged all-to-all by owning shard, and each layer installs its
+   CompressedKnnGraph.  Collective.  Synchronizes. */
+xknn_status_t xknn_layer_set_graph_rows(xknn_layer_t* h, const uint32_t* rows_dev, uint32_t k);
+
+/* The periodic graph refresh of the paper on the live layer: l2_normalize_rows of every rank's
+   weight shard (matrix.cpp:12-29, bit-exact; ZeroNormRow), xknn_graph_ring over the shards,
+   then xknn_layer_set_graph_rows.  Collective.  Synchronizes. */
+xknn_status_t xknn_layer_rebuild_graph(xknn_layer_t* h, uint32_t k, uint32_t kprime,
+                                       uint64_t* uncertified_rows);
+
+/* The installed CompressedKnnGraph of this shard (knn_graph.hpp:46-55): k_per_class and
+   offsets [num_classes], flat [*flat_len] (flat_capacity >= *flat_len, else ShapeMismatch);
+   NULL arrays are skipped.  Synchronizes. */
+xknn_status_t xknn_layer_get_graph(xknn_layer_t* h, uint32_t* k_per_class, uint64_t* offsets,
+                                   uint32_t* flat, uint64_t flat_capacity, uint64_t* flat_len,
+                                   int on_device);
 
 /* Kernel launch counter (all kernels this library launched on this layer since creation). */
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);

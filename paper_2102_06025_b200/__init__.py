@@ -105,6 +105,11 @@ for _name, _args in {
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_last_logits": [VP, VP, U64],
     "xknn_graph_bruteforce": [VP, U64, U64, C.c_uint32, C.c_uint32, VP, VP, C.POINTER(U64)],
+    "xknn_graph_ring": [VP, U64, U64, C.c_uint32, C.c_uint32, C.c_int, C.c_int, VP, VP, VP,
+                        C.POINTER(U64), C.POINTER(U64)],
+    "xknn_layer_set_graph_rows": [VP, VP, C.c_uint32],
+    "xknn_layer_rebuild_graph": [VP, C.c_uint32, C.c_uint32, C.POINTER(U64)],
+    "xknn_layer_get_graph": [VP, VP, VP, VP, U64, C.POINTER(U64), C.c_int],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
@@ -164,6 +169,23 @@ def graph_bruteforce(w_norm, k: int, kprime: int = 0):
     _check(_lib.xknn_graph_bruteforce(w.data_ptr(), n, d, k, kprime, out.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream, C.byref(unc)))
     return out, unc.value
+
+
+def graph_ring(w_norm_local, num_classes: int, k: int, kprime: int, rank: int, world: int,
+               comm=None):
+    """build_graph_ring (knn_graph.cpp:147-233) with one process per GPU: this rank's normalized
+    block of ShardLayout(num_classes, world) in, its rows of the exact graph out.  Collective.
+    Returns ((rows, k) int32 tensor of global ids, uncertified rows, transfer steps)."""
+    import torch
+
+    w = w_norm_local.contiguous()
+    rows, d = w.shape
+    out = torch.empty(rows, k, dtype=torch.int32, device=w.device)
+    unc, steps = U64(), U64()
+    _check(_lib.xknn_graph_ring(w.data_ptr(), num_classes, d, k, kprime, rank, world, comm,
+                                torch.cuda.current_stream().cuda_stream, out.data_ptr(),
+                                C.byref(unc), C.byref(steps)))
+    return out, unc.value, steps.value
 
 
 def _ptr(t) -> int:
@@ -254,6 +276,36 @@ class KnnSoftmaxLayer:
         self._enter()
         _check(_lib.xknn_layer_set_graph_csr(self.h, kpc.data_ptr(), off.data_ptr(),
                                              fl.data_ptr() if fl.numel() else 0, fl.numel(), dev))
+
+    def set_graph_rows(self, rows, k: int) -> None:
+        """compress_graph + set_shard_graphs from this rank's rows [begin, end) x k of the full
+        graph (device int32/uint32, global ids).  Collective over the layer's ranks."""
+        r = rows.contiguous()
+        assert r.shape == (self.shard_rows, k) and r.is_cuda
+        self._enter()
+        _check(_lib.xknn_layer_set_graph_rows(self.h, r.data_ptr(), k))
+
+    def rebuild_graph(self, k: int, kprime: int = 0) -> int:
+        """Exact KNN graph of the current (normalized) weights, sharded build + compression,
+        installed as this shard's CompressedKnnGraph.  Collective.  Returns uncertified rows."""
+        unc = U64()
+        self._enter()
+        _check(_lib.xknn_layer_rebuild_graph(self.h, k, kprime, C.byref(unc)))
+        return unc.value
+
+    def graph(self):
+        """The installed CompressedKnnGraph: (k_per_class u32[N], offsets u64[N], flat u32[])
+        as numpy arrays."""
+        import numpy as np
+
+        n = U64()
+        _check(_lib.xknn_layer_get_graph(self.h, None, None, None, 0, C.byref(n), 0))
+        kpc = np.zeros(self.num_classes, np.uint32)
+        off = np.zeros(self.num_classes, np.uint64)
+        flat = np.zeros(max(n.value, 1), np.uint32)
+        _check(_lib.xknn_layer_get_graph(self.h, kpc.ctypes.data, off.ctypes.data,
+                                         flat.ctypes.data, flat.size, C.byref(n), 0))
+        return kpc, off, flat[: n.value]
 
     # -- hot path ------------------------------------------------------------------------------
     def select_active_classes(self, labels):

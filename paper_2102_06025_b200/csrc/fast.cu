@@ -14,6 +14,7 @@
 // Warp roles (384 threads, one CTA per SM, persistent over tiles): warp 0 TMA producer,
 // warp 1 MMA issuer (one thread), warp 2 TMEM allocator, warps 4-11 epilogue (TMEM -> regs).
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include "kernels.cuh"
 #include "tc.cuh"
@@ -73,11 +74,19 @@ struct GemmArgs {
   const float* lr;
   float mu, wd;
   const unsigned long long* err;
-  // graph build (kG): candidate regions [row][half][ch] of (approx score, column)
+  // graph build (kG): own rows (A, global ids row_base..) against a held block of ncols
+  // columns (B, global ids col_base..).  Per in-flight unit slot (pair * 256 + row): two
+  // candidate regions [slot][half][ch] of (approx score, column id) with counts/cuts; per own
+  // row: the persistent candidate list [row][kprime], its length and cut (every column not in
+  // the list has approx score <= cut), merged at the end of each unit.
   float2* cand;
   uint32_t* cnt;
   float* tau;
-  uint32_t ch, kprime, nrows;
+  uint32_t ch, kprime, nrows, ncols;
+  uint32_t row_base, col_base;
+  float2* list;
+  uint32_t* lcnt;
+  float* lcut;
 };
 
 struct Tile {
@@ -470,10 +479,10 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
     x.valid = true;
     return x;
   }
-  if (KIND == kG) {  // one 256-row query block against every 256-column tile
+  if (KIND == kG) {  // one 256-row query block against every 256-column tile of the block
     x.row0 = u * 256;
     x.t0 = 0;
-    x.t1 = (a.nrows + 255) / 256;
+    x.t1 = (a.ncols + 255) / 256;
     x.valid = true;
     return x;
   }
@@ -510,6 +519,66 @@ __device__ __forceinline__ uint32_t fkey(float f) {
 }
 __device__ __forceinline__ float funkey(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Largest key `lo` with #{entries with key >= lo} > limit (warp-cooperative, all lanes return
+// it); entries (score, id) are read through get(e), e < total.
+template <typename Get>
+__device__ __forceinline__ uint32_t warp_cut_key(Get get, uint32_t total, uint32_t limit,
+                                                 uint32_t lane) {
+  uint32_t lo = 0, hi = 0xffffffffu;
+#pragma unroll 1
+  while (lo < hi) {
+    const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
+    uint32_t c = 0;
+    for (uint32_t e = lane; e < total; e += 32) c += fkey(get(e).x) >= mid;
+    c = warp_sum(c);
+    if (c > limit) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Merge of one row's persistent candidate list with the two regions of its unit slot: the cut
+// becomes the largest of the three cuts (every column left out of any of them scores <= it);
+// above it at most kprime entries are kept, raising the cut to the (kprime+1)-th largest score
+// if needed.  Invariant: every column not in the list has approx score <= lcut[row].
+__device__ __noinline__ void merge_candidates(float2* __restrict__ list, uint32_t* __restrict__ lcnt,
+                                              float* __restrict__ lcut,
+                                              const float2* __restrict__ cand,
+                                              const uint32_t* __restrict__ cnt,
+                                              const float* __restrict__ tau, uint32_t ch,
+                                              uint32_t kp, uint32_t row, uint32_t slot,
+                                              uint32_t lane) {
+  const uint32_t n0 = cnt[slot * 2], n1 = cnt[slot * 2 + 1];
+  if (n0 + n1 == 0) return;  // nothing new: the regions' cuts never rose above lcut
+  float2* L = list + (uint64_t)row * kp;
+  const float2* R0 = cand + (uint64_t)slot * 2 * ch;
+  const float2* R1 = R0 + ch;
+  const uint32_t nl = lcnt[row];
+  float T = fmaxf(lcut[row], fmaxf(tau[slot * 2], tau[slot * 2 + 1]));
+  const uint32_t total = nl + n0 + n1;
+  auto get = [&](uint32_t e) -> float2 {
+    return e < nl ? L[e] : (e < nl + n0 ? R0[e - nl] : R1[e - nl - n0]);
+  };
+  uint32_t above = 0;
+  for (uint32_t e = lane; e < total; e += 32) above += get(e).x > T;
+  above = warp_sum(above);
+  if (above > kp) T = funkey(warp_cut_key(get, total, kp, lane));
+  uint32_t w = 0;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t e = base + lane;
+    const float2 v = e < total ? get(e) : make_float2(-INFINITY, 0.f);
+    const bool keep = e < total && v.x > T;
+    __syncwarp();  // this chunk is read before any of it is overwritten (w <= base)
+    const uint32_t bal = __ballot_sync(XKNN_FULL_MASK, keep);
+    if (keep) L[w + __popc(bal & ((1u << lane) - 1))] = v;
+    w += __popc(bal);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    lcnt[row] = w;
+    lcut[row] = T;
+  }
 }
 
 // Region full: the new cut is the kprime-th largest score; keep the entries strictly above it.
@@ -641,7 +710,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
             const uint32_t b0 = tc::smem_u32(sB + stage * C::B_BYTES);
             if (KIND == kF || KIND == kG) {
-              constexpr uint32_t id = tc::idesc_bf16(256, 256, false, false);
+              constexpr uint32_t id = KIND == kG ? tc::idesc_f16(256, 256, false, false)
+                                                 : tc::idesc_bf16(256, 256, false, false);
               const uint32_t r0 = tc::smem_u32(sRes + k * 16384);
 #pragma unroll
               for (uint32_t kk = 0; kk < 4; ++kk)
@@ -698,9 +768,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t ntile = (KIND == kF || KIND == kG) ? x.t1 - x.t0 : 1;
       // kG: this thread's (row, column half) candidate region state for the whole unit
       const uint32_t grow = x.row0 + cta * 128 + row;
-      float2* creg = KIND == kG ? a.cand + ((uint64_t)grow * 2 + h) * a.ch : nullptr;
+      const uint32_t slot = pair * 256 + cta * 128 + row;
+      float2* creg = KIND == kG ? a.cand + ((uint64_t)slot * 2 + h) * a.ch : nullptr;
       uint32_t ccnt = 0;
       float ctau = -INFINITY;
+      if (KIND == kG && grow < a.nrows) ctau = a.lcut[grow];
       if (KIND == kDW && a.out == nullptr && grow < mw) {
         // fused update: pull this thread's W and V row halves into L2 while the MMA runs
         const uint64_t off = ((uint64_t)a.active[grow] - a.begin) * 512 + h * 256;
@@ -727,7 +799,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const uint32_t c = c0 + j;
-              if (vrow && v[j] > ctau && c < a.nrows && c != grow) mask |= 1u << j;
+              if (vrow && v[j] > ctau && c < a.ncols && a.col_base + c != a.row_base + grow)
+                mask |= 1u << j;
             }
             float sc[32];  // spill-friendly copy for the (rare) dynamic-index inserts
 #pragma unroll
@@ -755,15 +828,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                 ccnt = w;
                 if (!(sc[j] > ctau)) continue;
               }
-              creg[ccnt++] = make_float2(sc[j], __uint_as_float(c0 + j));
+              creg[ccnt++] = make_float2(sc[j], __uint_as_float(a.col_base + c0 + j));
             }
           }
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
-          if (t + 1 == ntile && vrow) {
-            a.cnt[grow * 2 + h] = ccnt;
-            a.tau[grow * 2 + h] = ctau;
+          if (t + 1 == ntile) {
+            a.cnt[slot * 2 + h] = ccnt;
+            a.tau[slot * 2 + h] = ctau;
           }
         } else if (KIND == kF) {
           const uint32_t ct = x.t0 + t;
@@ -953,6 +1026,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
         }
         if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+      }
+      if (KIND == kG) {
+        // unit end: fold both column halves' regions into the rows' persistent lists; warp
+        // (q, h) merges rows q*32 + 2i + h of this CTA
+        epilogue_bar();
+#pragma unroll 1
+        for (uint32_t i = 0; i < 16; ++i) {
+          const uint32_t r = q * 32 + 2 * i + h;
+          const uint32_t gr = x.row0 + cta * 128 + r;
+          if (gr < a.nrows)
+            merge_candidates(a.list, a.lcnt, a.lcut, a.cand, a.cnt, a.tau, a.ch, a.kprime, gr,
+                             pair * 256 + cta * 128 + r, lane);
+        }
+        epilogue_bar();  // regions free for the next unit
       }
     }
     if (lane == 0) tc::tma_store_wait_all();
@@ -1306,14 +1393,18 @@ static_assert(xknn::smem_bytes2<xknn::kG>() <= 232448, "graph GEMM pair smem");
 
 namespace xknn {
 
-// GEMM + threshold top-k' candidate pass of the graph build (graph.cu): Wb is the bf16 copy of
-// the normalized class weights (npad x 512, zero pad rows).
-cudaError_t launch_graph_candidates(const __nv_bfloat16* Wb, uint32_t n, uint32_t npad,
+// GEMM + threshold top-k' candidate pass of one ring hop of the graph build (graph.cu): own
+// (nrows x 512 fp16, zero rows up to a multiple of 256) against the held block (ncols rows of
+// global ids col_base.., buffer rows up to a multiple of 256), folded into the persistent lists.
+cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t row_base,
+                                    const __half* held, uint32_t ncols, uint32_t col_base,
+                                    float2* list, uint32_t* lcnt, float* lcut, uint32_t kprime,
                                     float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
-                                    uint32_t kprime, cudaStream_t s) {
+                                    cudaStream_t s) {
   CUtensorMap mA, mB;
-  if (!make_map(&mA, Wb, 512, npad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mB, Wb, 512, npad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+  const uint64_t apad = (nrows + 255) / 256 * 256, bpad = (ncols + 255) / 256 * 256;
+  if (!make_map(&mA, own, 512, apad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mB, held, 512, bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -1323,7 +1414,13 @@ cudaError_t launch_graph_candidates(const __nv_bfloat16* Wb, uint32_t n, uint32_
     attr = true;
   }
   GemmArgs ga{};
-  ga.nrows = n;
+  ga.nrows = nrows;
+  ga.ncols = ncols;
+  ga.row_base = row_base;
+  ga.col_base = col_base;
+  ga.list = list;
+  ga.lcnt = lcnt;
+  ga.lcut = lcut;
   ga.cand = cand;
   ga.cnt = cnt;
   ga.tau = tau;

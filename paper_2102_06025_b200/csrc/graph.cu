@@ -1,40 +1,75 @@
-// graph.cu -- exact KNN class graph on device: build_graph_bruteforce (knn_graph.cpp:124-145)
-// with the reference's ordering `better` (:20-26): self first, then descending inner product,
+// graph.cu -- exact KNN class graph on device, sharded over the class blocks of P GPUs:
+// build_graph_ring (knn_graph.cpp:147-233) and, at P = 1, build_graph_bruteforce (:124-145),
+// under the reference's ordering `better` (:20-26): self first, then descending inner product
+// (fp32, ascending d, separate multiply and add: matrix.cpp:57-68 / knn_graph.cpp:137-138),
 // ties to the lower class index.  Bit-exact with the reference:
-//   1. candidates: bf16 CTA-pair GEMM of the normalized weights against themselves with a
-//      threshold top-k' epilogue (fast.cu, k_gemm2<kG>): every column left out of a row's
-//      candidate set has approximate score <= T_row;
-//   2. exact re-score of the candidates in the reference's arithmetic (fp32, ascending d,
-//      separate multiply and add), sort under `better`, keep k;
-//   3. certificate: if the k-th exact score exceeds T_row + eps (eps bounds |bf16 GEMM - fp32
-//      reference|, 2^-8 for unit rows plus accumulation terms), no left-out column can belong
-//      to the top k; otherwise the row is recomputed by an exact scan over all N columns.
+//   1. candidate ring (fp16 tensor cores): every rank scores its own normalized rows against
+//      each class block as it passes around the ring (ncclSend/Recv to rank+1, P-1 hops, the
+//      reference's rotation held[(s+1)%p] = held[s]); a threshold top-k' epilogue of the GEMM
+//      (fast.cu, k_gemm2<kG>) keeps per row a list of at most k' candidates and a cut T: every
+//      column left out has approximate score <= T;
+//   2. certificate + window: with A = the (k-1)-th largest approximate score in the list and
+//      eps >= |approx - reference fp32 score|, the row is certified when A > T + 2 eps (its
+//      k-1 best exact scores then beat every left-out column); only list entries with approx
+//      >= A - 2 eps can reach the exact top k-1, the others are dropped;
+//   3. exact ring (fp32): the blocks pass around once more and each rank re-scores its
+//      windows' candidates in the reference's arithmetic as their block goes by; rows that
+//      failed the certificate are scanned exactly against every block instead;
+//   4. finalize: sort under `better`, self first, keep k.
+// compress_graph (knn_graph.cpp:235-266) of the row-distributed result is an all-to-all of
+// graph entries by owning shard (xknn_layer_rebuild_graph, layer_graph.cu).
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
+
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
+#include "graph.cuh"
 #include "kernels.cuh"
 
 namespace xknn {
 
-cudaError_t launch_graph_candidates(const __nv_bfloat16* Wb, uint32_t n, uint32_t npad,
+cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t row_base,
+                                    const __half* held, uint32_t ncols, uint32_t col_base,
+                                    float2* list, uint32_t* lcnt, float* lcut, uint32_t kprime,
                                     float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
-                                    uint32_t kprime, cudaStream_t s);
+                                    cudaStream_t s);
 
 namespace {
 
-constexpr float kEps = 0.0041f;  // >= 2^-8 (bf16 inputs, unit rows) + 2 * 512 * 2^-24
+// |fp16 tensor-core score - reference fp32 score| for unit rows at D = 512: input rounding
+// 2 * 2^-11 (+ subnormal terms 2e-6), fp32 accumulation of 512 products (512 * 2^-23), the
+// reference's own sequential fp32 sum (512 * 2^-24 + 2^-24); 1.07e-3 in total, with margin:
+constexpr float kEps = 0.00125f;
 
-__global__ void k_to_bf16(const float* __restrict__ w, uint64_t n, uint64_t npad, uint32_t d,
-                          __nv_bfloat16* __restrict__ out) {
+__global__ void k_to_f16(const float* __restrict__ w, uint64_t n, uint64_t npad, uint32_t d,
+                         __half* __restrict__ out) {
   const uint64_t total = npad * d / 2;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t row = (2 * e) / d;
     float2 v = row < n ? reinterpret_cast<const float2*>(w)[e] : make_float2(0.f, 0.f);
-    reinterpret_cast<__nv_bfloat162*>(out)[e] = __floats2bfloat162_rn(v.x, v.y);
+    reinterpret_cast<__half2*>(out)[e] = __floats2half2_rn(v.x, v.y);
   }
+}
+
+__global__ void k_list_init(uint32_t* lcnt, float* lcut, uint64_t n) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    lcnt[j] = 0;
+    lcut[j] = -INFINITY;
+  }
+}
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float funkey(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
 // the reference's score: dot += wj[d] * wi[d], d ascending, fp32 (knn_graph.cpp:137-138)
@@ -60,45 +95,144 @@ __device__ __forceinline__ bool before(float sa, uint32_t ia, float sb, uint32_t
   return ia < ib;
 }
 
-// One warp per row: exact re-score of its <= 2*ch candidates, warp bitonic sort, top k,
-// certificate.  Shared memory per warp: 2*ch (score, index) pairs, padded to a power of two.
-__global__ void k_graph_finalize(const float* __restrict__ wn, uint32_t n, uint32_t d,
-                                 const float2* __restrict__ cand, const uint32_t* __restrict__ cnt,
-                                 const float* __restrict__ tau, uint32_t ch, uint32_t k,
-                                 uint32_t* __restrict__ out, uint32_t* fail_count,
-                                 uint32_t* __restrict__ fail_list) {
+// Step 2, one warp per row: certificate and candidate window (see the file comment).
+__global__ void k_window(float2* __restrict__ list, uint32_t* __restrict__ lcnt,
+                         const float* __restrict__ lcut, uint32_t n, uint32_t kp, uint32_t need,
+                         uint32_t* __restrict__ flag, uint32_t* __restrict__ unc_count,
+                         uint32_t* __restrict__ unc_list) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
+       j += (gridDim.x * blockDim.x) >> 5) {
+    float2* L = list + (uint64_t)j * kp;
+    const uint32_t m = lcnt[j];
+    const float T = lcut[j];
+    bool cert = false;
+    float theta = -INFINITY;
+    if (m >= need) {
+      // A = need-th largest approximate score: largest key with #(>= key) >= need
+      uint32_t lo = 0, hi = 0xffffffffu;
+      while (lo < hi) {
+        const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
+        uint32_t c = 0;
+        for (uint32_t e = lane; e < m; e += 32) c += fkey(L[e].x) >= mid;
+        c = warp_sum(c);
+        if (c >= need) lo = mid; else hi = mid - 1;
+      }
+      const float A = funkey(lo);
+      cert = (T == -INFINITY) || (A > T + 2.0f * kEps);  // T = -inf: every column is listed
+      theta = A - 2.0f * kEps;
+    }
+    if (cert) {
+      uint32_t w = 0;
+      for (uint32_t base = 0; base < m; base += 32) {
+        const uint32_t e = base + lane;
+        const float2 v = e < m ? L[e] : make_float2(-INFINITY, 0.f);
+        const bool keep = e < m && v.x >= theta;
+        __syncwarp();
+        const uint32_t bal = __ballot_sync(XKNN_FULL_MASK, keep);
+        if (keep) L[w + __popc(bal & ((1u << lane) - 1))] = v;
+        w += __popc(bal);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        lcnt[j] = w;
+        flag[j] = 0;
+      }
+    } else if (lane == 0) {
+      const uint32_t u = atomicAdd(unc_count, 1u);
+      unc_list[u] = j;
+      flag[j] = u + 1;
+    }
+    __syncwarp();
+  }
+}
+
+// Step 3, one warp per own row: exact scores of the window entries that live in the held block
+// [cb, cb + nc) (fp32 rows `held`).  ex[row][e] parallels list[row][e].
+__global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
+                          const float2* __restrict__ list, const uint32_t* __restrict__ lcnt,
+                          const uint32_t* __restrict__ flag, uint32_t kp,
+                          const float* __restrict__ held, uint32_t cb, uint32_t nc,
+                          float* __restrict__ ex) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
+       j += (gridDim.x * blockDim.x) >> 5) {
+    if (flag[j]) continue;
+    const uint32_t m = lcnt[j];
+    const float2* L = list + (uint64_t)j * kp;
+    for (uint32_t e = lane; e < m; e += 32) {
+      const uint32_t id = __float_as_uint(L[e].y);
+      if (id - cb < nc)
+        ex[(uint64_t)j * kp + e] = exact_dot(own + (uint64_t)j * d, held + (uint64_t)(id - cb) * d, d);
+    }
+  }
+}
+
+// exact scores of one query row against every row of a block (keys ordered like `better`,
+// key 0 marks the query itself)
+__global__ void k_exact_scan(const float* __restrict__ q, const float* __restrict__ blk,
+                             uint32_t nc, uint32_t d, uint32_t cb, uint32_t self,
+                             uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    uint32_t key = 0;
+    if (cb + i != self) {
+      float s = exact_dot(q, blk + (uint64_t)i * d, d);
+      if (s == 0.0f) s = 0.0f;  // -0 == +0 under `better`: one key
+      key = fkey(s);
+    }
+    keys[i] = key;
+    idx[i] = i;
+  }
+}
+
+// first `need` entries of a descending-sorted scan as (score, global id); sentinels pad
+__global__ void k_take(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                       uint32_t nc, uint32_t need, uint32_t cb, float2* __restrict__ out) {
+  for (uint32_t e = threadIdx.x; e < need; e += blockDim.x) {
+    float2 v = make_float2(-INFINITY, __uint_as_float(0xffffffffu));
+    if (e < nc && keys[e] != 0) v = make_float2(funkey(keys[e]), __uint_as_float(cb + idx[e]));
+    out[e] = v;
+  }
+}
+
+// Step 4, one warp per row: sort the row's exactly scored candidates under `better` (warp
+// bitonic in shared memory), write self + the k-1 best.
+__global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t kp, uint32_t cap,
+                           const float2* __restrict__ list, const uint32_t* __restrict__ lcnt,
+                           const float* __restrict__ ex, const uint32_t* __restrict__ flag,
+                           const float2* __restrict__ ubuf, uint32_t ulen,
+                           uint32_t* __restrict__ out) {
   extern __shared__ uint8_t sm[];
   const uint32_t warps = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t cap = 1;
-  while (cap < 2 * ch) cap <<= 1;
   float* ss = reinterpret_cast<float*>(sm) + (uint64_t)w * cap;
   uint32_t* si = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(sm) + (uint64_t)warps * cap) +
                  (uint64_t)w * cap;
   for (uint32_t j = blockIdx.x * warps + w; j < n; j += gridDim.x * warps) {
-    const uint32_t c0 = cnt[2 * j], c1 = cnt[2 * j + 1];
-    const uint32_t m = c0 + c1;
-    const float T = fmaxf(tau[2 * j], tau[2 * j + 1]);
-    const float* wj = wn + (uint64_t)j * d;
+    const uint32_t f = flag[j];
+    const uint32_t m = f ? ulen : lcnt[j];
     for (uint32_t e = lane; e < cap; e += 32) {
+      float s = -INFINITY;
+      uint32_t i = 0xffffffffu;
       if (e < m) {
-        const float2 c = e < c0 ? cand[(uint64_t)j * 2 * ch + e]
-                                : cand[((uint64_t)j * 2 + 1) * ch + (e - c0)];
-        const uint32_t i = __float_as_uint(c.y);
-        ss[e] = exact_dot(wj, wn + (uint64_t)i * d, d);
-        si[e] = i;
-      } else {
-        ss[e] = -INFINITY;
-        si[e] = 0xffffffffu;
+        if (f) {
+          const float2 v = ubuf[(uint64_t)(f - 1) * ulen + e];
+          s = v.x;
+          i = __float_as_uint(v.y);
+        } else {
+          s = ex[(uint64_t)j * kp + e];
+          i = __float_as_uint(list[(uint64_t)j * kp + e].y);
+        }
       }
+      ss[e] = s;
+      si[e] = i;
     }
     __syncwarp();
-    // bitonic sort, descending under `before`
     for (uint32_t size = 2; size <= cap; size <<= 1) {
       for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
         for (uint32_t e = lane; e < cap; e += 32) {
           const uint32_t p = e ^ stride;
           if (p > e) {
-            const bool dir = (e & size) == 0;  // true: this pair sorts "before" first
+            const bool dir = (e & size) == 0;
             const bool swp = dir ? before(ss[p], si[p], ss[e], si[e])
                                  : before(ss[e], si[e], ss[p], si[p]);
             if (swp) {
@@ -114,149 +248,322 @@ __global__ void k_graph_finalize(const float* __restrict__ wn, uint32_t n, uint3
         __syncwarp();
       }
     }
-    // self first, then the k-1 best candidates
-    bool ok = true;
-    if (k > 1) ok = m >= k - 1 && ss[k - 2] > T + kEps;
-    if (ok) {
-      uint32_t* o = out + (uint64_t)j * k;
-      for (uint32_t e = lane; e < k; e += 32) o[e] = e == 0 ? j : si[e - 1];
-    } else if (lane == 0) {
-      fail_list[atomicAdd(fail_count, 1u)] = j;
-    }
+    uint32_t* o = out + (uint64_t)j * k;
+    for (uint32_t e = lane; e < k; e += 32) o[e] = e == 0 ? row_base + j : si[e - 1];
     __syncwarp();
   }
 }
 
-// exact scores of one query row against every column (self excluded)
-__global__ void k_exact_row(const float* __restrict__ wn, uint32_t n, uint32_t d, uint32_t j,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    float s = i == j ? -INFINITY : exact_dot(wn + (uint64_t)j * d, wn + (uint64_t)i * d, d);
-    if (s == 0.0f) s = 0.0f;  // -0 == +0 under `better`: one key
-    const uint32_t u = __float_as_uint(s);
-    keys[i] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-    idx[i] = i;
-  }
-}
-
-__global__ void k_write_row(const uint32_t* __restrict__ sorted_idx, uint32_t j, uint32_t k,
-                            uint32_t* __restrict__ out) {
-  for (uint32_t e = threadIdx.x; e < k; e += blockDim.x)
-    out[(uint64_t)j * k + e] = e == 0 ? j : sorted_idx[e - 1];
+__global__ void k_self_only(uint32_t n, uint32_t row_base, uint32_t* out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    out[j] = row_base + j;
 }
 
 }  // namespace
 
-// Exact rows by full scans (the certificate's fallback, and the whole graph for small N / D).
+// Exact rows by full scans at P = 1 (the whole graph for D != 512).
 static cudaError_t exact_rows(const float* wn, uint32_t n, uint32_t d, uint32_t k,
-                              const uint32_t* rows, uint32_t nrows, uint32_t* out,
-                              cudaStream_t s) {
-  uint32_t *keys = nullptr, *idx = nullptr, *keys2 = nullptr, *idx2 = nullptr;
+                              uint32_t* out, cudaStream_t s) {
+  uint32_t* keys = nullptr;
   void* tmp = nullptr;
   size_t tb = 0;
-  cudaError_t e = cudaSuccess;
-  e = cudaMalloc(&keys, (size_t)n * 16);
+  float2* row = nullptr;
+  cudaError_t e = cudaMalloc(&keys, (size_t)n * 16);
   if (e != cudaSuccess) return e;
-  idx = keys + n;
-  keys2 = keys + 2 * (size_t)n;
-  idx2 = keys + 3 * (size_t)n;
+  uint32_t* idx = keys + n;
+  uint32_t* keys2 = keys + 2 * (size_t)n;
+  uint32_t* idx2 = keys + 3 * (size_t)n;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, keys2, idx, idx2, (int)n, 0, 32, s);
   e = cudaMalloc(&tmp, tb);
-  for (uint32_t r = 0; r < nrows && e == cudaSuccess; ++r) {
-    const uint32_t j = rows ? rows[r] : r;
-    k_exact_row<<<grid_for(n, 256), 256, 0, s>>>(wn, n, d, j, keys, idx);
+  if (e == cudaSuccess) e = cudaMalloc(&row, (size_t)std::max<uint32_t>(k, 1) * sizeof(float2));
+  std::vector<float2> h(k);
+  for (uint32_t j = 0; j < n && e == cudaSuccess; ++j) {
+    k_exact_scan<<<grid_for(n, 256), 256, 0, s>>>(wn + (uint64_t)j * d, wn, n, d, 0, j, keys, idx);
     size_t t2 = tb;
     e = cub::DeviceRadixSort::SortPairsDescending(tmp, t2, keys, keys2, idx, idx2, (int)n, 0, 32, s);
-    if (e == cudaSuccess) k_write_row<<<1, 128, 0, s>>>(idx2, j, k, out);
-    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) break;
+    k_take<<<1, 128, 0, s>>>(keys2, idx2, n, k - 1, 0, row);
+    e = cudaMemcpyAsync(h.data(), row, (size_t)(k - 1) * sizeof(float2), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    std::vector<uint32_t> r(k);
+    r[0] = j;
+    for (uint32_t t = 1; t < k; ++t) std::memcpy(&r[t], &h[t - 1].y, 4);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out + (uint64_t)j * k, r.data(), (size_t)k * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   }
   cudaStreamSynchronize(s);
+  cudaFree(row);
   cudaFree(tmp);
   cudaFree(keys);
   return e;
 }
 
-xknn_status_t graph_bruteforce(const float* wn, uint64_t n64, uint64_t d64, uint32_t k,
-                               uint32_t kprime, uint32_t* out, cudaStream_t s,
-                               uint64_t* uncertified) {
-  const uint32_t n = (uint32_t)n64, d = (uint32_t)d64;
-  if (k > n64) return fail_msg(XKNN_ERR_K_TOO_LARGE, "build_graph_bruteforce: k exceeds class count");
-  if (k == 0) return fail_msg(XKNN_ERR_INVALID_ARGUMENT, "build_graph_bruteforce: k must be positive");
-  if (d % 4) return fail_msg(XKNN_ERR_SHAPE_MISMATCH, "dim must be a multiple of 4");
-  if (uncertified) *uncertified = 0;
-  cudaError_t e;
-  if (d != 512 || n < 1024) {  // exact scans only
-    e = exact_rows(wn, n, d, k, nullptr, n, out, s);
-    return e == cudaSuccess ? XKNN_OK : fail_msg(XKNN_ERR_CUDA, cudaGetErrorString(e));
+namespace {
+struct Dev {  // RAII device scratch
+  std::vector<void*> p;
+  ~Dev() {
+    for (void* q : p) cudaFree(q);
   }
-  kprime = std::max<uint32_t>(kprime, k + 16);
-  const uint32_t ch = (2 * kprime + 31) / 32 * 32;  // region capacity > kprime
-  const uint32_t npad = (n + 255) / 256 * 256;
-  __nv_bfloat16* wb = nullptr;
-  float2* cand = nullptr;
-  uint32_t *cnt = nullptr, *fails = nullptr;
-  float* tau = nullptr;
-  uint32_t nfail = 0;
-  std::vector<uint32_t> flist;
-#define G_CUDA(x)                                     \
-  do {                                                \
-    e = (x);                                          \
-    if (e != cudaSuccess) goto done;                  \
+  template <typename T>
+  cudaError_t get(T** out, uint64_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) p.push_back(q);
+    *out = static_cast<T*>(q);
+    return e;
+  }
+  void release(void* q) {
+    for (auto& x : p)
+      if (x == q) {
+        cudaFree(x);
+        x = nullptr;
+      }
+  }
+};
+
+inline void shard_range_of(uint64_t n, uint64_t p, uint64_t s, uint64_t* b, uint64_t* e) {
+  const uint64_t base = n / p, rem = n % p;
+  if (s < rem) {
+    *b = s * (base + 1);
+    *e = *b + base + 1;
+  } else {
+    *b = rem * (base + 1) + (s - rem) * base;
+    *e = *b + base;
+  }
+}
+}  // namespace
+
+xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint32_t k,
+                          uint32_t kprime, int rank, int world, ncclComm_t comm, cudaStream_t s,
+                          uint32_t* out, GraphBuildStats* stats) {
+  if (stats) *stats = GraphBuildStats{};
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail_msg(XKNN_ERR_INVALID_ARGUMENT, "graph build: bad rank/world");
+  if (k > n_total) return fail_msg(XKNN_ERR_K_TOO_LARGE, "build_graph: k exceeds class count");
+  if (k == 0) return fail_msg(XKNN_ERR_INVALID_ARGUMENT, "build_graph: k must be positive");
+  if (d64 == 0 || d64 % 4) return fail_msg(XKNN_ERR_SHAPE_MISMATCH, "dim must be a positive multiple of 4");
+  if (n_total >= (1ull << 32) - 1) return fail_msg(XKNN_ERR_UNSUPPORTED, "class ids must fit u32");
+  if (n_total < (uint64_t)world) return fail_msg(XKNN_ERR_EMPTY_SHARD, "build_graph_ring: a shard is empty");
+  if (world > 1 && !comm) return fail_msg(XKNN_ERR_INVALID_ARGUMENT, "graph ring: NCCL communicator required");
+  const uint32_t d = (uint32_t)d64;
+  uint64_t b64, e64;
+  shard_range_of(n_total, world, rank, &b64, &e64);
+  const uint32_t row_base = (uint32_t)b64, n = (uint32_t)(e64 - b64);
+  cudaError_t e = cudaSuccess;
+#define G_CUDA(x)                                                         \
+  do {                                                                    \
+    e = (x);                                                              \
+    if (e != cudaSuccess) return fail_msg(XKNN_ERR_CUDA, cudaGetErrorString(e)); \
   } while (0)
-  G_CUDA(cudaMalloc(&wb, (size_t)npad * 512 * 2));
-  G_CUDA(cudaMalloc(&cand, (size_t)npad * 2 * ch * sizeof(float2)));
-  G_CUDA(cudaMalloc(&cnt, (size_t)npad * 2 * 4));
-  G_CUDA(cudaMalloc(&tau, (size_t)npad * 2 * 4));
-  G_CUDA(cudaMalloc(&fails, ((size_t)n + 1) * 4));
-  G_CUDA(cudaMemsetAsync(fails, 0, 4, s));
-  k_to_bf16<<<grid_for((uint64_t)npad * 256, 256), 256, 0, s>>>(wn, n, npad, 512, wb);
-  G_CUDA(cudaGetLastError());
-  G_CUDA(launch_graph_candidates(wb, n, npad, cand, cnt, tau, ch, kprime, s));
-  if (getenv("XKNN_GRAPH_DEBUG")) {
+#define G_NCCL(x)                                                         \
+  do {                                                                    \
+    ncclResult_t r_ = (x);                                                \
+    if (r_ != ncclSuccess) return fail_msg(XKNN_ERR_NCCL, ncclGetErrorString(r_)); \
+  } while (0)
+  if (k == 1) {  // self only
+    k_self_only<<<grid_for(n, 256), 256, 0, s>>>(n, row_base, out);
+    G_CUDA(cudaGetLastError());
     G_CUDA(cudaStreamSynchronize(s));
-    std::vector<uint32_t> hc(2 * (size_t)npad);
-    std::vector<float> ht(2 * (size_t)npad);
-    std::vector<float2> hcand(2 * (size_t)ch);
-    cudaMemcpy(hc.data(), cnt, hc.size() * 4, cudaMemcpyDeviceToHost);
-    cudaMemcpy(ht.data(), tau, ht.size() * 4, cudaMemcpyDeviceToHost);
-    for (uint32_t j : {0u, 1u, 300u, n - 1}) {
-      cudaMemcpy(hcand.data(), cand + (size_t)j * 2 * ch, hcand.size() * 8, cudaMemcpyDeviceToHost);
-      fprintf(stderr, "row %u: cnt %u %u tau %g %g :", j, hc[2 * j], hc[2 * j + 1], ht[2 * j],
-              ht[2 * j + 1]);
-      for (uint32_t e = 0; e < 6 && e < hc[2 * j]; ++e)
-        { uint32_t ui; memcpy(&ui, &hcand[e].y, 4); fprintf(stderr, " (%u %.4f)", ui, hcand[e].x); }
-      fprintf(stderr, "\n");
+    return XKNN_OK;
+  }
+  if (d != 512) {
+    if (world > 1) return fail_msg(XKNN_ERR_UNSUPPORTED, "graph ring needs dim 512");
+    G_CUDA(exact_rows(wn, n, d, k, out, s));
+    if (stats) stats->uncertified_rows = n;
+    return XKNN_OK;
+  }
+  const uint32_t need = k - 1;
+  // k' is a performance knob here (the output never depends on it): large enough that the
+  // certificate holds for almost every row
+  const uint32_t kp = std::max<uint32_t>({kprime, 2 * k, k + 32});
+  const uint32_t ch = (2 * kp + 31) / 32 * 32;  // region capacity per (slot, half)
+  uint64_t maxrows = 0;
+  for (int r = 0; r < world; ++r) {
+    uint64_t rb, re;
+    shard_range_of(n_total, world, r, &rb, &re);
+    maxrows = std::max(maxrows, re - rb);
+  }
+  const uint64_t npad = (n + 255) / 256 * 256, mpad = (maxrows + 255) / 256 * 256;
+  Dev mem;
+  float2 *list = nullptr, *cand = nullptr;
+  uint32_t *lcnt = nullptr, *ccnt = nullptr, *flag = nullptr, *unc = nullptr;
+  float *lcut = nullptr, *ctau = nullptr, *ex = nullptr;
+  __half *own16 = nullptr, *buf16[2] = {nullptr, nullptr};
+  G_CUDA(mem.get(&list, (uint64_t)n * kp));
+  G_CUDA(mem.get(&lcnt, n));
+  G_CUDA(mem.get(&lcut, n));
+  G_CUDA(mem.get(&cand, (uint64_t)kNumSMs / 2 * 256 * 2 * ch));
+  G_CUDA(mem.get(&ccnt, (uint64_t)kNumSMs / 2 * 256 * 2));
+  G_CUDA(mem.get(&ctau, (uint64_t)kNumSMs / 2 * 256 * 2));
+  G_CUDA(mem.get(&own16, npad * 512));
+  if (world > 1) {
+    G_CUDA(mem.get(&buf16[0], mpad * 512));
+    G_CUDA(mem.get(&buf16[1], mpad * 512));
+  }
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> evs;
+  struct Cleanup {
+    cudaStream_t* cs;
+    std::vector<cudaEvent_t>* evs;
+    ~Cleanup() {
+      for (auto ev : *evs) cudaEventDestroy(ev);
+      if (*cs) cudaStreamDestroy(*cs);
+    }
+  } cleanup{&cs, &evs};
+  auto new_event = [&](cudaEvent_t* ev) {
+    cudaError_t r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (r == cudaSuccess) evs.push_back(*ev);
+    return r;
+  };
+  if (world > 1) G_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const int next = (rank + 1) % world, prev = (rank + world - 1) % world;
+
+  // ---- 1. candidate ring (fp16) ----
+  k_to_f16<<<grid_for(npad * 256, 256), 256, 0, s>>>(wn, n, npad, 512, own16);
+  G_CUDA(cudaGetLastError());
+  k_list_init<<<grid_for(n, 256), 256, 0, s>>>(lcnt, lcut, n);
+  G_CUDA(cudaGetLastError());
+  const __half* held = own16;
+  for (int h = 0; h < world; ++h) {
+    const int o = (rank - h + world) % world;
+    uint64_t cb, ce;
+    shard_range_of(n_total, world, o, &cb, &ce);
+    cudaEvent_t ev_recv = nullptr;
+    if (h + 1 < world) {
+      // pass the held block on (rank -> rank+1) while it is scored here; the receive buffer
+      // was last read by the previous hop's GEMM
+      cudaEvent_t ev_ready;
+      G_CUDA(new_event(&ev_ready));
+      G_CUDA(cudaEventRecord(ev_ready, s));
+      G_CUDA(cudaStreamWaitEvent(cs, ev_ready, 0));
+      const int po = (prev - h + world) % world;  // origin of the block prev holds at hop h
+      uint64_t pb, pe;
+      shard_range_of(n_total, world, po, &pb, &pe);
+      G_NCCL(ncclGroupStart());
+      G_NCCL(ncclSend(held, (ce - cb) * 512, ncclFloat16, next, comm, cs));
+      G_NCCL(ncclRecv(buf16[h % 2], (pe - pb) * 512, ncclFloat16, prev, comm, cs));
+      G_NCCL(ncclGroupEnd());
+      G_CUDA(new_event(&ev_recv));
+      G_CUDA(cudaEventRecord(ev_recv, cs));
+    }
+    G_CUDA(launch_graph_candidates(own16, n, row_base, held, (uint32_t)(ce - cb), (uint32_t)cb,
+                                   list, lcnt, lcut, kp, cand, ccnt, ctau, ch, s));
+    if (h + 1 < world) {
+      G_CUDA(cudaStreamWaitEvent(s, ev_recv, 0));
+      held = buf16[h % 2];
+      if (stats) ++stats->transfer_steps;
     }
   }
+  if (getenv("XKNN_GRAPH_DEBUG")) {
+    G_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> hc(n);
+    std::vector<float> ht(n);
+    cudaMemcpy(hc.data(), lcnt, (size_t)n * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ht.data(), lcut, (size_t)n * 4, cudaMemcpyDeviceToHost);
+    for (uint32_t j : {0u, 1u, n / 2, n - 1})
+      fprintf(stderr, "rank %d row %u: list %u cut %g\n", rank, row_base + j, hc[j], ht[j]);
+  }
+  mem.release(cand);
+  mem.release(own16);
+  mem.release(buf16[0]);
+  mem.release(buf16[1]);
+
+  // ---- 2. certificate + window ----
+  G_CUDA(mem.get(&flag, n));
+  G_CUDA(mem.get(&unc, (uint64_t)n + 1));
+  G_CUDA(cudaMemsetAsync(unc, 0, 4, s));
+  k_window<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(list, lcnt, lcut, n, kp, need, flag, unc,
+                                                           unc + 1);
+  G_CUDA(cudaGetLastError());
+  uint32_t nu = 0;
+  G_CUDA(cudaMemcpyAsync(&nu, unc, 4, cudaMemcpyDeviceToHost, s));
+  G_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> urows(nu);
+  if (nu) G_CUDA(cudaMemcpy(urows.data(), unc + 1, (size_t)nu * 4, cudaMemcpyDeviceToHost));
+  if (stats) stats->uncertified_rows = nu;
+
+  // ---- 3. exact ring (fp32) ----
+  G_CUDA(mem.get(&ex, (uint64_t)n * kp));
+  float* buf32[2] = {nullptr, nullptr};
+  if (world > 1) {
+    G_CUDA(mem.get(&buf32[0], maxrows * 512));
+    G_CUDA(mem.get(&buf32[1], maxrows * 512));
+  }
+  const uint32_t ulen = (uint32_t)world * need;
+  float2* ubuf = nullptr;
+  uint32_t *keys = nullptr, *kidx = nullptr, *keys2 = nullptr, *kidx2 = nullptr;
+  void* stmp = nullptr;
+  size_t stb = 0;
+  if (nu) {
+    G_CUDA(mem.get(&ubuf, (uint64_t)nu * ulen));
+    G_CUDA(mem.get(&keys, maxrows * 4));
+    kidx = keys + maxrows;
+    keys2 = keys + 2 * maxrows;
+    kidx2 = keys + 3 * maxrows;
+    G_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, stb, keys, keys2, kidx, kidx2,
+                                                     (int)maxrows, 0, 32, s));
+    G_CUDA(mem.get(reinterpret_cast<uint8_t**>(&stmp), stb));
+  }
+  const float* held32 = wn;
+  for (int h = 0; h < world; ++h) {
+    const int o = (rank - h + world) % world;
+    uint64_t cb, ce;
+    shard_range_of(n_total, world, o, &cb, &ce);
+    const uint32_t nc = (uint32_t)(ce - cb);
+    cudaEvent_t ev_recv = nullptr;
+    if (h + 1 < world) {
+      cudaEvent_t ev_ready;
+      G_CUDA(new_event(&ev_ready));
+      G_CUDA(cudaEventRecord(ev_ready, s));
+      G_CUDA(cudaStreamWaitEvent(cs, ev_ready, 0));
+      const int po = (prev - h + world) % world;
+      uint64_t pb, pe;
+      shard_range_of(n_total, world, po, &pb, &pe);
+      G_NCCL(ncclGroupStart());
+      G_NCCL(ncclSend(held32, (ce - cb) * 512, ncclFloat, next, comm, cs));
+      G_NCCL(ncclRecv(buf32[h % 2], (pe - pb) * 512, ncclFloat, prev, comm, cs));
+      G_NCCL(ncclGroupEnd());
+      G_CUDA(new_event(&ev_recv));
+      G_CUDA(cudaEventRecord(ev_recv, cs));
+    }
+    k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(wn, n, 512, list, lcnt, flag, kp,
+                                                              held32, (uint32_t)cb, nc, ex);
+    G_CUDA(cudaGetLastError());
+    for (uint32_t u = 0; u < nu; ++u) {  // rows without a certificate: exact scan of the block
+      const uint32_t j = urows[u];
+      k_exact_scan<<<grid_for(nc, 256), 256, 0, s>>>(wn + (uint64_t)j * 512, held32, nc, 512,
+                                                     (uint32_t)cb, row_base + j, keys, kidx);
+      size_t t2 = stb;
+      G_CUDA(cub::DeviceRadixSort::SortPairsDescending(stmp, t2, keys, keys2, kidx, kidx2, (int)nc,
+                                                       0, 32, s));
+      k_take<<<1, 128, 0, s>>>(keys2, kidx2, nc, need, (uint32_t)cb,
+                               ubuf + (uint64_t)u * ulen + (uint64_t)h * need);
+      G_CUDA(cudaGetLastError());
+    }
+    if (h + 1 < world) {
+      G_CUDA(cudaStreamWaitEvent(s, ev_recv, 0));
+      held32 = buf32[h % 2];
+    }
+  }
+
+  // ---- 4. finalize ----
   {
     uint32_t cap = 1;
-    while (cap < 2 * ch) cap <<= 1;
+    while (cap < std::max(kp, nu ? ulen : 1u)) cap <<= 1;
     const uint32_t warps = 4;
     const size_t smem = (size_t)warps * cap * 8;
     if (smem > 48 * 1024)
-      G_CUDA(cudaFuncSetAttribute(k_graph_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      G_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    k_graph_finalize<<<grid_for((uint64_t)n * 32, warps * 32, 148u * 32u), warps * 32, smem, s>>>(
-        wn, n, 512, cand, cnt, tau, ch, k, out, fails, fails + 1);
+    k_finalize<<<grid_for((uint64_t)n * 32, warps * 32, 148u * 32u), warps * 32, smem, s>>>(
+        n, row_base, k, kp, cap, list, lcnt, ex, flag, ubuf, ulen, out);
     G_CUDA(cudaGetLastError());
   }
-  G_CUDA(cudaMemcpyAsync(&nfail, fails, 4, cudaMemcpyDeviceToHost, s));
   G_CUDA(cudaStreamSynchronize(s));
-  if (nfail) {
-    flist.resize(nfail);
-    G_CUDA(cudaMemcpy(flist.data(), fails + 1, (size_t)nfail * 4, cudaMemcpyDeviceToHost));
-    G_CUDA(exact_rows(wn, n, 512, k, flist.data(), nfail, out, s));
-  }
-  if (uncertified) *uncertified = nfail;
-done:
+  if (cs) G_CUDA(cudaStreamSynchronize(cs));
 #undef G_CUDA
-  cudaStreamSynchronize(s);
-  cudaFree(wb);
-  cudaFree(cand);
-  cudaFree(cnt);
-  cudaFree(tau);
-  cudaFree(fails);
-  if (e != cudaSuccess) return fail_msg(XKNN_ERR_CUDA, cudaGetErrorString(e));
+#undef G_NCCL
   return XKNN_OK;
 }
 
@@ -266,6 +573,25 @@ extern "C" xknn_status_t xknn_graph_bruteforce(const float* w_norm_dev, uint64_t
                                                uint64_t dim, uint32_t k, uint32_t kprime,
                                                uint32_t* out_dev, void* stream,
                                                uint64_t* uncertified_rows) {
-  return xknn::graph_bruteforce(w_norm_dev, num_classes, dim, k, kprime, out_dev,
-                                static_cast<cudaStream_t>(stream), uncertified_rows);
+  xknn::GraphBuildStats st{};
+  xknn_status_t r = xknn::graph_build(w_norm_dev, num_classes, dim, k, kprime, 0, 1, nullptr,
+                                      static_cast<cudaStream_t>(stream), out_dev, &st);
+  if (uncertified_rows) *uncertified_rows = st.uncertified_rows;
+  return r;
+}
+
+extern "C" xknn_status_t xknn_graph_ring(const float* w_norm_local_dev, uint64_t num_classes,
+                                         uint64_t dim, uint32_t k, uint32_t kprime, int rank,
+                                         int world, void* comm, void* stream,
+                                         uint32_t* out_rows_dev, uint64_t* uncertified_rows,
+                                         uint64_t* transfer_steps) {
+  if (kprime < k)
+    return xknn::fail_msg(XKNN_ERR_INVALID_ARGUMENT, "build_graph_ring: k' must be >= k");
+  xknn::GraphBuildStats st{};
+  xknn_status_t r = xknn::graph_build(w_norm_local_dev, num_classes, dim, k, kprime, rank, world,
+                                      static_cast<ncclComm_t>(comm),
+                                      static_cast<cudaStream_t>(stream), out_rows_dev, &st);
+  if (uncertified_rows) *uncertified_rows = st.uncertified_rows;
+  if (transfer_steps) *transfer_steps = st.transfer_steps;
+  return r;
 }

@@ -18,6 +18,10 @@ static xknn_status_t fail(xknn_status_t s, const std::string& msg) {
 }
 
 xknn_status_t fail_msg(xknn_status_t s, const char* msg) { return fail(s, msg); }
+xknn_status_t fail_row(xknn_status_t s, const char* msg, uint64_t row) {
+  g_row = row;
+  return fail(s, msg);
+}
 
 xknn_status_t Layer::cuda_ok(cudaError_t e, const char* file, int line, const char* expr) {
   if (e == cudaSuccess) return XKNN_OK;
@@ -343,9 +347,6 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
 using xknn::Layer;
 using xknn::fail;
 
-struct xknn_layer {
-  Layer L;
-};
 
 #define GUARD_H(h) \
   if (!(h)) return fail(XKNN_ERR_INVALID_ARGUMENT, "null layer handle")

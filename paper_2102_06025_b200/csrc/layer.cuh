@@ -27,6 +27,7 @@
 namespace xknn {
 
 xknn_status_t fail_msg(xknn_status_t s, const char* msg);  // sets xknn_last_error_message
+xknn_status_t fail_row(xknn_status_t s, const char* msg, uint64_t row);  // + last_error_row
 
 struct SelState {
   unsigned long long pool_local;   // |pool ∩ shard|
@@ -165,6 +166,11 @@ struct Layer {
 };
 
 }  // namespace xknn
+
+// the opaque handle of the C ABI
+struct xknn_layer {
+  xknn::Layer L;
+};
 
 // error helpers usable inside Layer methods
 #define XK_CUDA(expr)                                                      \

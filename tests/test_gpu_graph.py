@@ -57,3 +57,69 @@ def test_graph_large_sampled_rows():
     for j in np.random.default_rng(1).integers(0, n, 24):
         assert np.array_equal(got[j], O.graph_row(wn, int(j), k)), j
     assert unc < n // 100  # the certificate holds for almost every row
+
+
+def _dup_weights(seed, n_base, n_rand, scale=0.05):
+    """Random rows plus exact and near duplicates (exact score ties, certificate failures)."""
+    rng = np.random.default_rng(seed)
+    base = rng.standard_normal((n_base, 512)).astype(np.float32)
+    w = np.concatenate([base, base, base + 1e-4 * rng.standard_normal((n_base, 512)).astype(np.float32),
+                        rng.standard_normal((n_rand, 512)).astype(np.float32)])
+    return (w * scale).astype(np.float32)
+
+
+def test_layer_rebuild_graph_single_gpu():
+    """xknn_layer_rebuild_graph == compress_graph(build_graph_bruteforce(l2_normalize_rows(W)))
+    and the rebuilt graph drives selection exactly like the reference's."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    n, k, m, b = 3000, 12, 300, 64
+    w = _dup_weights(11, 200, n - 600)
+    wn = _normalized(w)
+    rc, g = O.bruteforce_graph("oracle", wn, k)
+    assert rc == 0
+    kpc, off, flat = O.compress(g, 1, 0)
+    layer = X.KnnSoftmaxLayer(n, 512, m_active=m, max_batch=b, rng_seed=42)
+    layer.set_weights(torch.from_numpy(w).cuda())
+    layer.rebuild_graph(k)
+    gk, go, gf = layer.graph()
+    assert np.array_equal(gk, kpc) and np.array_equal(go, off) and np.array_equal(gf, flat)
+    lab = np.random.default_rng(3).integers(0, n, b).astype(np.uint32)
+    act, _ = layer.select_active_classes(torch.from_numpy(lab.view(np.int32)).cuda())
+    rc, want, _ = O.select_shards("oracle", n, [(kpc, off, flat)], lab, m, 42)
+    assert rc == 0 and np.array_equal(act.cpu().numpy().view(np.uint32), want)
+    layer.close()
+
+
+def test_graph_errors():
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    wn = torch.from_numpy(_normalized(np.random.default_rng(0).standard_normal((300, 512))
+                                      .astype(np.float32))).cuda()
+    with pytest.raises(X.KTooLarge):
+        X.graph_bruteforce(wn, 301)
+    with pytest.raises(X.InvalidArgument):
+        X.graph_bruteforce(wn, 0)
+    with pytest.raises(X.InvalidArgument):  # k' < k (build_graph_ring)
+        X.graph_ring(wn, 300, 10, 5, 0, 1)
+    g, _ = X.graph_bruteforce(wn, 1)
+    assert np.array_equal(g.cpu().numpy()[:, 0], np.arange(300))
+    rows, unc, steps = X.graph_ring(wn, 300, 7, 7, 0, 1)
+    rc, want = O.bruteforce_graph("oracle", wn.cpu().numpy(), 7)
+    assert rc == 0 and np.array_equal(rows.cpu().numpy().view(np.uint32), want) and steps == 0
+
+
+def test_layer_rebuild_zero_norm_row():
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    w = (np.random.default_rng(1).standard_normal((500, 512)) * 0.05).astype(np.float32)
+    w[123] = 0.0
+    layer = X.KnnSoftmaxLayer(500, 512, m_active=50, max_batch=16, rng_seed=42)
+    layer.set_weights(torch.from_numpy(w).cuda())
+    with pytest.raises(X.ZeroNormRow) as ei:
+        layer.rebuild_graph(5)
+    assert ei.value.row == 123
+    layer.close()

@@ -61,3 +61,31 @@ def test_multi_gpu_step(p, m, precision, tol_loss, tol_g, tmp_path):
     assert rel_err(wg - w, w_or - w) <= tol_g
     untouched = np.all(w_or == w, axis=1)
     assert np.array_equal(wg[untouched], w[untouched])
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_multi_gpu_graph_ring_and_rebuild(p, tmp_path):
+    """build_graph_ring over P GPUs == build_graph_bruteforce (bit-exact rows), and the layer's
+    rebuild (normalize + ring + all-to-all compression) == compress_graph(g, layout, s)."""
+    if _ngpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    n, k = 3000, 10
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr=127.0.0.1", f"--master-port={29650 + p}",
+           os.path.join(HERE, "mp_graph_worker.py"), "--out", str(tmp_path), "--num-classes",
+           str(n), "--knn", str(k)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"graph{i}.npz")) for i in range(p)]
+    from mp_graph_worker import problem
+
+    rc, wn, _, _ = O.l2_normalize(problem(n, 5))
+    assert rc == 0
+    rc, g = O.bruteforce_graph("oracle", wn, k)
+    assert rc == 0
+    assert np.array_equal(np.concatenate([x["rows"] for x in res]), g)
+    assert all(int(x["steps"]) == p - 1 for x in res)
+    for s, x in enumerate(res):
+        kpc, off, flat = O.compress(g, p, s)
+        assert np.array_equal(x["kpc"], kpc) and np.array_equal(x["off"], off)
+        assert np.array_equal(x["flat"], flat)
