@@ -538,6 +538,40 @@ __device__ __forceinline__ uint32_t warp_cut_key(Get get, uint32_t total, uint32
   return lo;
 }
 
+// A cut T over the n entries rp[] (all scoring above lo) with kp/2 <= #(> T) <= kp when the
+// scores allow (bisection in score space; at most kp entries above T in every case), so that
+// compactions free at least half the region while keeping the best kp/2.  Warp-cooperative.
+__device__ __noinline__ float warp_cut_band(const float2* __restrict__ rp, uint32_t n, float lo,
+                                            uint32_t kp, uint32_t lane) {
+  float hi = -INFINITY;
+  for (uint32_t e = lane; e < n; e += 32) hi = fmaxf(hi, rp[e].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(XKNN_FULL_MASK, hi, o));
+  // invariant: #(> lo) > kp, #(> hi) <= kp
+  if (!(lo > -INFINITY)) {  // first compaction of a unit: start from the region's minimum
+    float mn = INFINITY;
+    for (uint32_t e = lane; e < n; e += 32) mn = fminf(mn, rp[e].x);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(XKNN_FULL_MASK, mn, o));
+    lo = nextafterf(mn, -INFINITY);
+  }
+#pragma unroll 1
+  for (int it = 0; it < 40; ++it) {
+    const float mid = 0.5f * (lo + hi);
+    if (!(mid > lo && mid < hi)) break;  // adjacent floats
+    uint32_t c = 0;
+    for (uint32_t e = lane; e < n; e += 32) c += rp[e].x > mid;
+    c = warp_sum(c);
+    if (c > kp) {
+      lo = mid;
+    } else {
+      hi = mid;
+      if (2 * c >= kp) break;
+    }
+  }
+  return hi;
+}
+
 // Merge of one row's persistent candidate list with the two regions of its unit slot: the cut
 // becomes the largest of the three cuts (every column left out of any of them scores <= it);
 // above it at most kprime entries are kept, raising the cut to the (kprime+1)-th largest score
@@ -797,38 +831,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const uint32_t c0 = t * 256 + col;
             uint32_t mask = 0;  // columns of this chunk above the current cut
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const uint32_t c = c0 + j;
-              if (vrow && v[j] > ctau && c < a.ncols && a.col_base + c != a.row_base + grow)
-                mask |= 1u << j;
-            }
-            float sc[32];  // spill-friendly copy for the (rare) dynamic-index inserts
+            for (int j = 0; j < 32; ++j) mask |= (v[j] > ctau ? 1u : 0u) << j;
+            // columns past the block's end and the row itself never enter
+            if (!vrow) mask = 0;
+            if (c0 + 32 > a.ncols) mask &= a.ncols > c0 ? (0xffffffffu >> (32 - (a.ncols - c0))) : 0u;
+            const uint32_t selfc = a.row_base + grow - a.col_base - c0;  // self column in chunk
+            if (selfc < 32) mask &= ~(1u << selfc);
+            if (!__any_sync(XKNN_FULL_MASK, mask != 0)) continue;
+            float sc[32];  // spill-friendly copy for the dynamic-index inserts
 #pragma unroll
             for (int j = 0; j < 32; ++j) sc[j] = v[j];
-            while (mask) {
-              const int j = __ffs(mask) - 1;
-              mask &= mask - 1;
-              if (!(sc[j] > ctau)) continue;  // the cut may have risen since the mask
-              if (ccnt >= cap) {
-                // region full: new cut = kprime-th largest score; keep entries above it
-                uint32_t lo = 0, hi = 0xffffffffu;
+            // warp-synchronous insertion: each round every lane inserts its next column above
+            // the cut; lanes whose region is full are compacted by the whole warp in turn
+            // (a lane-serial compaction would diverge the warp 32 ways)
 #pragma unroll 1
-                while (lo < hi) {
-                  const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
-                  uint32_t cntge = 0;
-#pragma unroll 1
-                  for (uint32_t i = 0; i < ccnt; ++i) cntge += fkey(creg[i].x) >= mid;
-                  if (cntge >= kp) lo = mid; else hi = mid - 1;
+            while (__any_sync(XKNN_FULL_MASK, mask != 0)) {
+              bool full = false;
+              if (mask) {
+                const int j = __ffs(mask) - 1;
+                const float sj = sc[j];
+                if (!(sj > ctau)) {
+                  mask &= mask - 1;
+                } else if (ccnt < cap) {
+                  creg[ccnt++] = make_float2(sj, __uint_as_float(a.col_base + c0 + j));
+                  mask &= mask - 1;
+                } else {
+                  full = true;  // bit j stays set: retried after the compaction
                 }
-                ctau = funkey(lo);
-                uint32_t w = 0;
-#pragma unroll 1
-                for (uint32_t i = 0; i < ccnt; ++i)
-                  if (creg[i].x > ctau) creg[w++] = creg[i];
-                ccnt = w;
-                if (!(sc[j] > ctau)) continue;
               }
-              creg[ccnt++] = make_float2(sc[j], __uint_as_float(a.col_base + c0 + j));
+              uint32_t fb = __ballot_sync(XKNN_FULL_MASK, full);
+              while (fb) {
+                const int f = __ffs(fb) - 1;
+                fb &= fb - 1;
+                float2* rp = reinterpret_cast<float2*>(
+                    __shfl_sync(XKNN_FULL_MASK, reinterpret_cast<unsigned long long>(creg), f));
+                const uint32_t n = __shfl_sync(XKNN_FULL_MASK, ccnt, f);
+                // new cut: a score with between kp/2 and kp entries above it (bisection in
+                // score space from [old cut, max]); the entries above it are kept
+                const float T = warp_cut_band(rp, n, __shfl_sync(XKNN_FULL_MASK, ctau, f), kp,
+                                              lane);
+                uint32_t w = 0;
+                for (uint32_t base = 0; base < n; base += 32) {
+                  const uint32_t e = base + lane;
+                  const float2 x = e < n ? rp[e] : make_float2(-INFINITY, 0.f);
+                  const bool keep = e < n && x.x > T;
+                  __syncwarp();
+                  const uint32_t bal = __ballot_sync(XKNN_FULL_MASK, keep);
+                  if (keep) rp[w + __popc(bal & ((1u << lane) - 1))] = x;
+                  w += __popc(bal);
+                  __syncwarp();
+                }
+                if ((int)lane == f) {
+                  ctau = T;
+                  ccnt = w;
+                }
+              }
             }
           }
           tc::fence_before_sync();

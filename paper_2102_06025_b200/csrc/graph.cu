@@ -419,6 +419,15 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   if (world > 1) G_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   const int next = (rank + 1) % world, prev = (rank + world - 1) % world;
 
+  // optional phase timing (XKNN_GRAPH_TIMING=1): candidates, window, exact ring, finalize
+  const bool timing = getenv("XKNN_GRAPH_TIMING") != nullptr;
+  cudaEvent_t tev[5] = {};
+  if (timing)
+    for (auto& ev : tev) {
+      G_CUDA(cudaEventCreate(&ev));
+      evs.push_back(ev);
+    }
+  if (timing) G_CUDA(cudaEventRecord(tev[0], s));
   // ---- 1. candidate ring (fp16) ----
   k_to_f16<<<grid_for(npad * 256, 256), 256, 0, s>>>(wn, n, npad, 512, own16);
   G_CUDA(cudaGetLastError());
@@ -470,6 +479,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   mem.release(buf16[1]);
 
   // ---- 2. certificate + window ----
+  if (timing) G_CUDA(cudaEventRecord(tev[1], s));
   G_CUDA(mem.get(&flag, n));
   G_CUDA(mem.get(&unc, (uint64_t)n + 1));
   G_CUDA(cudaMemsetAsync(unc, 0, 4, s));
@@ -484,6 +494,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   if (stats) stats->uncertified_rows = nu;
 
   // ---- 3. exact ring (fp32) ----
+  if (timing) G_CUDA(cudaEventRecord(tev[2], s));
   G_CUDA(mem.get(&ex, (uint64_t)n * kp));
   float* buf32[2] = {nullptr, nullptr};
   if (world > 1) {
@@ -548,6 +559,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   }
 
   // ---- 4. finalize ----
+  if (timing) G_CUDA(cudaEventRecord(tev[3], s));
   {
     uint32_t cap = 1;
     while (cap < std::max(kp, nu ? ulen : 1u)) cap <<= 1;
@@ -560,8 +572,17 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
         n, row_base, k, kp, cap, list, lcnt, ex, flag, ubuf, ulen, out);
     G_CUDA(cudaGetLastError());
   }
+  if (timing) G_CUDA(cudaEventRecord(tev[4], s));
   G_CUDA(cudaStreamSynchronize(s));
   if (cs) G_CUDA(cudaStreamSynchronize(cs));
+  if (timing) {
+    float ms[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], tev[i], tev[i + 1]);
+    fprintf(stderr,
+            "[xknn graph] rank %d rows %u k %u k' %u: candidates %.2f ms, window %.2f ms, "
+            "exact ring %.2f ms, finalize %.2f ms, uncertified %u\n",
+            rank, n, k, kp, ms[0], ms[1], ms[2], ms[3], nu);
+  }
 #undef G_CUDA
 #undef G_NCCL
   return XKNN_OK;
