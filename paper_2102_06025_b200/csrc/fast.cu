@@ -25,32 +25,6 @@ namespace {
 
 enum Kind : int { kF = 0, kDX = 1, kDW = 2, kG = 3 };
 
-template <int KIND>
-struct Cfg;
-template <>
-struct Cfg<kF> {
-  static constexpr uint32_t BK = 64, STAGES = 4;
-  static constexpr uint32_t A_BYTES = 128 * 64 * 2, B_BYTES = 256 * 64 * 2;
-  static constexpr uint32_t NBUF = 2, ACC = 256;
-};
-template <>
-struct Cfg<kDX> {
-  static constexpr uint32_t BK = 32, STAGES = 5;
-  static constexpr uint32_t A_BYTES = 128 * 32 * 2, B_BYTES = 512 * 32 * 2;
-  static constexpr uint32_t NBUF = 1, ACC = 512;
-};
-template <>
-struct Cfg<kDW> {
-  static constexpr uint32_t BK = 32, STAGES = 5;
-  static constexpr uint32_t A_BYTES = 128 * 32 * 2, B_BYTES = 512 * 32 * 2;
-  static constexpr uint32_t NBUF = 1, ACC = 512;
-};
-
-template <int KIND>
-constexpr uint32_t smem_bytes() {
-  return Cfg<KIND>::STAGES * (Cfg<KIND>::A_BYTES + Cfg<KIND>::B_BYTES) + 1024 + 256 + 2048;
-}
-
 __device__ __forceinline__ void epilogue_bar() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, 256;" ::: "memory");
 }
@@ -64,7 +38,7 @@ struct GemmArgs {
   uint64_t ldp;
   float* partial;
   float* labelterm;
-  float* out;
+  __nv_bfloat16* out16;  // GEMM-dW output (nullptr: fused update)
   // GEMM-dW fused update (normalize-backward + SgdMomentum::step_rows) -- out == nullptr
   float* W;
   float* V;
@@ -89,45 +63,6 @@ struct GemmArgs {
   float* lcut;
 };
 
-struct Tile {
-  uint32_t a_row, b_row;  // meaning depends on KIND
-  uint32_t k0, nk;
-  uint32_t id;
-};
-
-template <int KIND>
-__device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a, uint32_t mw) {
-  if (KIND == kF) return a.nbt * ((mw + 255) / 256);
-  if (KIND == kDX) return a.nbt * a.splits;
-  return (mw + 127) / 128;
-}
-
-template <int KIND>
-__device__ __forceinline__ Tile tile_of(const GemmArgs& a, uint32_t mw, uint32_t t) {
-  Tile x{};
-  x.id = t;
-  if (KIND == kF) {  // consecutive tiles share the class tile: W_sub streamed once through L2
-    x.a_row = (t % a.nbt) * 128;
-    x.b_row = (t / a.nbt) * 256;
-    x.k0 = 0;
-    x.nk = a.dim / 64;
-  } else if (KIND == kDX) {
-    const uint32_t nkc = (mw + 31) / 32;
-    const uint32_t per = (nkc + a.splits - 1) / a.splits;
-    const uint32_t s = t / a.nbt;
-    x.a_row = (t % a.nbt) * 128;
-    x.k0 = s * per;
-    const uint32_t k1 = min(nkc, x.k0 + per);
-    x.nk = k1 > x.k0 ? k1 - x.k0 : 0;
-  } else {
-    x.a_row = t * 128;  // class tile
-    x.k0 = 0;
-    x.nk = a.bpad / 32;
-  }
-  return x;
-}
-
-// 2^x on the MUFU pipe; arguments here lie in [-2s log2 e, 0] (no denormal results for s <= 40)
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -139,288 +74,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(384, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           GemmArgs a) {
-  using C = Cfg<KIND>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + C::STAGES;
-  uint64_t* tfull = bars + 2 * C::STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* xdot = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [2][128]
-
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    for (uint32_t s = 0; s < C::STAGES; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-    }
-    for (uint32_t s = 0; s < 2; ++s) {
-      tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 8);
-    }
-    tc::fence_barrier_init();
-    tc::tma_prefetch(&tmA);
-    tc::tma_prefetch(&tmB);
-  }
-  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tbase = *tmem_slot;
-
-  const uint32_t mw = a.st->active_count;
-  const uint32_t ntiles = num_tiles<KIND>(a, mw);
-
-  if (warp == 0) {
-    // ================= TMA producer =================
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile x = tile_of<KIND>(a, mw, t);
-        for (uint32_t k = 0; k < x.nk; ++k) {
-          tc::mbar_wait(&empty[stage], phase ^ 1);
-          tc::mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-          uint8_t* dA = sA + stage * C::A_BYTES;
-          uint8_t* dB = sB + stage * C::B_BYTES;
-          const int32_t kk = (int32_t)((x.k0 + k) * C::BK);
-          if (KIND == kF) {
-            tc::tma_load_2d(dA, &tmA, &full[stage], kk, (int32_t)x.a_row);
-            tc::tma_load_2d(dB, &tmB, &full[stage], kk, (int32_t)x.b_row);
-          } else if (KIND == kDX) {
-            tc::tma_load_2d(dA, &tmA, &full[stage], kk, (int32_t)x.a_row);  // P~ [b][class]
-#pragma unroll
-            for (int j = 0; j < 8; ++j)  // W_sub [class][d], 64-wide d atoms
-              tc::tma_load_2d(dB + j * 4096, &tmB, &full[stage], j * 64, kk);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 2; ++j)  // P~ᵀ: class atoms of 64 at batch rows kk..kk+31
-              tc::tma_load_2d(dA + j * 4096, &tmA, &full[stage], (int32_t)x.a_row + j * 64, kk);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)  // X_hat' [b][d]
-              tc::tma_load_2d(dB + j * 4096, &tmB, &full[stage], j * 64, kk);
-          }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile x = tile_of<KIND>(a, mw, t);
-        tc::mbar_wait(&tempty[buf], tphase ^ 1);
-        tc::fence_after_sync();
-        const uint32_t dcol = tbase + buf * C::ACC;
-        for (uint32_t k = 0; k < x.nk; ++k) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::fence_after_sync();
-          const uint32_t a0 = tc::smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = tc::smem_u32(sB + stage * C::B_BYTES);
-          if (KIND == kF) {
-            constexpr uint32_t id = tc::idesc_bf16(128, 256, false, false);
-#pragma unroll
-            for (uint32_t kk = 0; kk < 4; ++kk) {
-              const uint64_t da = tc::smem_desc(a0 + kk * 32, 16, 1024, tc::kSwizzle128);
-              const uint64_t db = tc::smem_desc(b0 + kk * 32, 16, 1024, tc::kSwizzle128);
-              tc::mma_bf16(dcol, da, db, id, (k | kk) != 0);
-            }
-          } else {
-            constexpr uint32_t id = tc::idesc_bf16(128, 256, KIND == kDW, true);
-#pragma unroll
-            for (uint32_t kk = 0; kk < 2; ++kk) {
-              const uint64_t da = KIND == kDX
-                                      ? tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64)
-                                      : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
-#pragma unroll
-              for (uint32_t nh = 0; nh < 2; ++nh) {
-                const uint64_t db =
-                    tc::smem_desc(b0 + nh * 16384 + kk * 2048, 4096, 1024, tc::kSwizzle128);
-                tc::mma_bf16(dcol + nh * 256, da, db, id, (k | kk) != 0);
-              }
-            }
-          }
-          tc::mma_commit(&empty[stage]);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-        }
-        if (x.nk) tc::mma_commit(&tfull[buf]);
-        else tc::mbar_arrive(&tfull[buf]);
-        if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
-      }
-    }
-  } else if (warp >= 4) {
-    // ================= epilogue: TMEM -> registers -> HBM =================
-    const uint32_t q = warp & 3;          // TMEM lane quadrant this warp may access
-    const uint32_t h = (warp - 4) >> 2;   // column half
-    const uint32_t row = q * 32 + lane;
-    const uint32_t lane_addr = (q * 32) << 16;
-    uint32_t buf = 0, tphase = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const Tile x = tile_of<KIND>(a, mw, t);
-      tc::mbar_wait(&tfull[buf], tphase);
-      tc::fence_after_sync();
-      const uint32_t tb = tbase + buf * C::ACC + lane_addr;
-      if (KIND == kF) {
-        const uint32_t b = x.a_row + row;
-        const bool vrow = b < a.B;
-        const int32_t lc = vrow ? a.label_col[b] : -1;
-        const float k2 = a.scale * 1.4426950408889634f;
-        float sum = 0.f, lab = 0.f;
-        bool has = false;
-#pragma unroll 1
-        for (uint32_t ch = 0; ch < 4; ++ch) {
-          const uint32_t col = h * 128 + ch * 32;
-          float v[32];
-          tc::tmem_ld32(tb + col, v);
-          const uint32_t c0 = x.b_row + col;
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            float e[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const uint32_t c = c0 + j + u;
-              const bool ok = vrow && c < mw;
-              e[u] = ok ? exp2f(fmaf(v[j + u], k2, -k2)) : 0.f;
-              sum += e[u];
-              if ((int32_t)c == lc) { lab = v[j + u] * a.scale; has = true; }
-            }
-            pk[j / 2] = pack_bf16(e[0], e[1]);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(a.Pt + (uint64_t)b * a.ldp + c0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-        const uint32_t ct = x.b_row / 256;
-        a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
-        if (has) a.labelterm[b] = lab - a.scale;
-      } else if (KIND == kDW && a.out == nullptr) {
-        // dW tile stays in TMEM: normalize-backward through the cached row norm, then momentum
-        // SGD on the weight and velocity rows (parallel.cpp:653-667, fccs.cpp:74-89), per
-        // active row.  The two column halves of a row meet through shared memory for the dot.
-        const uint32_t c = x.a_row + row;
-        const bool valid = c < mw && *a.err == 0;
-        const uint64_t grow = valid ? (uint64_t)a.active[c] - a.begin : 0;
-        float* wrow = a.W + grow * 512;
-        float* vrow = a.V + grow * 512;
-        const float norm = valid ? a.wnorm[c] : 1.f;
-        const float inv = 1.0f / norm;
-        double dot = 0.0;
-#pragma unroll 1
-        for (uint32_t ch = 0; ch < 8; ++ch) {
-          const uint32_t col = h * 256 + ch * 32;
-          float g[32];
-          tc::tmem_ld32(tb + col, g);
-          if (valid) {
-            const float4* w4 = reinterpret_cast<const float4*>(wrow + col);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const float4 w = w4[u];
-              dot += (double)g[4 * u + 0] * __fmul_rn(w.x, inv);
-              dot += (double)g[4 * u + 1] * __fmul_rn(w.y, inv);
-              dot += (double)g[4 * u + 2] * __fmul_rn(w.z, inv);
-              dot += (double)g[4 * u + 3] * __fmul_rn(w.w, inv);
-            }
-          }
-        }
-        double* xd = xdot;  // one buffer: the barrier pair keeps tiles apart
-        xd[h * 128 + row] = dot;
-        epilogue_bar();
-        const float dd = (float)(xd[row] + xd[128 + row]);
-        epilogue_bar();
-        const float lr = *a.lr, mu = a.mu, wd = a.wd;
-#pragma unroll 1
-        for (uint32_t ch = 0; ch < 8; ++ch) {
-          const uint32_t col = h * 256 + ch * 32;
-          float g[32];
-          tc::tmem_ld32(tb + col, g);
-          if (valid) {
-            float4* w4 = reinterpret_cast<float4*>(wrow + col);
-            float4* v4 = reinterpret_cast<float4*>(vrow + col);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              float4 w = w4[u], v = v4[u];
-              float gr, vv;
-#define XKNN_UPD(comp, j)                                                                     \
-  gr = __fmul_rn(__fsub_rn(g[4 * u + j], __fmul_rn(dd, __fmul_rn(w.comp, inv))), inv);      \
-  vv = __fadd_rn(__fadd_rn(__fmul_rn(mu, v.comp), gr), __fmul_rn(wd, w.comp));              \
-  v.comp = vv;                                                                                \
-  w.comp = __fsub_rn(w.comp, __fmul_rn(lr, vv));
-              XKNN_UPD(x, 0) XKNN_UPD(y, 1) XKNN_UPD(z, 2) XKNN_UPD(w, 3)
-#undef XKNN_UPD
-              w4[u] = w;
-              v4[u] = v;
-            }
-          }
-        }
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-      } else {
-        // dX: split-K partial rows (128 x 512 fp32);  dW: dW rows of this class tile
-        float* dst_row;
-        bool valid;
-        if (KIND == kDX) {
-          dst_row = a.partial + ((uint64_t)x.id * 128 + row) * 512;
-          valid = true;
-        } else {
-          const uint32_t c = x.a_row + row;
-          dst_row = a.out + (uint64_t)c * 512;
-          valid = c < mw;
-        }
-#pragma unroll 1
-        for (uint32_t ch = 0; ch < 8; ++ch) {
-          const uint32_t col = h * 256 + ch * 32;
-          float v[32];
-          if (x.nk) {
-            tc::tmem_ld32(tb + col, v);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
-          }
-          if (valid) {
-            float4* d4 = reinterpret_cast<float4*>(dst_row + col);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              d4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-          }
-        }
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-      }
-      if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 2) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tbase);
-  }
-}
-
-
-// =============================================================================================
-// CTA-pair (cta_group::2) GEMMs: M = 256 rows per pair (128 per SM), the N operand split across
-// the pair, MMAs issued by the leader CTA only, TMEM accumulators in both.  GEMM-F keeps the
-// pair's X_hat rows resident in shared memory for a whole unit, so only W_sub streams: 128
-// MAC/B of L2 traffic per SM (vs 44 for the 1-CTA kernel), under the chip's L2 bandwidth.
-// Epilogues stage each 32x32 chunk in swizzled shared memory and store with TMA (full lines).
-// =============================================================================================
 template <int KIND>
 struct Cfg2;
 template <>
@@ -807,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       uint32_t ccnt = 0;
       float ctau = -INFINITY;
       if (KIND == kG && grow < a.nrows) ctau = a.lcut[grow];
-      if (KIND == kDW && a.out == nullptr && grow < mw) {
+      if (KIND == kDW && a.out16 == nullptr && grow < mw) {
         // fused update: pull this thread's W and V row halves into L2 while the MMA runs
         const uint64_t off = ((uint64_t)a.active[grow] - a.begin) * 512 + h * 256;
         tc::prefetch_l2_bulk(a.W + off, 1024);
@@ -890,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
           if (t + 1 == ntile) {
             a.cnt[slot * 2 + h] = ccnt;
             a.tau[slot * 2 + h] = ctau;
@@ -943,10 +596,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
-        } else if (KIND == kDW && a.out == nullptr) {
+        } else if (KIND == kDW && a.out16 == nullptr) {
           // Fused normalize-backward + momentum SGD (parallel.cpp:653-667, fccs.cpp:74-89) on
           // this CTA's 128 active rows; this warp owns rows q*32.. and column half h.  Each
           // 32x32 chunk of g is transposed through the swizzled staging buffer, then lane l
@@ -1060,7 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
         } else {
           // dX: split-K partial rows of unit x.id; dW: dW rows (compact active order)
           const int32_t orow = KIND == kDX ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
@@ -1075,12 +728,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
-            stage_f32(stg + sbuf * C::STG, lane, v);
+            if (KIND == kDW) {  // dW rows in bf16 (64-B swizzled staging rows)
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) pk[j / 2] = pack_bf16(v[j], v[j + 1]);
+              stage_bf16(stg + sbuf * C::STG, lane, pk);
+            } else {
+              stage_f32(stg + sbuf * C::STG, lane, v);
+            }
             stage_flush((int32_t)col, orow);
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
         }
         if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
       }
@@ -1237,14 +897,14 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
 }  // namespace
 
 struct FastState {
-  uint32_t bpad = 0, nbt = 0, mwpad = 0, splits = 0;
-  bool pair = true;              // CTA-pair kernels (k_gemm2); XKNN_GEMM_1SM=1 selects k_gemm
+  uint32_t bpad = 0, mwpad = 0;
   uint64_t dx_units_cap = 0;
-  float* partial_f = nullptr;   // [2 * mwpad/256][bpad]
-  float* labelterm = nullptr;   // [bpad]
-  float* partial_dx = nullptr;  // [units][rows per unit][512]
-  CUtensorMap mF_A, mF_B, mDX_A, mDX_B, mDW_A, mDW_B;
-  CUtensorMap mF2_B, mPt_st, mDXP_st, mDW_st;
+  float* partial_f = nullptr;       // [2 * mwpad/256][bpad]
+  float* labelterm = nullptr;       // [bpad]
+  float* partial_dx = nullptr;      // [units][256][512]
+  __nv_bfloat16* dW16 = nullptr;    // [mwpad][512] weight gradient, compact active order
+  CUtensorMap mF_A, mF2_B, mDX_A, mDX_B, mDW_A, mDW_B;
+  CUtensorMap mPt_st, mDXP_st, mDW_st;
 };
 
 // splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
@@ -1266,24 +926,9 @@ xknn_status_t Layer::init_fast() {
   auto* f = new FastState;
   fast = f;
   if (d != 512) return fail_msg(XKNN_ERR_UNSUPPORTED, "BF16 path is specialised for D = 512");
-  const char* env1 = getenv("XKNN_GEMM_1SM");
-  f->pair = !(env1 && env1[0] == '1');
   f->bpad = (uint32_t)((bmax + 255) / 256 * 256);
-  f->nbt = f->bpad / 128;
   f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
   ldp = f->mwpad;
-  // split-K of GEMM-dX: enough (batch tile, class range) units to fill the SMs in whole waves
-  {
-    uint32_t best = 1;
-    double best_eff = 0;
-    for (uint32_t s = 1; s <= 64; ++s) {
-      const uint32_t units = f->nbt * s;
-      const double eff = (double)units / (((units + kNumSMs - 1) / kNumSMs) * kNumSMs);
-      if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
-      if (units >= 2 * kNumSMs) break;
-    }
-    f->splits = best;
-  }
   XK_CUDA(dalloc(&Xhat16, (uint64_t)f->bpad * d));
   XK_CUDA(dalloc(&Xs16, (uint64_t)f->bpad * d));
   XK_CUDA(cudaMemsetAsync(Xhat16, 0, (uint64_t)f->bpad * d * 2, stream));
@@ -1293,33 +938,22 @@ xknn_status_t Layer::init_fast() {
   XK_CUDA(cudaMemsetAsync(Pt, 0, (uint64_t)f->bpad * ldp * 2, stream));
   XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
   XK_CUDA(dalloc(&f->labelterm, f->bpad));
-  f->dx_units_cap = std::max<uint64_t>((uint64_t)f->nbt * f->splits * 128,
-                                        (uint64_t)(f->bpad / 256) *
-                                            pair_splits(f->bpad / 256, 296) * 256);
+  f->dx_units_cap = (uint64_t)(f->bpad / 256) * pair_splits(f->bpad / 256, 148) * 256;
   XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
-  // fast path dW holds whole 256-class pair tiles
-  if (dW) cudaFree(dW);
-  XK_CUDA(dalloc(&dW, (uint64_t)f->mwpad * d));
+  XK_CUDA(dalloc(&f->dW16, (uint64_t)f->mwpad * d));
   XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
   bool ok = true;
   ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&f->mF_B, Wsub16, d, f->mwpad, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mF2_B, Wsub16, d, f->mwpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
   ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&f->mF2_B, Wsub16, d, f->mwpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mPt_st, Pt, ldp, f->bpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   ok &= make_map(&f->mDXP_st, f->partial_dx, 512, f->dx_units_cap, 32, 32,
                  CU_TENSOR_MAP_SWIZZLE_128B, true);
-  ok &= make_map(&f->mDW_st, dW, 512, f->mwpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  ok &= make_map(&f->mDW_st, f->dW16, 512, f->mwpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  XK_CUDA(cudaFuncSetAttribute(k_gemm<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem_bytes<kF>()));
-  XK_CUDA(cudaFuncSetAttribute(k_gemm<kDX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem_bytes<kDX>()));
-  XK_CUDA(cudaFuncSetAttribute(k_gemm<kDW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem_bytes<kDW>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes2<kF>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1335,6 +969,7 @@ void Layer::free_fast() {
   if (f->partial_f) cudaFree(f->partial_f);
   if (f->labelterm) cudaFree(f->labelterm);
   if (f->partial_dx) cudaFree(f->partial_dx);
+  if (f->dW16) cudaFree(f->dW16);
   delete f;
   fast = nullptr;
 }
@@ -1357,24 +992,19 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.st = st;
   ga.B = (uint32_t)B;
   ga.bpad = f->bpad;
-  ga.nbt = (uint32_t)((B + 127) / 128);
-  ga.splits = f->splits;
   ga.dim = D;
   ga.scale = cfg.scale;
   ga.label_col = label_col;
   ga.Pt = Pt;
   ga.ldp = ldp;
   ga.labelterm = f->labelterm;
-  // (b) GEMM-F with the fused exp/row-sum/label-logit epilogue
-  ga.partial = f->partial_f;
+  // (b) GEMM-F with the fused exp/row-sum/label-logit epilogue; units are (256-row pair tile,
+  //     class-tile range)
   const uint32_t nbp = (uint32_t)((B + 255) / 256);
-  if (f->pair) {
-    ga.nbt = nbp;
-    ga.splits = pair_splits(nbp, 1u << 30);  // units are (pair tile, class-tile range)
-    k_gemm2<kF><<<kNumSMs, 384, smem_bytes2<kF>(), stream>>>(f->mF_A, f->mF2_B, f->mPt_st, ga);
-  } else {
-    k_gemm<kF><<<kNumSMs, 384, smem_bytes<kF>(), stream>>>(f->mF_A, f->mF_B, ga);
-  }
+  ga.partial = f->partial_f;
+  ga.nbt = nbp;
+  ga.splits = pair_splits(nbp, 1u << 30);
+  k_gemm2<kF><<<kNumSMs, 384, smem_bytes2<kF>(), stream>>>(f->mF_A, f->mF2_B, f->mPt_st, ga);
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over class shards -> loss
@@ -1389,10 +1019,10 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
       rowred, label_col, X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16);
   XK_LAUNCH();
   mark(5);
-  // (e) GEMM-dW; with XKNN_FLAG_FUSED_UPDATE the normalize-backward + momentum-SGD update
-  //     runs in its epilogue (otherwise dW goes to HBM and k_update_rows applies it)
+  // (e) GEMM-dW -> bf16 dW (compact active order); with XKNN_FLAG_FUSED_UPDATE the
+  //     normalize-backward + momentum-SGD update runs in its epilogue instead
   const bool fused = (cfg.flags & XKNN_FLAG_FUSED_UPDATE) != 0;
-  ga.out = fused ? nullptr : dW;
+  ga.out16 = fused ? nullptr : f->dW16;
   ga.W = W;
   ga.V = V;
   ga.active = active;
@@ -1402,43 +1032,32 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.mu = cfg.momentum;
   ga.wd = cfg.weight_decay;
   ga.err = err;
-  if (f->pair) {
-    k_gemm2<kDW><<<kNumSMs, 384, smem_bytes2<kDW>(), stream>>>(f->mDW_A, f->mDW_B, f->mDW_st, ga);
-  } else {
-    k_gemm<kDW><<<kNumSMs, 384, smem_bytes<kDW>(), stream>>>(f->mDW_A, f->mDW_B, ga);
-  }
+  k_gemm2<kDW><<<kNumSMs, 384, smem_bytes2<kDW>(), stream>>>(f->mDW_A, f->mDW_B, f->mDW_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
   ga.partial = f->partial_dx;
-  uint32_t dx_rows, dx_tiles, dx_splits;
-  if (f->pair) {
-    dx_rows = 256;
-    dx_tiles = nbp;
-    dx_splits = pair_splits(nbp, 148);
-    ga.nbt = dx_tiles;
-    ga.splits = dx_splits;
-    k_gemm2<kDX><<<kNumSMs, 384, smem_bytes2<kDX>(), stream>>>(f->mDX_A, f->mDX_B, f->mDXP_st,
-                                                               ga);
-  } else {
-    dx_rows = 128;
-    dx_tiles = (uint32_t)((B + 127) / 128);
-    dx_splits = f->splits;
-    ga.nbt = dx_tiles;
-    ga.splits = dx_splits;
-    k_gemm<kDX><<<kNumSMs, 384, smem_bytes<kDX>(), stream>>>(f->mDX_A, f->mDX_B, ga);
-  }
+  const uint32_t dx_splits = pair_splits(nbp, 148);
+  ga.nbt = nbp;
+  ga.splits = dx_splits;
+  k_gemm2<kDX><<<kNumSMs, 384, smem_bytes2<kDX>(), stream>>>(f->mDX_A, f->mDX_B, f->mDXP_st, ga);
   XK_LAUNCH();
   mark(7);
   k_dx_reduce<<<grid_for(B * 128, 256), 256, 0, stream>>>(f->partial_dx, rowred, (uint32_t)B,
-                                                           dx_tiles, dx_splits, dx_rows, cfg.scale,
-                                                           dXpart);
+                                                           nbp, dx_splits, 256, cfg.scale, dXpart);
   XK_LAUNCH();
   const uint64_t bl = B / world;
   if (world > 1)
     XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
   else
     XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  // (g) normalize-backward + momentum SGD on the active rows (parallel.cpp:649-667)
+  mark(8);
+  if (!fused) {
+    XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
+                                    wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream));
+    ++launches;
+  }
   return XKNN_OK;
 }
 

@@ -14,6 +14,11 @@ cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
                                const unsigned long long* err, cudaStream_t s,
                                unsigned max_grid = 148u * 16u);
+cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
+                                    const uint32_t* active, const unsigned int* count,
+                                    uint64_t max_rows, uint64_t begin, uint32_t d,
+                                    const float* wnorm, const float* lr, float mu, float wd,
+                                    const unsigned long long* err, cudaStream_t s);
 cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
                                     uint64_t rows, uint32_t d, float* out, cudaStream_t s);
 

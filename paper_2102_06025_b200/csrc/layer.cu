@@ -110,9 +110,9 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(dalloc(&wnorm, mw_cap));
   XK_CUDA(dalloc(&rowmax, bmax));
   XK_CUDA(dalloc(&rowred, 3 * bmax));
-  XK_CUDA(dalloc(&dW, mw_cap * d));
   XK_CUDA(dalloc(&dX, bmax * d));
   if (cfg.precision == XKNN_PREC_FP32_EXACT) {
+    XK_CUDA(dalloc(&dW, mw_cap * d));
     XK_CUDA(dalloc(&Xhat, bmax * d));
     XK_CUDA(dalloc(&Wsub, mw_cap * d));
     XK_CUDA(dalloc(&logits, bmax * mw_cap * 2));  // logits, then G
@@ -261,11 +261,10 @@ xknn_status_t Layer::run_core(uint64_t B) {
     XK_TRY(run_fast_core(B));
   }
   // (8) normalize-backward + momentum SGD on the active rows only (parallel.cpp:649-667);
-  //     fused into the GEMM-dW epilogue in BF16 precision
-  mark(8);
-  // (an overlap of this HBM-bound kernel with the L2-bound feature-gradient GEMM on a side
-  //  stream was measured slower: both saturate the memory system)
-  if (cfg.precision == XKNN_PREC_FP32_EXACT || !(cfg.flags & XKNN_FLAG_FUSED_UPDATE)) {
+  //     the BF16 path runs it at the end of run_fast_core (from its bf16 dW, or fused into
+  //     the GEMM-dW epilogue)
+  if (cfg.precision == XKNN_PREC_FP32_EXACT) {
+    mark(8);
     XK_CUDA(launch_update_rows(W, V, dW, active, cnt, mw_cap, begin, D, wnorm, lr_dev,
                                cfg.momentum, cfg.weight_decay, err, stream));
     ++launches;

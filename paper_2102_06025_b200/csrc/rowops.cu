@@ -79,9 +79,18 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
 // Normalize-backward of each active row through its cached norm, then SgdMomentum::step_rows
 // on (W, V).  g rows are compact (row t <-> active[t]).  Skipped entirely if any error was
 // raised earlier in the step (the reference throws before touching parameters).
-template <int DV>
+__device__ __forceinline__ float4 load_g4(const float* __restrict__ G, uint64_t i) {
+  return reinterpret_cast<const float4*>(G)[i];
+}
+__device__ __forceinline__ float4 load_g4(const __nv_bfloat16* __restrict__ G, uint64_t i) {
+  const uint2 u = reinterpret_cast<const uint2*>(G)[i];
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
+
+template <int DV, typename GT>
 __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
-                              const float* __restrict__ G, const uint32_t* __restrict__ active,
+                              const GT* __restrict__ G, const uint32_t* __restrict__ active,
                               const unsigned int* count, uint64_t begin, uint32_t d,
                               const float* __restrict__ wnorm, const float* __restrict__ lr_dev,
                               float mu, float wd, const unsigned long long* err) {
@@ -94,7 +103,7 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
     const uint64_t row = (uint64_t)active[t] - begin;
     float4* wp = reinterpret_cast<float4*>(W + row * d);
     float4* vp = reinterpret_cast<float4*>(V + row * d);
-    const float4* gp = reinterpret_cast<const float4*>(G + t * d);
+    const uint64_t g0 = t * d / 4;
     const float norm = wnorm[t];
     const float inv = 1.0f / norm;
     float4 w[DV], g[DV], nh[DV];
@@ -102,7 +111,7 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
 #pragma unroll
     for (int c = 0; c < DV; ++c) {
       w[c] = wp[lane + 32 * c];
-      g[c] = gp[lane + 32 * c];
+      g[c] = load_g4(G, g0 + lane + 32 * c);
       nh[c].x = __fmul_rn(w[c].x, inv);
       nh[c].y = __fmul_rn(w[c].y, inv);
       nh[c].z = __fmul_rn(w[c].z, inv);
@@ -203,6 +212,18 @@ cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_
   const unsigned grid = grid_for(max_rows * 32, 256, max_grid);
   XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,
                   wd, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
+                                    const uint32_t* active, const unsigned int* count,
+                                    uint64_t max_rows, uint64_t begin, uint32_t d,
+                                    const float* wnorm, const float* lr, float mu, float wd,
+                                    const unsigned long long* err, cudaStream_t s) {
+  if (d != 512) return cudaErrorInvalidValue;
+  const unsigned grid = grid_for(max_rows * 32, 256, 148u * 16u);
+  k_update_rows<4, __nv_bfloat16><<<grid, 256, 0, s>>>(W, V, G, active, count, begin, d, wnorm,
+                                                       lr, mu, wd, err);
   return cudaGetLastError();
 }
 

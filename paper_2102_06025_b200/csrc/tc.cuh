@@ -123,6 +123,17 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
       "r"(rank)
       : "memory");
 }
+// relaxed variant for TMEM-empty signals: the arriving threads' tcgen05.ld have completed
+// (tcgen05.wait::ld), so no memory ordering is needed -- and a release would stall on the
+// epilogue's outstanding global stores
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
 // 2-SM TMA load: data lands in this CTA's smem, completion is counted on the leader CTA's
 // barrier (peer bit of the shared::cluster address cleared)
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m,
