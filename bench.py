@@ -236,8 +236,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
     with torch.cuda.stream(stream):
         layer = X.KnnSoftmaxLayer(n, D, rank=rank, world=world, m_active=m, max_batch=b,
                                   scale=SCALE, momentum=MOMENTUM, rng_seed=SEED, precision=prec,
-                                  comm=comm, stream=stream,
-                                  fused_update=args.fused_update)
+                                  comm=comm, stream=stream)
         gw = torch.Generator(device="cuda")
         gw.manual_seed(10 + rank)
         wv = layer.weights_view().tensor
@@ -402,8 +401,6 @@ def main():
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fused-update", action="store_true",
-                    help="row update in the GEMM-dW epilogue instead of a separate kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
 

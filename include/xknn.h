@@ -70,9 +70,6 @@ typedef struct {
 /* The step's device work (selection .. update) is captured once per batch size into a CUDA
    graph and replayed; this flag launches it kernel by kernel instead. */
 #define XKNN_FLAG_NO_GRAPH 1
-/* BF16: apply the normalize-backward + momentum-SGD update inside the weight-gradient GEMM's
-   epilogue instead of a separate row kernel (experimental). */
-#define XKNN_FLAG_FUSED_UPDATE 2
 
 typedef struct xknn_layer xknn_layer_t;
 

@@ -29,7 +29,6 @@ VP = C.c_void_p
 PREC_BF16 = 0
 PREC_FP32_EXACT = 1
 FLAG_NO_GRAPH = 1
-FLAG_FUSED_UPDATE = 2
 
 
 class XknnConfig(C.Structure):
@@ -203,14 +202,13 @@ class KnnSoftmaxLayer:
     def __init__(self, num_classes: int, dim: int, *, rank: int = 0, world: int = 1,
                  m_active: int, max_batch: int, scale: float = 30.0, momentum: float = 0.9,
                  weight_decay: float = 0.0, rng_seed: int = 0, precision: int = PREC_BF16,
-                 comm=None, stream=None, use_graph: bool = True, fused_update: bool = False):
+                 comm=None, stream=None, use_graph: bool = True):
         import torch  # plumbing only: device memory and streams
 
         self._torch = torch
         self.num_classes, self.dim, self.rank, self.world = num_classes, dim, rank, world
         self.cfg = XknnConfig(scale, momentum, weight_decay, m_active, rng_seed, max_batch,
-                              precision, (0 if use_graph else FLAG_NO_GRAPH) |
-                              (FLAG_FUSED_UPDATE if fused_update else 0))
+                              precision, (0 if use_graph else FLAG_NO_GRAPH))
         # the layer works on its own stream (capturable into a CUDA graph); every call is
         # ordered after the caller's current stream and the caller's stream after it
         self.stream = stream if stream is not None else torch.cuda.Stream()

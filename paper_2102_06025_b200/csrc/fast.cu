@@ -38,16 +38,7 @@ struct GemmArgs {
   uint64_t ldp;
   float* partial;
   float* labelterm;
-  __nv_bfloat16* out16;  // GEMM-dW output (nullptr: fused update)
-  // GEMM-dW fused update (normalize-backward + SgdMomentum::step_rows) -- out == nullptr
-  float* W;
-  float* V;
-  const uint32_t* active;
-  uint64_t begin;
-  const float* wnorm;
-  const float* lr;
-  float mu, wd;
-  const unsigned long long* err;
+  __nv_bfloat16* out16;  // GEMM-dW output rows (bf16, compact active order)
   // graph build (kG): own rows (A, global ids row_base..) against a held block of ncols
   // columns (B, global ids col_base..).  Per in-flight unit slot (pair * 256 + row): two
   // candidate regions [slot][half][ch] of (approx score, column id) with counts/cuts; per own
@@ -105,8 +96,7 @@ struct Cfg2<kG> {
 template <int KIND>
 constexpr uint32_t smem_bytes2() {
   using C = Cfg2<KIND>;
-  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * 2 * C::STG + 1024 + 256 +
-         (KIND == kDW ? 2048 + 64 : 0);  // dW: fp64 row-dot exchange of the fused update
+  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * 2 * C::STG + 1024 + 256;
 }
 
 struct Unit2 {
@@ -460,12 +450,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       uint32_t ccnt = 0;
       float ctau = -INFINITY;
       if (KIND == kG && grow < a.nrows) ctau = a.lcut[grow];
-      if (KIND == kDW && a.out16 == nullptr && grow < mw) {
-        // fused update: pull this thread's W and V row halves into L2 while the MMA runs
-        const uint64_t off = ((uint64_t)a.active[grow] - a.begin) * 512 + h * 256;
-        tc::prefetch_l2_bulk(a.W + off, 1024);
-        tc::prefetch_l2_bulk(a.V + off, 1024);
-      }
       for (uint32_t t = 0; t < ntile; ++t) {
         tc::mbar_wait(&tfull[buf], tphase);
         tc::fence_after_sync();
@@ -599,121 +583,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
-        } else if (KIND == kDW && a.out16 == nullptr) {
-          // Fused normalize-backward + momentum SGD (parallel.cpp:653-667, fccs.cpp:74-89) on
-          // this CTA's 128 active rows; this warp owns rows q*32.. and column half h.  Each
-          // 32x32 chunk of g is transposed through the swizzled staging buffer, then lane l
-          // works on row 4*i + l/8, columns 4*(l%8).. of the chunk: float4 accesses, four
-          // 128-B row segments per instruction.  W/V were prefetched into L2 above.
-          const uint32_t cr = x.row0 + cta * 128 + row;  // lane r owns row r's metadata
-          const bool vr = cr < mw && *a.err == 0;
-          const uint32_t gr = vr ? a.active[cr] - (uint32_t)a.begin : 0;
-          const float invr = vr ? 1.0f / a.wnorm[cr] : 1.0f;
-          const uint32_t sub = lane >> 3, c4 = lane & 7;
-          uint8_t* tb_s = stg;  // transpose buffer (32 rows x 128 B, SW128)
-          uint32_t rg[8];
-          float rinv[8];
-          bool rv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t r = 4 * i + sub;
-            rg[i] = __shfl_sync(XKNN_FULL_MASK, gr, r);
-            rinv[i] = __shfl_sync(XKNN_FULL_MASK, invr, r);
-            rv[i] = __shfl_sync(XKNN_FULL_MASK, vr, r);
-          }
-          double p[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) p[i] = 0.0;
-#pragma unroll 1
-          for (uint32_t ch = 0; ch < 8; ++ch) {
-            const uint32_t col = h * 256 + ch * 32;
-            {
-              float v[32];
-              tc::tmem_ld32(tb + col, v);
-              stage_f32(tb_s, lane, v);
-            }
-            __syncwarp();
-            float4 w4[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              w4[i] = rv[i] ? *reinterpret_cast<const float4*>(a.W + (uint64_t)rg[i] * 512 + col +
-                                                               c4 * 4)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint32_t r = 4 * i + sub;
-              const float4 g = *reinterpret_cast<const float4*>(tb_s + r * 128 +
-                                                                ((c4 ^ (r & 7)) * 16));
-              p[i] += (double)g.x * (double)__fmul_rn(w4[i].x, rinv[i]);
-              p[i] += (double)g.y * (double)__fmul_rn(w4[i].y, rinv[i]);
-              p[i] += (double)g.z * (double)__fmul_rn(w4[i].z, rinv[i]);
-              p[i] += (double)g.w * (double)__fmul_rn(w4[i].w, rinv[i]);
-            }
-            __syncwarp();
-          }
-          // row dots: the 8 lanes of a row, then the two column halves
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1) p[i] += __shfl_xor_sync(XKNN_FULL_MASK, p[i], o);
-          }
-          double* xd = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 64);
-          if (c4 == 0) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) xd[h * 128 + q * 32 + 4 * i + sub] = p[i];
-          }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          float rdd[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t r = q * 32 + 4 * i + sub;
-            rdd[i] = (float)(xd[r] + xd[128 + r]);
-          }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          const float lr = *a.lr, mu = a.mu, wd = a.wd;
-#pragma unroll 1
-          for (uint32_t ch = 0; ch < 8; ++ch) {
-            const uint32_t col = h * 256 + ch * 32;
-            {
-              float v[32];
-              tc::tmem_ld32(tb + col, v);
-              stage_f32(tb_s, lane, v);
-            }
-            __syncwarp();
-            float4 w4[8], v4[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint64_t off = (uint64_t)rg[i] * 512 + col + c4 * 4;
-              if (rv[i]) {
-                w4[i] = *reinterpret_cast<const float4*>(a.W + off);
-                v4[i] = *reinterpret_cast<const float4*>(a.V + off);
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (!rv[i]) continue;
-              const uint32_t r = 4 * i + sub;
-              const float4 g = *reinterpret_cast<const float4*>(tb_s + r * 128 +
-                                                                ((c4 ^ (r & 7)) * 16));
-              const float inv = rinv[i], dd = rdd[i];
-              float4 w = w4[i], v = v4[i];
-#define XKNN_FUPD(c)                                                                         \
-  {                                                                                          \
-    const float grd = __fmul_rn(__fsub_rn(g.c, __fmul_rn(dd, __fmul_rn(w.c, inv))), inv);    \
-    v.c = __fadd_rn(__fadd_rn(__fmul_rn(mu, v.c), grd), __fmul_rn(wd, w.c));                 \
-    w.c = __fsub_rn(w.c, __fmul_rn(lr, v.c));                                                \
-  }
-              XKNN_FUPD(x) XKNN_FUPD(y) XKNN_FUPD(z) XKNN_FUPD(w)
-#undef XKNN_FUPD
-              const uint64_t off = (uint64_t)rg[i] * 512 + col + c4 * 4;
-              *reinterpret_cast<float4*>(a.V + off) = v;
-              *reinterpret_cast<float4*>(a.W + off) = w;
-            }
-            __syncwarp();
-          }
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
         } else {
           // dX: split-K partial rows of unit x.id; dW: dW rows (compact active order)
           const int32_t orow = KIND == kDX ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
@@ -1019,19 +888,8 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
       rowred, label_col, X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16);
   XK_LAUNCH();
   mark(5);
-  // (e) GEMM-dW -> bf16 dW (compact active order); with XKNN_FLAG_FUSED_UPDATE the
-  //     normalize-backward + momentum-SGD update runs in its epilogue instead
-  const bool fused = (cfg.flags & XKNN_FLAG_FUSED_UPDATE) != 0;
-  ga.out16 = fused ? nullptr : f->dW16;
-  ga.W = W;
-  ga.V = V;
-  ga.active = active;
-  ga.begin = begin;
-  ga.wnorm = wnorm;
-  ga.lr = lr_dev;
-  ga.mu = cfg.momentum;
-  ga.wd = cfg.weight_decay;
-  ga.err = err;
+  // (e) GEMM-dW -> bf16 dW rows (compact active order)
+  ga.out16 = f->dW16;
   k_gemm2<kDW><<<kNumSMs, 384, smem_bytes2<kDW>(), stream>>>(f->mDW_A, f->mDW_B, f->mDW_st, ga);
   XK_LAUNCH();
   mark(6);
@@ -1052,12 +910,12 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   else
     XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
   // (g) normalize-backward + momentum SGD on the active rows (parallel.cpp:649-667)
+  //     (a separate HBM-streaming kernel: it runs at the copy roofline, while inside the
+  //     GEMM-dW kernel the few spare warps per SM could not keep enough bytes in flight)
   mark(8);
-  if (!fused) {
-    XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
-                                    wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream));
-    ++launches;
-  }
+  XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
+                                  wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream));
+  ++launches;
   return XKNN_OK;
 }
 

@@ -106,12 +106,17 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
     const uint64_t g0 = t * d / 4;
     const float norm = wnorm[t];
     const float inv = 1.0f / norm;
-    float4 w[DV], g[DV], nh[DV];
+    float4 w[DV], g[DV], nh[DV], vel[DV];
     double dot = 0.0;
+    // every load of the row in flight before the first use (W, G, V: 3 x 2 KiB per warp)
 #pragma unroll
     for (int c = 0; c < DV; ++c) {
       w[c] = wp[lane + 32 * c];
       g[c] = load_g4(G, g0 + lane + 32 * c);
+      vel[c] = vp[lane + 32 * c];
+    }
+#pragma unroll
+    for (int c = 0; c < DV; ++c) {
       nh[c].x = __fmul_rn(w[c].x, inv);
       nh[c].y = __fmul_rn(w[c].y, inv);
       nh[c].z = __fmul_rn(w[c].z, inv);
@@ -126,7 +131,7 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
     const float inv2 = 1.0f / norm;
 #pragma unroll
     for (int c = 0; c < DV; ++c) {
-      float4 v = vp[lane + 32 * c];
+      float4 v = vel[c];
       float gr, vv;
 #define XKNN_UPD(comp)                                                                  \
   gr = __fmul_rn(__fsub_rn(g[c].comp, __fmul_rn(dd, nh[c].comp)), inv2);               \
