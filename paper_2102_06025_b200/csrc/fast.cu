@@ -68,35 +68,35 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int KIND>
 struct Cfg2;
 template <>
-struct Cfg2<kF> {
-  static constexpr uint32_t STAGES = 4, A_BYTES = 0, B_BYTES = 128 * 64 * 2;
+struct Cfg2<kF> {  // P~ rows leave through one staging block per warp (plain stores)
+  static constexpr uint32_t STAGES = 5, A_BYTES = 0, B_BYTES = 128 * 64 * 2;
   static constexpr uint32_t ARES_BYTES = 8 * 128 * 64 * 2;  // resident X_hat: 128 rows x 512
-  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 2048;  // staging per warp buffer
+  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 2048, NSTG = 1;
 };
 template <>
 struct Cfg2<kDX> {
   static constexpr uint32_t STAGES = 6, A_BYTES = 128 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
   static constexpr uint32_t ARES_BYTES = 0;
-  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096;
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = 2;  // TMA-store staging
 };
 template <>
 struct Cfg2<kDW> {
   static constexpr uint32_t STAGES = 6, A_BYTES = 2 * 64 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
   static constexpr uint32_t ARES_BYTES = 0;
-  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096;
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = 2;  // TMA-store staging
 };
 
 template <>
 struct Cfg2<kG> {
   static constexpr uint32_t STAGES = 6, A_BYTES = 0, B_BYTES = 128 * 64 * 2;
   static constexpr uint32_t ARES_BYTES = 8 * 128 * 64 * 2;
-  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 0;
+  static constexpr uint32_t NBUF = 2, ACC = 256, STG = 0, NSTG = 0;
 };
 
 template <int KIND>
 constexpr uint32_t smem_bytes2() {
   using C = Cfg2<KIND>;
-  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * 2 * C::STG + 1024 + 256;
+  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * C::NSTG * C::STG + 1024 + 256;
 }
 
 struct Unit2 {
@@ -153,6 +153,22 @@ __device__ __forceinline__ void stage_bf16(uint8_t* buf, uint32_t r, const uint3
     uint4* d = reinterpret_cast<uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
     *d = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
   }
+}
+
+// 32 rows x 32 bf16 of a 64-B-swizzled staging block (stage_bf16) to global rows `ld` elements
+// apart: lane l writes row 8i + l/4, 16-B column unit l%4 -- eight 64-B row segments per
+// instruction instead of 32 scattered ones, no async-proxy round trip.  Caller: __syncwarp()
+// after staging; the block may be overwritten after this returns (+ __syncwarp).
+__device__ __forceinline__ void store_bf16_block(const uint8_t* buf, __nv_bfloat16* dst, uint64_t ld,
+                                                 uint32_t lane) {
+  const uint32_t c = lane & 3;
+#pragma unroll
+  for (uint32_t i = 0; i < 4; ++i) {
+    const uint32_t r = 8 * i + (lane >> 2);
+    const uint4 v = *reinterpret_cast<const uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
+    *reinterpret_cast<uint4*>(dst + (uint64_t)r * ld + c * 8) = v;
+  }
+  __syncwarp();
 }
 
 // order-preserving float -> uint32 key (larger score, larger key)
@@ -271,8 +287,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint8_t* sRes = smem;                                      // F: resident A
   uint8_t* sA = sRes + C::ARES_BYTES;                        // staged A
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;                 // staged B
-  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;               // epilogue staging, 8 warps x 2
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 2 * C::STG);
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;               // epilogue staging, 8 warps
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * C::NSTG * C::STG);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -425,7 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const uint32_t q = warp & 3, h = (warp - 4) >> 2, ew = warp - 4;
     const uint32_t row = q * 32 + lane;
     const uint32_t lane_addr = (q * 32) << 16;
-    uint8_t* stg = sStg + ew * 2 * C::STG;
+    uint8_t* stg = sStg + ew * C::NSTG * C::STG;
     uint32_t sbuf = 0;
     uint32_t buf = 0, tphase = 0;
     auto stage_flush = [&](int32_t c0, int32_t r0) {
@@ -575,8 +591,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               lab = sel * a.scale;
               has = true;
             }
-            stage_bf16(stg + sbuf * C::STG, lane, pk);
-            stage_flush((int32_t)c0, grow0);
+            stage_bf16(stg, lane, pk);
+            __syncwarp();
+            store_bf16_block(stg, a.Pt + (uint64_t)grow0 * a.ldp + c0, a.ldp, lane);
           }
           tc::fence_before_sync();
           __syncwarp();
