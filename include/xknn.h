@@ -198,9 +198,30 @@ xknn_status_t xknn_layer_set_graph_rows(xknn_layer_t* h, const uint32_t* rows_de
 
 /* The periodic graph refresh of the paper on the live layer: l2_normalize_rows of every rank's
    weight shard (matrix.cpp:12-29, bit-exact; ZeroNormRow), xknn_graph_ring over the shards,
-   then xknn_layer_set_graph_rows.  Collective.  Synchronizes. */
+   then xknn_layer_set_graph_rows.  rows_out_dev (may be NULL) receives this rank's rows
+   [begin, end) x k of the full graph (e.g. for xknn_graph_save_rows).  Collective.
+   Synchronizes. */
 xknn_status_t xknn_layer_rebuild_graph(xknn_layer_t* h, uint32_t k, uint32_t kprime,
-                                       uint64_t* uncertified_rows);
+                                       uint32_t* rows_out_dev, uint64_t* uncertified_rows);
+
+/* save_graph (knn_graph.cpp:276-291) for a row-distributed KnnGraph: writes classes
+   [begin, end) (rows: (end - begin) x k u32, host or device) as XKNN v1 records ("XKNN", u32
+   version 1, u64 num_classes, then per class u32 k + k u32 ids, little-endian) at their byte
+   offsets.  create != 0 creates/truncates the file and writes the header: one writer (rank 0)
+   does that first, then every shard writes its own rows (records have a fixed size).  IoError
+   on open/write failure. */
+xknn_status_t xknn_graph_save_rows(const char* path, uint64_t num_classes, uint32_t k,
+                                   uint64_t begin, uint64_t end, const uint32_t* rows,
+                                   int on_device, int create);
+
+/* load_graph (knn_graph.cpp:293-311) restricted to classes [begin, end): IoError for a file that
+   cannot be opened, a bad magic, an unsupported version, truncation, or a record whose k differs
+   from class 0's ("per-class k varies; not a full graph"); ShapeMismatch when the file's class
+   count differs from num_classes (compress_graph's layout check).  *k_out receives the file's
+   k; rows (capacity entries, host or device; NULL: header only) receives (end - begin) x k ids. */
+xknn_status_t xknn_graph_load_rows(const char* path, uint64_t num_classes, uint64_t begin,
+                                   uint64_t end, uint32_t* rows, uint64_t capacity, int on_device,
+                                   uint32_t* k_out);
 
 /* The installed CompressedKnnGraph of this shard (knn_graph.hpp:46-55): k_per_class and
    offsets [num_classes], flat [*flat_len] (flat_capacity >= *flat_len, else ShapeMismatch);

@@ -114,6 +114,27 @@ int ref_build_graph_ring(uint64_t n, uint64_t d, const float* w, uint64_t p, uin
   })
 }
 
+// save_graph / load_graph (knn_graph.cpp:276-311).  load: *n and *k out; flat (>= n*k) may be
+// NULL to query the sizes only.
+int ref_save_graph(const char* path, uint64_t n, uint64_t k, const uint32_t* g_flat) {
+  GUARD({
+    KnnGraph g;
+    g.num_classes = n;
+    g.k = k;
+    g.flat.assign(g_flat, g_flat + n * k);
+    save_graph(g, path);
+  })
+}
+
+int ref_load_graph(const char* path, uint64_t* n, uint64_t* k, uint32_t* flat) {
+  GUARD({
+    auto g = load_graph(path);
+    *n = g.num_classes;
+    *k = g.k;
+    if (flat) std::memcpy(flat, g.flat.data(), g.flat.size() * sizeof(uint32_t));
+  })
+}
+
 // Returns Σ kept through *total; arrays sized by caller (flat_out ≥ n*k).
 int ref_compress_graph(uint64_t n, uint64_t k, const uint32_t* g_flat, uint64_t p, uint64_t shard,
                        uint32_t* kpc, uint64_t* offsets, uint32_t* flat_out, uint64_t* total) {

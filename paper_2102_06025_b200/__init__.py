@@ -11,6 +11,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libxknn.so")
 
@@ -107,7 +109,10 @@ for _name, _args in {
     "xknn_graph_ring": [VP, U64, U64, C.c_uint32, C.c_uint32, C.c_int, C.c_int, VP, VP, VP,
                         C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_set_graph_rows": [VP, VP, C.c_uint32],
-    "xknn_layer_rebuild_graph": [VP, C.c_uint32, C.c_uint32, C.POINTER(U64)],
+    "xknn_layer_rebuild_graph": [VP, C.c_uint32, C.c_uint32, VP, C.POINTER(U64)],
+    "xknn_graph_save_rows": [C.c_char_p, U64, C.c_uint32, U64, U64, VP, C.c_int, C.c_int],
+    "xknn_graph_load_rows": [C.c_char_p, U64, U64, U64, VP, U64, C.c_int,
+                             C.POINTER(C.c_uint32)],
     "xknn_layer_get_graph": [VP, VP, VP, VP, U64, C.POINTER(U64), C.c_int],
 }.items():
     getattr(_lib, _name).argtypes = _args
@@ -185,6 +190,33 @@ def graph_ring(w_norm_local, num_classes: int, k: int, kprime: int, rank: int, w
                                 torch.cuda.current_stream().cuda_stream, out.data_ptr(),
                                 C.byref(unc), C.byref(steps)))
     return out, unc.value, steps.value
+
+
+def save_graph_rows(path: str, num_classes: int, begin: int, rows, create: bool) -> None:
+    """save_graph (knn_graph.cpp:276-291) of classes [begin, begin + len(rows)): rows is a
+    (n, k) uint32/int32 numpy array or CUDA tensor.  create: write the header (first writer)."""
+    if hasattr(rows, "is_cuda") and rows.is_cuda:
+        r = rows.contiguous()
+        n, k = r.shape
+        ptr, dev = r.data_ptr(), 1
+    else:
+        r = np.ascontiguousarray(rows).view(np.uint32)
+        n, k = r.shape
+        ptr, dev = r.ctypes.data, 0
+    _check(_lib.xknn_graph_save_rows(path.encode(), num_classes, k, begin, begin + n, ptr, dev,
+                                     int(create)))
+
+
+def load_graph_rows(path: str, num_classes: int, begin: int = 0, end: int | None = None):
+    """load_graph (knn_graph.cpp:293-311) of classes [begin, end): returns (k, rows u32 numpy)."""
+    end = num_classes if end is None else end
+    k = C.c_uint32()
+    _check(_lib.xknn_graph_load_rows(path.encode(), num_classes, begin, end, None, 0, 0,
+                                     C.byref(k)))
+    rows = np.zeros((end - begin, k.value), np.uint32)
+    _check(_lib.xknn_graph_load_rows(path.encode(), num_classes, begin, end, rows.ctypes.data,
+                                     rows.size, 0, C.byref(k)))
+    return k.value, rows
 
 
 def _ptr(t) -> int:
@@ -283,13 +315,25 @@ class KnnSoftmaxLayer:
         self._enter()
         _check(_lib.xknn_layer_set_graph_rows(self.h, r.data_ptr(), k))
 
-    def rebuild_graph(self, k: int, kprime: int = 0) -> int:
+    def rebuild_graph(self, k: int, kprime: int = 0, rows_out=None) -> int:
         """Exact KNN graph of the current (normalized) weights, sharded build + compression,
-        installed as this shard's CompressedKnnGraph.  Collective.  Returns uncertified rows."""
+        installed as this shard's CompressedKnnGraph.  rows_out: optional (shard_rows, k) int32
+        CUDA tensor receiving this rank's rows of the full graph.  Collective.  Returns the
+        number of uncertified (exactly rescanned) rows."""
         unc = U64()
         self._enter()
-        _check(_lib.xknn_layer_rebuild_graph(self.h, k, kprime, C.byref(unc)))
+        _check(_lib.xknn_layer_rebuild_graph(self.h, k, kprime, _ptr(rows_out), C.byref(unc)))
+        self._leave()
         return unc.value
+
+    def load_graph(self, path: str) -> int:
+        """load_graph + compress_graph + set_shard_graphs from an XKNN file: this rank reads its
+        rows [begin, end) and the shards exchange entries.  Collective.  Returns k."""
+        k, rows = load_graph_rows(path, self.num_classes, self.begin, self.end)
+        import torch
+
+        self.set_graph_rows(torch.from_numpy(rows.view(np.int32)).cuda(), k)
+        return k
 
     def graph(self):
         """The installed CompressedKnnGraph: (k_per_class u32[N], offsets u64[N], flat u32[])

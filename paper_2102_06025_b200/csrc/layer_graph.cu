@@ -224,7 +224,7 @@ xknn_status_t xknn_layer_set_graph_rows(xknn_layer_t* h, const uint32_t* rows_de
 }
 
 xknn_status_t xknn_layer_rebuild_graph(xknn_layer_t* h, uint32_t k, uint32_t kprime,
-                                       uint64_t* uncertified_rows) {
+                                       uint32_t* rows_out_dev, uint64_t* uncertified_rows) {
   if (!h) return xknn::fail_msg(XKNN_ERR_INVALID_ARGUMENT, "null layer handle");
   Layer& L = h->L;
   if (!L.has_weights) return xknn::fail_msg(XKNN_ERR_INVALID_ARGUMENT, "rebuild_graph: weights not set");
@@ -263,6 +263,8 @@ xknn_status_t xknn_layer_rebuild_graph(xknn_layer_t* h, uint32_t k, uint32_t kpr
   st = xknn::graph_build(wn, L.n, L.d, k, kprime, L.rank, L.world, L.comm, L.stream, rows, &gs);
   if (st != XKNN_OK) return st;
   if (uncertified_rows) *uncertified_rows = gs.uncertified_rows;
+  if (rows_out_dev)
+    LG_CUDA(cudaMemcpyAsync(rows_out_dev, rows, L.nw * k * 4, cudaMemcpyDeviceToDevice, L.stream));
   return xknn_layer_set_graph_rows(h, rows, k);
 }
 

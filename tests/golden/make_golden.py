@@ -75,6 +75,9 @@ def main():
     rc, gr = O.bruteforce_graph("ref", wn, 7)
     assert rc == 0
     np.savez_compressed(os.path.join(HERE, "graph_bf.npz"), w=w, k=7, graph=gr)
+    # an XKNN graph file written by the reference's save_graph (knn_graph.cpp:276-291)
+    g = O.random_graph(50, 5, 31)
+    assert O.ref_save_graph(os.path.join(HERE, "graph_small.xknn"), g) == 0
 
 
 if __name__ == "__main__":

@@ -286,3 +286,26 @@ def ref_feature_grad(w, x, labels, active, p, scale=30.0):
             np.ascontiguousarray(labels, np.uint32), b, np.ascontiguousarray(active, np.uint32),
             active.size, scale, C.byref(loss), g)
     return rc, loss.value, g
+
+
+def ref_save_graph(path: str, g: np.ndarray) -> int:
+    """The reference's save_graph (through oracle/_ref)."""
+    g = np.ascontiguousarray(g, np.uint32)
+    fn = ref().ref_save_graph
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, U64, U64, u32p]
+    return fn(path.encode(), g.shape[0], g.shape[1], g)
+
+
+def ref_load_graph(path: str):
+    """The reference's load_graph: (rc, graph ndarray or None)."""
+    fn = ref().ref_load_graph
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, C.POINTER(U64), C.POINTER(U64), C.c_void_p]
+    n, k = U64(), U64()
+    rc = fn(path.encode(), C.byref(n), C.byref(k), None)
+    if rc:
+        return rc, None
+    out = np.zeros((n.value, k.value), np.uint32)
+    rc = fn(path.encode(), C.byref(n), C.byref(k), out.ctypes.data)
+    return rc, out

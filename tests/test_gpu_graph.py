@@ -123,3 +123,27 @@ def test_layer_rebuild_zero_norm_row():
         layer.rebuild_graph(5)
     assert ei.value.row == 123
     layer.close()
+
+
+def test_rebuild_save_load_roundtrip(tmp_path):
+    """rebuild -> rows -> XKNN file -> load_graph on a fresh layer: the same CompressedKnnGraph,
+    and the file equals the reference's save_graph of the oracle graph."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    n, k = 2000, 9
+    w = _dup_weights(3, 100, n - 300)
+    layer = X.KnnSoftmaxLayer(n, 512, m_active=200, max_batch=32, rng_seed=42)
+    layer.set_weights(torch.from_numpy(w).cuda())
+    rows = torch.empty(n, k, dtype=torch.int32, device="cuda")
+    layer.rebuild_graph(k, rows_out=rows)
+    path = str(tmp_path / "g.xknn")
+    X.save_graph_rows(path, n, 0, rows, create=True)
+    rc, g = O.bruteforce_graph("oracle", _normalized(w), k)
+    assert rc == 0 and np.array_equal(rows.cpu().numpy().view(np.uint32), g)
+    fresh = X.KnnSoftmaxLayer(n, 512, m_active=200, max_batch=32, rng_seed=42)
+    assert fresh.load_graph(path) == k
+    for a, b in zip(fresh.graph(), layer.graph()):
+        assert np.array_equal(a, b)
+    layer.close()
+    fresh.close()
