@@ -230,6 +230,17 @@ xknn_status_t xknn_layer_get_graph(xknn_layer_t* h, uint32_t* k_per_class, uint6
                                    uint32_t* flat, uint64_t flat_capacity, uint64_t* flat_len,
                                    int on_device);
 
+/* classify_retrieval (the paper's retrieval evaluation): the nearest class of
+   each query among the L2-normalized class weights of all shards = the argmax of the fp32 cosine
+   logits (matmul(q_hat, w_hat, T) order), ties to the lower class id.  Every rank scores its
+   shard (fp16 tensor-core candidates, exact re-score of the certified window, exact scans
+   otherwise) and the ranks' winners are merged over NCCL.  queries_dev: n_queries x dim fp32
+   (normalized here, bit-exact with l2_normalize_rows; ZeroNormRow); out_class_dev: n_queries
+   u32, out_score_dev (may be NULL): the winning cosine; identical on every rank.  Collective.
+   Synchronizes. */
+xknn_status_t xknn_layer_classify(xknn_layer_t* h, const float* queries_dev, uint64_t n_queries,
+                                  uint32_t* out_class_dev, float* out_score_dev);
+
 /* Kernel launch counter (all kernels this library launched on this layer since creation). */
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);
 

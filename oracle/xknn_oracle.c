@@ -563,6 +563,44 @@ int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k,
   return OR_OK;
 }
 
+/* classify_retrieval (the reference tree has no implementation, this
+   restates the spec): the nearest class of each query among the L2-normalized class weights,
+   i.e. the argmax of the cosine logits matmul(q_hat, w_hat, T) (matrix.cpp:57-68 order; the
+   logit scale does not move the argmax), ties to the lower class index.  q and w are
+   normalized with l2_normalize_rows (matrix.cpp:12-29).  out_score: the winning cosine. */
+int or_classify_retrieval(uint64_t nq, uint64_t n, uint64_t d, const float* q, const float* w,
+                          uint32_t* out_class, float* out_score) {
+  if (nq == 0 || n == 0 || d == 0) return OR_ERR_SHAPE_MISMATCH;
+  float* qn = (float*)malloc(nq * d * sizeof(float));
+  float* wn = (float*)malloc(n * d * sizeof(float));
+  float* nq_norm = (float*)malloc(nq * sizeof(float));
+  float* nw_norm = (float*)malloc(n * sizeof(float));
+  uint64_t bad = 0;
+  int rc = or_l2_normalize_rows(nq, d, q, 1e-12f, qn, nq_norm, &bad);
+  if (rc == OR_OK) rc = or_l2_normalize_rows(n, d, w, 1e-12f, wn, nw_norm, &bad);
+  for (uint64_t i = 0; rc == OR_OK && i < nq; ++i) {
+    const float* qi = qn + i * d;
+    float best = 0.0f;
+    uint32_t arg = 0;
+    for (uint64_t j = 0; j < n; ++j) {
+      const float* wj = wn + j * d;
+      float acc = 0.0f;
+      for (uint64_t t = 0; t < d; ++t) acc += qi[t] * wj[t];
+      if (j == 0 || acc > best) {
+        best = acc;
+        arg = (uint32_t)j;
+      }
+    }
+    out_class[i] = arg;
+    if (out_score) out_score[i] = best;
+  }
+  free(qn);
+  free(wn);
+  free(nq_norm);
+  free(nw_norm);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* The fc half of HybridSim::train_step in kKnn mode with one micro-batch    */
 /* (parallel.cpp:455-572, :638-668), the composite the device layer replaces. */

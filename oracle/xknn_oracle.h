@@ -47,6 +47,8 @@ int or_distributed_softmax_xent_cols(uint64_t p, uint64_t m, const float* const*
 void or_sgd_step_rows(uint64_t cols, float* params, const float* grad_rows, float* velocity,
                       const uint32_t* rows, uint64_t nrows, float lr, float momentum, float wd);
 int or_build_graph_bruteforce(uint64_t n, uint64_t d, const float* w, uint64_t k, uint32_t* out);
+int or_classify_retrieval(uint64_t nq, uint64_t n, uint64_t d, const float* q, const float* w,
+                          uint32_t* out_class, float* out_score);
 int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k, uint32_t* out);
 int or_fc_train_step(uint64_t n, uint64_t d, uint64_t p, float* w, float* velocity,
                      const float* x, const uint32_t* labels, uint64_t b,

@@ -114,6 +114,7 @@ for _name, _args in {
     "xknn_graph_load_rows": [C.c_char_p, U64, U64, U64, VP, U64, C.c_int,
                              C.POINTER(C.c_uint32)],
     "xknn_layer_get_graph": [VP, VP, VP, VP, U64, C.POINTER(U64), C.c_int],
+    "xknn_layer_classify": [VP, VP, U64, VP, VP],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
@@ -348,6 +349,19 @@ class KnnSoftmaxLayer:
         _check(_lib.xknn_layer_get_graph(self.h, kpc.ctypes.data, off.ctypes.data,
                                          flat.ctypes.data, flat.size, C.byref(n), 0))
         return kpc, off, flat[: n.value]
+
+    def classify(self, queries):
+        """classify_retrieval: nearest normalized class embedding of each query
+        (n, dim) fp32 CUDA tensor.  Collective.  Returns (classes int32 tensor, cosines)."""
+        torch = self._torch
+        q = queries.contiguous()
+        cls = torch.empty(q.shape[0], dtype=torch.int32, device="cuda")
+        sc = torch.empty(q.shape[0], dtype=torch.float32, device="cuda")
+        self._enter()
+        _check(_lib.xknn_layer_classify(self.h, q.data_ptr(), q.shape[0], cls.data_ptr(),
+                                        sc.data_ptr()))
+        self._leave()
+        return cls, sc
 
     # -- hot path ------------------------------------------------------------------------------
     def select_active_classes(self, labels):

@@ -254,6 +254,50 @@ __global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t k
   }
 }
 
+// classify: one warp per query, the best exactly scored candidate (higher score, then lower
+// class id) of its window, or its exact scan's winner when uncertified
+__global__ void k_top1(uint32_t n, uint32_t kp, const float2* __restrict__ list,
+                       const uint32_t* __restrict__ lcnt, const float* __restrict__ ex,
+                       const uint32_t* __restrict__ flag, const float2* __restrict__ ubuf,
+                       float* __restrict__ best_score, uint32_t* __restrict__ best_id) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
+       j += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t f = flag[j];
+    float bs = -INFINITY;
+    uint32_t bi = 0xffffffffu;
+    if (f) {
+      if (lane == 0) {
+        const float2 v = ubuf[f - 1];
+        bs = v.x;
+        bi = __float_as_uint(v.y);
+      }
+    } else {
+      for (uint32_t e = lane; e < lcnt[j]; e += 32) {
+        const float sc = ex[(uint64_t)j * kp + e];
+        const uint32_t id = __float_as_uint(list[(uint64_t)j * kp + e].y);
+        if (before(sc, id, bs, bi)) {
+          bs = sc;
+          bi = id;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(XKNN_FULL_MASK, bs, o);
+      const uint32_t oi = __shfl_xor_sync(XKNN_FULL_MASK, bi, o);
+      if (before(os, oi, bs, bi)) {
+        bs = os;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      best_score[j] = bs;
+      best_id[j] = bi;
+    }
+  }
+}
+
 __global__ void k_self_only(uint32_t n, uint32_t row_base, uint32_t* out) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     out[j] = row_base + j;
@@ -585,6 +629,105 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   }
 #undef G_CUDA
 #undef G_NCCL
+  return XKNN_OK;
+}
+
+// classify_retrieval on one shard: for each normalized query (qn, nq x 512)
+// the exactly best class among the normalized rows wn (nw x 512, global ids col_base..) --
+// argmax of the reference-order fp32 cosine, ties to the lower id -- by the graph build's
+// scheme with one neighbour and no self: fp16 tensor-core candidates (up to 32 per query above
+// a cut), the certificate A_1 > T + 2 eps, exact re-scores of the window, exact scans for the
+// uncertified.  best_score / best_id: nq each, device.
+xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn, uint32_t nw,
+                                   uint32_t col_base, uint32_t d, cudaStream_t s,
+                                   float* best_score, uint32_t* best_id, uint64_t* uncertified) {
+  cudaError_t e = cudaSuccess;
+#define G_CUDA(x)                                                         \
+  do {                                                                    \
+    e = (x);                                                              \
+    if (e != cudaSuccess) return fail_msg(XKNN_ERR_CUDA, cudaGetErrorString(e)); \
+  } while (0)
+  if ((uint64_t)col_base + nw + nq >= 0xffffffffull)
+    return fail_msg(XKNN_ERR_UNSUPPORTED, "classify: class ids + queries must fit u32");
+  const uint32_t kp = 32, ch = 64;
+  Dev mem;
+  float2* list = nullptr;
+  uint32_t *lcnt = nullptr, *flag = nullptr, *unc = nullptr;
+  float *lcut = nullptr, *ex = nullptr;
+  G_CUDA(mem.get(&list, (uint64_t)nq * kp));
+  G_CUDA(mem.get(&lcnt, nq));
+  G_CUDA(mem.get(&lcut, nq));
+  G_CUDA(mem.get(&flag, nq));
+  G_CUDA(mem.get(&unc, (uint64_t)nq + 1));
+  G_CUDA(mem.get(&ex, (uint64_t)nq * kp));
+  G_CUDA(cudaMemsetAsync(unc, 0, 4, s));
+  uint32_t nu = 0;
+  if (d == 512) {
+    const uint64_t qpad = (nq + 255) / 256 * 256, wpad = ((uint64_t)nw + 255) / 256 * 256;
+    __half *q16 = nullptr, *w16 = nullptr;
+    float2* cand = nullptr;
+    uint32_t* ccnt = nullptr;
+    float* ctau = nullptr;
+    G_CUDA(mem.get(&q16, qpad * 512));
+    G_CUDA(mem.get(&w16, wpad * 512));
+    G_CUDA(mem.get(&cand, (uint64_t)kNumSMs / 2 * 256 * 2 * ch));
+    G_CUDA(mem.get(&ccnt, (uint64_t)kNumSMs / 2 * 256 * 2));
+    G_CUDA(mem.get(&ctau, (uint64_t)kNumSMs / 2 * 256 * 2));
+    k_to_f16<<<grid_for(qpad * 256, 256), 256, 0, s>>>(qn, nq, qpad, 512, q16);
+    k_to_f16<<<grid_for(wpad * 256, 256), 256, 0, s>>>(wn, nw, wpad, 512, w16);
+    k_list_init<<<grid_for(nq, 256), 256, 0, s>>>(lcnt, lcut, nq);
+    G_CUDA(cudaGetLastError());
+    // queries are not classes: their "self" ids lie above every class id
+    G_CUDA(launch_graph_candidates(q16, nq, 0xffffffffu - nq, w16, nw, col_base, list, lcnt, lcut,
+                                   kp, cand, ccnt, ctau, ch, s));
+    k_window<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(list, lcnt, lcut, nq, kp, 1, flag,
+                                                              unc, unc + 1);
+    G_CUDA(cudaGetLastError());
+    G_CUDA(cudaMemcpyAsync(&nu, unc, 4, cudaMemcpyDeviceToHost, s));
+    G_CUDA(cudaStreamSynchronize(s));
+    k_rescore<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(qn, nq, 512, list, lcnt, flag, kp,
+                                                               wn, col_base, nw, ex);
+    G_CUDA(cudaGetLastError());
+  } else {  // exact scans for every query
+    nu = nq;
+    std::vector<uint32_t> ids(nq);
+    for (uint32_t j = 0; j < nq; ++j) ids[j] = j;
+    std::vector<uint32_t> fl(nq);
+    for (uint32_t j = 0; j < nq; ++j) fl[j] = j + 1;
+    G_CUDA(cudaMemcpyAsync(unc + 1, ids.data(), (size_t)nq * 4, cudaMemcpyHostToDevice, s));
+    G_CUDA(cudaMemcpyAsync(flag, fl.data(), (size_t)nq * 4, cudaMemcpyHostToDevice, s));
+    G_CUDA(cudaStreamSynchronize(s));
+  }
+  float2* ubuf = nullptr;
+  if (nu) {
+    std::vector<uint32_t> urows(nu);
+    G_CUDA(cudaMemcpy(urows.data(), unc + 1, (size_t)nu * 4, cudaMemcpyDeviceToHost));
+    uint32_t* keys = nullptr;
+    void* stmp = nullptr;
+    size_t stb = 0;
+    G_CUDA(mem.get(&ubuf, nu));
+    G_CUDA(mem.get(&keys, (uint64_t)nw * 4));
+    uint32_t *kidx = keys + nw, *keys2 = keys + 2 * (uint64_t)nw, *kidx2 = keys + 3 * (uint64_t)nw;
+    G_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, stb, keys, keys2, kidx, kidx2,
+                                                     (int)nw, 0, 32, s));
+    G_CUDA(mem.get(reinterpret_cast<uint8_t**>(&stmp), stb));
+    for (uint32_t u = 0; u < nu; ++u) {
+      const uint32_t j = urows[u];
+      k_exact_scan<<<grid_for(nw, 256), 256, 0, s>>>(qn + (uint64_t)j * d, wn, nw, d, col_base,
+                                                     0xffffffffu, keys, kidx);
+      size_t t2 = stb;
+      G_CUDA(cub::DeviceRadixSort::SortPairsDescending(stmp, t2, keys, keys2, kidx, kidx2, (int)nw,
+                                                       0, 32, s));
+      k_take<<<1, 32, 0, s>>>(keys2, kidx2, nw, 1, col_base, ubuf + u);
+      G_CUDA(cudaGetLastError());
+    }
+  }
+  k_top1<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(nq, kp, list, lcnt, ex, flag, ubuf,
+                                                          best_score, best_id);
+  G_CUDA(cudaGetLastError());
+  G_CUDA(cudaStreamSynchronize(s));
+  if (uncertified) *uncertified = nu;
+#undef G_CUDA
   return XKNN_OK;
 }
 

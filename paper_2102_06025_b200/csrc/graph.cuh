@@ -19,4 +19,9 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d, uint32_
                           uint32_t kprime, int rank, int world, ncclComm_t comm, cudaStream_t s,
                           uint32_t* out, GraphBuildStats* stats);
 
+// classify_retrieval on one shard (graph.cu): best class (score, global id) of each query.
+xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn, uint32_t nw,
+                                   uint32_t col_base, uint32_t d, cudaStream_t s,
+                                   float* best_score, uint32_t* best_id, uint64_t* uncertified);
+
 }  // namespace xknn

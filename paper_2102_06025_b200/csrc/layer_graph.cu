@@ -91,6 +91,32 @@ __global__ void k_comp_scatter(const uint32_t* __restrict__ rows, uint32_t n, ui
   }
 }
 
+// classify: the global winner of each query from every rank's (score, id) -- higher score,
+// then lower class id (shards own ascending class ranges)
+__global__ void k_merge_top1(const float2* __restrict__ all, uint32_t nq, uint32_t world,
+                             uint32_t* __restrict__ out_class, float* __restrict__ out_score) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
+    float bs = -INFINITY;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t r = 0; r < world; ++r) {
+      const float2 v = all[(uint64_t)r * nq + j];
+      const uint32_t id = __float_as_uint(v.y);
+      if (v.x > bs || (v.x == bs && id < bi)) {
+        bs = v.x;
+        bi = id;
+      }
+    }
+    out_class[j] = bi;
+    if (out_score) out_score[j] = bs;
+  }
+}
+
+__global__ void k_pack_top1(const float* __restrict__ sc, const uint32_t* __restrict__ id,
+                            uint32_t nq, float2* __restrict__ out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x)
+    out[j] = make_float2(sc[j], __uint_as_float(id[j]));
+}
+
 }  // namespace
 }  // namespace xknn
 
@@ -266,6 +292,58 @@ xknn_status_t xknn_layer_rebuild_graph(xknn_layer_t* h, uint32_t k, uint32_t kpr
   if (rows_out_dev)
     LG_CUDA(cudaMemcpyAsync(rows_out_dev, rows, L.nw * k * 4, cudaMemcpyDeviceToDevice, L.stream));
   return xknn_layer_set_graph_rows(h, rows, k);
+}
+
+xknn_status_t xknn_layer_classify(xknn_layer_t* h, const float* queries_dev, uint64_t n_queries,
+                                  uint32_t* out_class_dev, float* out_score_dev) {
+  if (!h) return xknn::fail_msg(XKNN_ERR_INVALID_ARGUMENT, "null layer handle");
+  Layer& L = h->L;
+  if (!L.has_weights) return xknn::fail_msg(XKNN_ERR_INVALID_ARGUMENT, "classify: weights not set");
+  if (n_queries == 0 || n_queries >= (1ull << 31))
+    return xknn::fail_msg(XKNN_ERR_SHAPE_MISMATCH, "classify: bad query count");
+  const uint32_t nq = (uint32_t)n_queries, d = (uint32_t)L.d;
+  Scratch mem;
+  float *qn = nullptr, *wn = nullptr, *bs = nullptr;
+  uint32_t* bi = nullptr;
+  float2 *mine = nullptr, *all = nullptr;
+  LG_CUDA(mem.get(&qn, (uint64_t)nq * d));
+  LG_CUDA(mem.get(&wn, L.nw * d));
+  LG_CUDA(mem.get(&bs, nq));
+  LG_CUDA(mem.get(&bi, nq));
+  const unsigned threads = 256;
+  const size_t smem = (threads / 32) * L.d * sizeof(float);
+  if (smem > 48 * 1024)
+    LG_CUDA(cudaFuncSetAttribute(xknn::k_normalize_rows_seq,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // l2_normalize_rows of the queries and of this shard's class weights, bit-exact
+  xknn::k_normalize_rows_seq<<<xknn::grid_for((uint64_t)nq * 32, threads), threads, smem,
+                               L.stream>>>(queries_dev, nq, d, qn, L.err);
+  LG_CUDA(cudaGetLastError());
+  xknn_status_t st = check_device_error(L);
+  if (st != XKNN_OK) return st;
+  xknn::k_normalize_rows_seq<<<xknn::grid_for(L.nw * 32, threads), threads, smem, L.stream>>>(
+      L.W, L.nw, d, wn, L.err);
+  LG_CUDA(cudaGetLastError());
+  L.launches += 2;
+  st = check_device_error(L);
+  if (st != XKNN_OK) return st;
+  uint64_t unc = 0;
+  st = xknn::retrieval_top1_local(qn, nq, wn, (uint32_t)L.nw, (uint32_t)L.begin, d, L.stream, bs,
+                                  bi, &unc);
+  if (st != XKNN_OK) return st;
+  LG_CUDA(mem.get(&mine, nq));
+  LG_CUDA(mem.get(&all, (uint64_t)nq * L.world));
+  xknn::k_pack_top1<<<xknn::grid_for(nq, 256), 256, 0, L.stream>>>(bs, bi, nq, mine);
+  if (L.world > 1)
+    LG_NCCL(ncclAllGather(mine, all, 2ull * nq, ncclFloat, L.comm, L.stream));
+  else
+    LG_CUDA(cudaMemcpyAsync(all, mine, 8ull * nq, cudaMemcpyDeviceToDevice, L.stream));
+  xknn::k_merge_top1<<<xknn::grid_for(nq, 256), 256, 0, L.stream>>>(all, nq, (uint32_t)L.world,
+                                                                    out_class_dev, out_score_dev);
+  LG_CUDA(cudaGetLastError());
+  L.launches += 2;
+  LG_CUDA(cudaStreamSynchronize(L.stream));
+  return XKNN_OK;
 }
 
 xknn_status_t xknn_layer_get_graph(xknn_layer_t* h, uint32_t* k_per_class, uint64_t* offsets,

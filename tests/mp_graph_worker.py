@@ -53,8 +53,12 @@ def main():
     layer.set_weights(torch.from_numpy(np.ascontiguousarray(w[b:e])).cuda())
     unc2 = layer.rebuild_graph(k)
     kpc, off, flat = layer.graph()
+    q = np.random.default_rng(77).standard_normal((200, 512)).astype(np.float32)
+    q[:3] = w[[5, n // 2, n - 1]]
+    cls, sc = layer.classify(torch.from_numpy(q).cuda())
     np.savez(os.path.join(args.out, f"graph{rank}.npz"), rows=rows.cpu().numpy().view(np.uint32),
-             unc=unc, unc2=unc2, steps=steps, kpc=kpc, off=off, flat=flat)
+             unc=unc, unc2=unc2, steps=steps, kpc=kpc, off=off, flat=flat,
+             cls=cls.cpu().numpy().view(np.uint32), sc=sc.cpu().numpy())
     layer.close()
     X.nccl_comm_destroy(comm)
     dist.barrier()

@@ -309,3 +309,16 @@ def ref_load_graph(path: str):
     out = np.zeros((n.value, k.value), np.uint32)
     rc = fn(path.encode(), C.byref(n), C.byref(k), out.ctypes.data)
     return rc, out
+
+
+def classify_retrieval(q: np.ndarray, w: np.ndarray):
+    """classify_retrieval restated in oracle/: (rc, classes u32, cosines)."""
+    q = np.ascontiguousarray(q, np.float32)
+    w = np.ascontiguousarray(w, np.float32)
+    out = np.zeros(q.shape[0], np.uint32)
+    sc = np.zeros(q.shape[0], np.float32)
+    fn = oracle().or_classify_retrieval
+    fn.restype = C.c_int
+    fn.argtypes = [U64, U64, U64, f32p, f32p, u32p, f32p]
+    rc = fn(q.shape[0], w.shape[0], q.shape[1], q, w, out, sc)
+    return rc, out, sc

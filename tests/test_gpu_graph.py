@@ -147,3 +147,27 @@ def test_rebuild_save_load_roundtrip(tmp_path):
         assert np.array_equal(a, b)
     layer.close()
     fresh.close()
+
+
+@pytest.mark.parametrize("d", [512, 128])
+def test_classify_retrieval(d):
+    """classify_retrieval == argmax of the reference-order cosine (oracle restatement of
+    SPEC.md:568-576), ties to the lower id; a query equal to w_j returns j."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    n = 5000 if d == 512 else 700
+    rng = np.random.default_rng(d)
+    w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    w[n - 1] = w[17]  # exact duplicate class: ties resolve to the lower id
+    q = np.concatenate([rng.standard_normal((300, d)).astype(np.float32), w[[3, 17, n - 1, 4000 % n]] * 3.0])
+    layer = X.KnnSoftmaxLayer(n, d, m_active=n // 10, max_batch=16, rng_seed=42,
+                              precision=X.PREC_BF16 if d == 512 else X.PREC_FP32_EXACT)
+    layer.set_weights(torch.from_numpy(w).cuda())
+    cls, sc = layer.classify(torch.from_numpy(q).cuda())
+    rc, want, wsc = O.classify_retrieval(q, w)
+    assert rc == 0
+    assert np.array_equal(cls.cpu().numpy().view(np.uint32), want)
+    assert np.array_equal(sc.cpu().numpy(), wsc)
+    assert list(want[-4:]) == [3, 17, 17, 4000 % n]
+    layer.close()

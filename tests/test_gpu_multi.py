@@ -89,3 +89,11 @@ def test_multi_gpu_graph_ring_and_rebuild(p, tmp_path):
         kpc, off, flat = O.compress(g, p, s)
         assert np.array_equal(x["kpc"], kpc) and np.array_equal(x["off"], off)
         assert np.array_equal(x["flat"], flat)
+    # classify_retrieval over the shards: the oracle's argmax, identical on every rank
+    w = problem(n, 5)
+    q = np.random.default_rng(77).standard_normal((200, 512)).astype(np.float32)
+    q[:3] = w[[5, n // 2, n - 1]]
+    rc, want, wsc = O.classify_retrieval(q, w)
+    assert rc == 0
+    for x in res:
+        assert np.array_equal(x["cls"], want) and np.array_equal(x["sc"], wsc)
