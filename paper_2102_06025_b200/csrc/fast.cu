@@ -919,13 +919,18 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   XK_LAUNCH();
   mark(7);
   k_dx_reduce<<<grid_for(B * 128, 256), 256, 0, stream>>>(f->partial_dx, rowred, (uint32_t)B,
-                                                           nbp, dx_splits, 256, cfg.scale, dXpart);
+                                                           nbp, dx_splits, 256, cfg.scale,
+                                                           world > 1 ? dXpart : dX);
   XK_LAUNCH();
   const uint64_t bl = B / world;
-  if (world > 1)
-    XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
-  else
-    XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  if (world > 1) {
+    // the feature-gradient reduce-scatter over NVLink runs on the side stream, under the
+    // HBM-bound row update (the only collective in flight on the communicator)
+    XK_CUDA(cudaEventRecord(ev_fork, stream));
+    XK_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, side));
+    XK_CUDA(cudaEventRecord(ev_join, side));
+  }
   // (g) normalize-backward + momentum SGD on the active rows (parallel.cpp:649-667)
   //     (a separate HBM-streaming kernel: it runs at the copy roofline, while inside the
   //     GEMM-dW kernel the few spare warps per SM could not keep enough bytes in flight)
@@ -933,6 +938,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
                                   wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream));
   ++launches;
+  if (world > 1) XK_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
   return XKNN_OK;
 }
 

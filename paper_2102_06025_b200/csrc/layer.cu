@@ -97,6 +97,8 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   XK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   XK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_feat, cudaEventDisableTiming));
 
   // cub temp: max over the sorts/scans/selects we run
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
@@ -140,6 +142,9 @@ void Layer::free_all() {
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_in) cudaEventDestroy(ev_in);
+  if (ev_feat) cudaEventDestroy(ev_feat);
+  if (comm_ag) ncclCommDestroy(comm_ag);
   free_fast();
 }
 
@@ -220,6 +225,7 @@ xknn_status_t Layer::run_core(uint64_t B) {
   unsigned int* cnt = &st->active_count;
   // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
   // whole shard as parallel.cpp:490-492 does -- row-wise identical)
+  if (world > 1) XK_TRY(wait_features());
   if (cfg.precision == XKNN_PREC_FP32_EXACT) {
     XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, Xhat, nullptr, xnorm, err, stream));
     ++launches;
@@ -273,6 +279,18 @@ xknn_status_t Layer::run_core(uint64_t B) {
   return XKNN_OK;
 }
 
+// the core waits for the feature all-gather of run_step (an external event-wait node when the
+// core is being captured into the step's CUDA graph)
+xknn_status_t Layer::wait_features() {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  XK_CUDA(cudaStreamIsCapturing(stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    XK_CUDA(cudaStreamWaitEvent(stream, ev_feat, cudaEventWaitExternal));
+  else
+    XK_CUDA(cudaStreamWaitEvent(stream, ev_feat, 0));
+  return XKNN_OK;
+}
+
 xknn_status_t Layer::ensure_graph(uint64_t B) {
   if (graph_exec && graph_b == B && graph_prof == prof_on) return XKNN_OK;
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -306,12 +324,17 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   graph_mode = !(cfg.flags & XKNN_FLAG_NO_GRAPH) && stream != nullptr;
   if (prof_on) prof_collect(false);
   mark(0);
-  // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544)
+  // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544).  The labels go
+  //     first on the layer stream (selection needs them); the features travel on the side
+  //     stream over a split communicator while the selection runs, and the core waits for them
+  //     right before the first kernel that reads X.
   if (world > 1) {
-    XK_NCCL(ncclGroupStart());
-    XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm, stream));
+    if (!comm_ag) XK_NCCL(ncclCommSplit(comm, 0, rank, &comm_ag, nullptr));  // collective
     XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
-    XK_NCCL(ncclGroupEnd());
+    XK_CUDA(cudaEventRecord(ev_in, stream));
+    XK_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
+    XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm_ag, side));
+    XK_CUDA(cudaEventRecord(ev_feat, side));
   } else {
     XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t), cudaMemcpyDeviceToDevice,

@@ -58,6 +58,9 @@ struct Layer {
   uint64_t n = 0, d = 0, begin = 0, end = 0, nw = 0;
   xknn_config_t cfg{};
   ncclComm_t comm = nullptr;
+  ncclComm_t comm_ag = nullptr;       // split of comm: the feature all-gather, which overlaps
+                                      // the selection's own collectives on comm
+  cudaEvent_t ev_in = nullptr, ev_feat = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // overlaps the row update with the feature-gradient GEMM
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -141,6 +144,7 @@ struct Layer {
   xknn_status_t run_selection(uint64_t batch);    // labels_all already on device
   xknn_status_t run_core(uint64_t batch);
   xknn_status_t ensure_graph(uint64_t batch);
+  xknn_status_t wait_features();
   xknn_status_t run_step(const float* feats_local, const uint32_t* labels_local,
                          uint64_t batch_local, float lr, double* loss_out, float* gfeat_local);
   xknn_status_t nccl_ok(ncclResult_t r);
