@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "xknn.h"
 
 #define XKNN_FULL_MASK 0xffffffffu
@@ -21,6 +23,13 @@ struct DevError {
 __device__ __forceinline__ void raise_error(unsigned long long* err, int code, uint64_t row = 0) {
   unsigned long long w = (unsigned long long)code | ((unsigned long long)row << 8);
   atomicCAS(err, 0ull, w);
+}
+
+// Programmatic dependent launch (PDL): the step's kernels are launched with programmatic
+// stream serialization so each one is resident before its predecessor drains; every kernel
+// first waits for its predecessors' results (a no-op when launched without the attribute).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <typename T>
@@ -43,6 +52,22 @@ template <typename T>
 inline cudaError_t dalloc(T** p, uint64_t count) {
   if (count == 0) count = 1;
   return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 16u) {

@@ -22,6 +22,7 @@ constexpr int kKc = 32;  // inner chunk
 __global__ void k_gemm_nt_exact(const float* __restrict__ A, const float* __restrict__ Bm,
                                 uint64_t rows, const unsigned int* cols_dev, uint32_t d,
                                 float scale, float* __restrict__ C) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   __shared__ float As[kT][kKc + 1];
   __shared__ float Bs[kT][kKc + 1];
@@ -51,6 +52,7 @@ __global__ void k_gemm_nt_exact(const float* __restrict__ A, const float* __rest
 __global__ void k_gemm_tn_exact(const float* __restrict__ G, const float* __restrict__ X,
                                 uint64_t rows, const unsigned int* cols_dev, uint32_t d, float sw,
                                 float* __restrict__ out) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   const uint64_t total = cols * d;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
@@ -67,6 +69,7 @@ __global__ void k_gemm_tn_exact(const float* __restrict__ G, const float* __rest
 __global__ void k_gemm_nn_exact(const float* __restrict__ G, const float* __restrict__ Wsub,
                                 uint64_t rows, const unsigned int* cols_dev, uint32_t d,
                                 float scale, float* __restrict__ out) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   const uint64_t total = rows * d;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
@@ -82,6 +85,7 @@ __global__ void k_gemm_nn_exact(const float* __restrict__ G, const float* __rest
 // ---- distributed softmax statistics (parallel.cpp:123-156): one warp per row
 __global__ void k_rowmax(const float* __restrict__ L, uint64_t rows, const unsigned int* cols_dev,
                          float* __restrict__ rowmax) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
@@ -98,6 +102,7 @@ __global__ void k_rowmax(const float* __restrict__ L, uint64_t rows, const unsig
 __global__ void k_rowsum(const float* __restrict__ L, uint64_t rows, const unsigned int* cols_dev,
                          const float* __restrict__ rowmax, const int32_t* __restrict__ label_col,
                          double* __restrict__ red) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
@@ -119,6 +124,7 @@ __global__ void k_rowsum(const float* __restrict__ L, uint64_t rows, const unsig
 // exactly one per row.
 __global__ void k_loss(const double* __restrict__ red, uint64_t rows, double* loss,
                        SelState* st, unsigned long long* err) {
+  griddep_wait();
   __shared__ double part[256];
   double s = 0.0;
   // fixed-order blocked sum: thread t sums rows [t*c, (t+1)*c) sequentially
@@ -142,6 +148,7 @@ __global__ void k_loss(const double* __restrict__ red, uint64_t rows, double* lo
 __global__ void k_softmax_grad(float* __restrict__ L, uint64_t rows, const unsigned int* cols_dev,
                                const float* __restrict__ rowmax, const double* __restrict__ red,
                                const int32_t* __restrict__ label_col) {
+  griddep_wait();
   const uint64_t cols = *cols_dev;
   const float inv_m = 1.0f / (float)rows;
   const uint64_t total = rows * cols;
@@ -161,7 +168,7 @@ cudaError_t launch_logits_exact(const float* xhat, const float* wsub, uint64_t r
                                 const unsigned int* cols, uint64_t max_cols, uint32_t d,
                                 float scale, float* out, cudaStream_t s) {
   const uint64_t tiles = ((rows + kT - 1) / kT) * ((max_cols + kT - 1) / kT);
-  k_gemm_nt_exact<<<grid_for(tiles, 1, 148u * 64u), dim3(kT, kT), 0, s>>>(xhat, wsub, rows, cols,
+  launch_pdl(k_gemm_nt_exact, grid_for(tiles, 1, 148u * 64u), dim3(kT, kT), 0, s, xhat, wsub, rows, cols,
                                                                            d, scale, out);
   return cudaGetLastError();
 }
@@ -169,7 +176,7 @@ cudaError_t launch_logits_exact(const float* xhat, const float* wsub, uint64_t r
 cudaError_t launch_dw_exact(const float* G, const float* xhat, uint64_t rows,
                             const unsigned int* cols, uint64_t max_cols, uint32_t d, float sw,
                             float* out, cudaStream_t s) {
-  k_gemm_tn_exact<<<grid_for(max_cols * d, 256, 148u * 64u), 256, 0, s>>>(G, xhat, rows, cols, d,
+  launch_pdl(k_gemm_tn_exact, grid_for(max_cols * d, 256, 148u * 64u), 256, 0, s, G, xhat, rows, cols, d,
                                                                           sw, out);
   return cudaGetLastError();
 }
@@ -177,34 +184,34 @@ cudaError_t launch_dw_exact(const float* G, const float* xhat, uint64_t rows,
 cudaError_t launch_dx_exact(const float* G, const float* wsub, uint64_t rows,
                             const unsigned int* cols, uint32_t d, float scale, float* out,
                             cudaStream_t s) {
-  k_gemm_nn_exact<<<grid_for(rows * d, 256, 148u * 64u), 256, 0, s>>>(G, wsub, rows, cols, d,
+  launch_pdl(k_gemm_nn_exact, grid_for(rows * d, 256, 148u * 64u), 256, 0, s, G, wsub, rows, cols, d,
                                                                       scale, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rowmax(const float* L, uint64_t rows, const unsigned int* cols, float* rowmax,
                           cudaStream_t s) {
-  k_rowmax<<<grid_for(rows * 32, 256), 256, 0, s>>>(L, rows, cols, rowmax);
+  launch_pdl(k_rowmax, grid_for(rows * 32, 256), 256, 0, s, L, rows, cols, rowmax);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rowsum(const float* L, uint64_t rows, const unsigned int* cols,
                           const float* rowmax, const int32_t* label_col, double* red,
                           cudaStream_t s) {
-  k_rowsum<<<grid_for(rows * 32, 256), 256, 0, s>>>(L, rows, cols, rowmax, label_col, red);
+  launch_pdl(k_rowsum, grid_for(rows * 32, 256), 256, 0, s, L, rows, cols, rowmax, label_col, red);
   return cudaGetLastError();
 }
 
 cudaError_t launch_loss(const double* red, uint64_t rows, double* loss, SelState* st,
                         unsigned long long* err, cudaStream_t s) {
-  k_loss<<<1, 256, 0, s>>>(red, rows, loss, st, err);
+  launch_pdl(k_loss, 1, 256, 0, s, red, rows, loss, st, err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_softmax_grad(float* L, uint64_t rows, const unsigned int* cols,
                                 uint64_t max_cols, const float* rowmax, const double* red,
                                 const int32_t* label_col, cudaStream_t s) {
-  k_softmax_grad<<<grid_for(rows * max_cols, 256), 256, 0, s>>>(L, rows, cols, rowmax, red,
+  launch_pdl(k_softmax_grad, grid_for(rows * max_cols, 256), 256, 0, s, L, rows, cols, rowmax, red,
                                                                 label_col);
   return cudaGetLastError();
 }

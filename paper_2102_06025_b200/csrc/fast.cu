@@ -324,6 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   tc::cluster_sync();  // peers see initialised barriers before any remote arrive / TMA
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
+  griddep_wait();  // the setup above overlapped the previous kernel's tail (PDL)
 
   const uint32_t mw = KIND == kG ? a.nrows : a.st->active_count;
   const uint32_t nunits = num_units2<KIND>(a, mw);
@@ -664,6 +665,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 __global__ void k_rowreduce(const SelState* st, const float* __restrict__ partial,
                             const float* __restrict__ labelterm, const int32_t* __restrict__ lcol,
                             uint32_t B, uint32_t bpad, double* __restrict__ red) {
+  griddep_wait();
   __shared__ double part[32][33];
   const uint32_t nt = 2 * ((st->active_count + 255) / 256);
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // row in block, tile group
@@ -689,6 +691,7 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
                         const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
                         uint32_t bpad, uint32_t d, float scale, __nv_bfloat16* __restrict__ Pt,
                         uint64_t ldp, __nv_bfloat16* __restrict__ Xs) {
+  griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < bpad;
        b += (gridDim.x * blockDim.x) >> 5) {
@@ -720,6 +723,7 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
 __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __restrict__ red,
                             uint32_t B, uint32_t nbt, uint32_t splits, uint32_t rows_per_unit,
                             float scale, float* __restrict__ out) {
+  griddep_wait();
   const uint64_t total = (uint64_t)B * 128;  // float4 units (D = 512)
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -742,6 +746,7 @@ __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __r
 
 __global__ void k_zero_rows_bf16(const SelState* st, __nv_bfloat16* W16, uint32_t cap_rows,
                                  uint32_t d) {
+  griddep_wait();
   // rows [count, round_up(count, 256)) of W_sub must be zero for the K loop of GEMM-dX
   const uint32_t c = st->active_count;
   const uint32_t e = min(cap_rows, (c + 255) / 256 * 256);
@@ -870,7 +875,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, nullptr, Wsub16,
                                 wnorm, err, stream));
   ++launches;
-  k_zero_rows_bf16<<<64, 256, 0, stream>>>(st, Wsub16, f->mwpad, D);
+  launch_pdl(k_zero_rows_bf16, 64, 256, 0, stream, st, Wsub16, f->mwpad, D);
   XK_LAUNCH();
 
   mark(3);
@@ -890,24 +895,24 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.partial = f->partial_f;
   ga.nbt = nbp;
   ga.splits = pair_splits(nbp, 1u << 30);
-  k_gemm2<kF><<<kNumSMs, 384, smem_bytes2<kF>(), stream>>>(f->mF_A, f->mF2_B, f->mPt_st, ga);
+  launch_pdl(k_gemm2<kF>, kNumSMs, 384, smem_bytes2<kF>(), stream, f->mF_A, f->mF2_B, f->mPt_st, ga);
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over class shards -> loss
-  k_rowreduce<<<(unsigned)((B + 31) / 32), 1024, 0, stream>>>(st, f->partial_f, f->labelterm, label_col,
+  launch_pdl(k_rowreduce, (unsigned)((B + 31) / 32), 1024, 0, stream, st, f->partial_f, f->labelterm, label_col,
                                                      (uint32_t)B, f->bpad, rowred);
   XK_LAUNCH();
   if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
   XK_CUDA(launch_loss(rowred, B, loss_dev, st, err, stream));
   ++launches;
   // (d) label-column fix-up of P~ and the row-scaled X_hat'
-  k_fixup<4><<<grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream>>>(
+  launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, 
       rowred, label_col, X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16);
   XK_LAUNCH();
   mark(5);
   // (e) GEMM-dW -> bf16 dW rows (compact active order)
   ga.out16 = f->dW16;
-  k_gemm2<kDW><<<kNumSMs, 384, smem_bytes2<kDW>(), stream>>>(f->mDW_A, f->mDW_B, f->mDW_st, ga);
+  launch_pdl(k_gemm2<kDW>, kNumSMs, 384, smem_bytes2<kDW>(), stream, f->mDW_A, f->mDW_B, f->mDW_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
@@ -915,10 +920,10 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   const uint32_t dx_splits = pair_splits(nbp, 148);
   ga.nbt = nbp;
   ga.splits = dx_splits;
-  k_gemm2<kDX><<<kNumSMs, 384, smem_bytes2<kDX>(), stream>>>(f->mDX_A, f->mDX_B, f->mDXP_st, ga);
+  launch_pdl(k_gemm2<kDX>, kNumSMs, 384, smem_bytes2<kDX>(), stream, f->mDX_A, f->mDX_B, f->mDXP_st, ga);
   XK_LAUNCH();
   mark(7);
-  k_dx_reduce<<<grid_for(B * 128, 256), 256, 0, stream>>>(f->partial_dx, rowred, (uint32_t)B,
+  launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred, (uint32_t)B,
                                                            nbp, dx_splits, 256, cfg.scale,
                                                            world > 1 ? dXpart : dX);
   XK_LAUNCH();
@@ -984,7 +989,7 @@ cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t 
   ga.ch = ch;
   ga.kprime = kprime;
   ga.dim = 512;
-  k_gemm2<kG><<<kNumSMs, 384, smem_bytes2<kG>(), s>>>(mA, mB, mA, ga);
+  launch_pdl(k_gemm2<kG>, kNumSMs, 384, smem_bytes2<kG>(), s, mA, mB, mA, ga);
   return cudaGetLastError();
 }
 

@@ -168,7 +168,8 @@ xknn_status_t Layer::ensure_mt_cache() {
   return XKNN_OK;
 }
 
-__global__ void k_set_f32(float* p, float v) { *p = v; }
+__global__ void k_set_f32(float* p, float v) {
+  griddep_wait(); *p = v; }
 
 void Layer::mark(int i, cudaStream_t on) {
   if (!prof_on) return;
@@ -341,7 +342,7 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
                             stream));
   }
   // the learning rate travels through device memory so the captured core stays valid
-  k_set_f32<<<1, 1, 0, stream>>>(lr_dev, lr);
+  launch_pdl(k_set_f32, 1, 1, 0, stream, lr_dev, lr);
   XK_LAUNCH();
   mark(1);
   if (graph_mode) {
@@ -538,6 +539,7 @@ namespace {
 __global__ void k_graph_check(const uint32_t* kpc, const uint64_t* off, const uint32_t* flat,
                               uint64_t n, uint64_t flat_len, uint64_t begin, uint64_t end,
                               unsigned int* kmax, unsigned long long* bad) {
+  xknn::griddep_wait();
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < n;
        c += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t k = kpc[c];
@@ -578,7 +580,7 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   XK_CUDA_H(cudaMalloc(&dk, 16));
   db = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(dk) + 8);
   XK_CUDA_H(cudaMemsetAsync(dk, 0, 16, L.stream));
-  k_graph_check<<<xknn::grid_for(L.n, 256), 256, 0, L.stream>>>(L.g_kpc, L.g_off, L.g_flat, L.n,
+  xknn::launch_pdl(k_graph_check, xknn::grid_for(L.n, 256), 256, 0, L.stream, L.g_kpc, L.g_off, L.g_flat, L.n,
                                                                  flat_len, L.begin, L.end, dk, db);
   ++L.launches;
   unsigned int kmax = 0;

@@ -38,6 +38,7 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
                                  uint64_t id_base, float* __restrict__ out32,
                                  __nv_bfloat16* __restrict__ out16, float* __restrict__ norms,
                                  unsigned long long* err) {
+  griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = count ? *count : rows;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
@@ -88,12 +89,13 @@ __device__ __forceinline__ float4 load_g4(const __nv_bfloat16* __restrict__ G, u
                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
 }
 
-template <int DV, typename GT>
+template <int DV, typename GT = float>
 __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
                               const GT* __restrict__ G, const uint32_t* __restrict__ active,
                               const unsigned int* count, uint64_t begin, uint32_t d,
                               const float* __restrict__ wnorm, const float* __restrict__ lr_dev,
                               float mu, float wd, const unsigned long long* err) {
+  griddep_wait();
   if (*err) return;
   const float lr = *lr_dev;
   const uint32_t lane = threadIdx.x & 31;
@@ -152,6 +154,7 @@ template <int DV>
 __global__ void k_feature_backward(const float* __restrict__ X, const float* __restrict__ xnorm,
                                    const float* __restrict__ G, uint64_t rows, uint32_t d,
                                    float* __restrict__ out) {
+  griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
@@ -193,10 +196,10 @@ __global__ void k_feature_backward(const float* __restrict__ X, const float* __r
 
 #define XKNN_DISPATCH_D(d, KERNEL, GRID, BLOCK, STREAM, ...)                              \
   switch ((d) / 128) {                                                                    \
-    case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
-    case 2: KERNEL<2><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
-    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
-    case 8: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                    \
+    case 1: launch_pdl(KERNEL<1>, GRID, BLOCK, 0, STREAM, __VA_ARGS__); break;                    \
+    case 2: launch_pdl(KERNEL<2>, GRID, BLOCK, 0, STREAM, __VA_ARGS__); break;                    \
+    case 4: launch_pdl(KERNEL<4>, GRID, BLOCK, 0, STREAM, __VA_ARGS__); break;                    \
+    case 8: launch_pdl(KERNEL<8>, GRID, BLOCK, 0, STREAM, __VA_ARGS__); break;                    \
     default: return cudaErrorInvalidValue;                                                \
   }
 
@@ -227,7 +230,7 @@ cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
                                     const unsigned long long* err, cudaStream_t s) {
   if (d != 512) return cudaErrorInvalidValue;
   const unsigned grid = grid_for(max_rows * 32, 256, 148u * 16u);
-  k_update_rows<4, __nv_bfloat16><<<grid, 256, 0, s>>>(W, V, G, active, count, begin, d, wnorm,
+  launch_pdl(k_update_rows<4, __nv_bfloat16>, grid, 256, 0, s, W, V, G, active, count, begin, d, wnorm,
                                                        lr, mu, wd, err);
   return cudaGetLastError();
 }

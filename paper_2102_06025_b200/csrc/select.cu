@@ -37,6 +37,7 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
                             const uint64_t* __restrict__ off, const uint32_t* __restrict__ flat,
                             uint32_t* pool_bits, uint32_t* lab_bits, uint32_t* best, uint32_t* occ,
                             SelState* st, unsigned long long* err, int reset) {
+  griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -83,6 +84,7 @@ __device__ __forceinline__ uint32_t final_word(int mode, const SelState* st, con
 
 // exclusive scan of the per-block counts (nblocks + 1 entries, last is the total), one CTA
 __global__ void k_scan_blocks(const uint32_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
+  griddep_wait();
   using BS = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ uint32_t carry;
@@ -103,6 +105,7 @@ __global__ void k_scan_blocks(const uint32_t* __restrict__ in, uint32_t n, uint3
 __global__ void k_bits_count(int mode, SelState* st, const uint32_t* __restrict__ act,
                              const uint32_t* __restrict__ pool, const uint32_t* __restrict__ lab,
                              uint64_t nwords, uint32_t* blk_counts) {
+  griddep_wait();
   using BR = cub::BlockReduce<uint32_t, kCompactBlock>;
   __shared__ typename BR::TempStorage tmp;
   __shared__ typename BR::TempStorage tmp2;
@@ -126,6 +129,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
                              uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
                              uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
                              int rank) {
+  griddep_wait();
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
   __shared__ typename BS::TempStorage tmp;
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
@@ -159,6 +163,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
 __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int world, int rank,
                        uint64_t n, uint64_t m, uint64_t begin, uint64_t nw,
                        unsigned long long* err) {
+  griddep_wait();
   unsigned long long total = 0, before = 0, nd = 0;
   for (int s = 0; s < world; ++s) {
     total += pool_counts[2 * s];
@@ -189,6 +194,7 @@ __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int 
 
 // ---- padding: Lemire draws from the cached mt19937_64 stream
 __global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint32_t* __restrict__ key) {
+  griddep_wait();
   if (st->branch != kPad) return;
   const uint64_t need = st->need, csize = st->csize;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < need;
@@ -208,6 +214,7 @@ __global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint32_t*
 // probability ~ need*csize/2^64 per step.
 __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, uint64_t mt_len,
                                uint32_t* key, unsigned long long* err) {
+  griddep_wait();
   if (st->branch != kPad || st->first_rej == kNone) return;
   const uint64_t need = st->need, csize = st->csize;
   uint64_t pos = st->first_rej;
@@ -233,6 +240,7 @@ __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, ui
 // (~need^2 / 2|C| pairs), so groups have one or two members.
 __global__ void k_link(const SelState* st, const uint32_t* __restrict__ key, uint32_t* head,
                        uint32_t* __restrict__ nxt, uint32_t* __restrict__ lw) {
+  griddep_wait();
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
@@ -247,6 +255,7 @@ __global__ void k_link(const SelState* st, const uint32_t* __restrict__ key, uin
 __global__ void k_resolve(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ head, const uint32_t* __restrict__ nxt,
                           uint32_t* __restrict__ pred, uint32_t* __restrict__ lw) {
+  griddep_wait();
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
@@ -269,6 +278,7 @@ __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ pred, const uint32_t* __restrict__ lw,
                           const uint32_t* __restrict__ pool_list, uint64_t begin,
                           uint32_t* act_bits, uint32_t* head) {
+  griddep_wait();
   if (st->branch != kPad) return;
   const uint64_t need = st->need, cbase = st->cbase, cl = st->compl_local;
   const uint32_t npool = st->pool_count;
@@ -299,6 +309,7 @@ __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
 __global__ void k_of_hist_rank(const SelState* st, const uint32_t* __restrict__ pool_list,
                                uint64_t begin, const uint32_t* __restrict__ lab_bits,
                                const uint32_t* __restrict__ best, uint32_t* hist) {
+  griddep_wait();
   if (st->branch != kOverfull) return;
   const uint32_t np = st->pool_count;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -309,6 +320,7 @@ __global__ void k_of_hist_rank(const SelState* st, const uint32_t* __restrict__ 
 }
 
 __global__ void k_of_plan_rank(SelState* st, const uint32_t* hist, uint32_t nbins) {
+  griddep_wait();
   if (st->branch != kOverfull) return;
   const unsigned long long t = st->take;
   unsigned long long cum = 0;
@@ -325,6 +337,7 @@ __global__ void k_of_hist_occ(const SelState* st, const uint32_t* __restrict__ p
                               uint64_t begin, const uint32_t* __restrict__ lab_bits,
                               const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
                               uint32_t* hist) {
+  griddep_wait();
   if (st->branch != kOverfull) return;
   const uint32_t np = st->pool_count, rs = st->r_star;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -335,6 +348,7 @@ __global__ void k_of_hist_occ(const SelState* st, const uint32_t* __restrict__ p
 }
 
 __global__ void k_of_plan_occ(SelState* st, const uint32_t* hist, uint32_t nbins) {
+  griddep_wait();
   if (st->branch != kOverfull) return;
   const unsigned long long t = st->tie_quota;
   unsigned long long cum = 0;
@@ -352,6 +366,7 @@ __global__ void k_of_tie_count(SelState* st, const uint32_t* __restrict__ pool_l
                                uint64_t begin, const uint32_t* __restrict__ lab_bits,
                                const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
                                unsigned long long* tie_counts, int rank) {
+  griddep_wait();
   if (st->branch != kOverfull) { if (threadIdx.x == 0 && blockIdx.x == 0) tie_counts[rank] = 0; return; }
   const uint32_t np = st->pool_count, rs = st->r_star, os = st->o_star;
   __shared__ unsigned int cnt;
@@ -372,6 +387,7 @@ __global__ void k_of_select(SelState* st, const uint32_t* __restrict__ pool_list
                             const uint32_t* __restrict__ lab_bits, const uint32_t* __restrict__ best,
                             const uint32_t* __restrict__ occ, const unsigned long long* tie_counts,
                             int rank, uint32_t nbins_rank, uint32_t* act_bits) {
+  griddep_wait();
   if (st->branch != kOverfull) return;
   using BS = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
@@ -413,6 +429,7 @@ __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ la
                              const uint32_t* __restrict__ pos_of, uint64_t begin, uint64_t end,
                              int32_t* label_col, const uint32_t* __restrict__ pool_list,
                              uint32_t* best, uint32_t* occ) {
+  griddep_wait();
   const uint32_t na = st->active_count, np = st->pool_count;
   // reset the candidate ranks of this step's pool (every touched class is in the pool)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -432,6 +449,7 @@ __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ la
 }
 
 __global__ void k_zero_sel(SelState* st) {
+  griddep_wait();
   st->labels_local = 0;
   st->labels_found = 0;
   st->pool_count = 0;
@@ -443,13 +461,13 @@ __global__ void k_zero_sel(SelState* st) {
 // Compacts this shard's bitmap (mode 0: pool, mode 1: final active set) into sorted global ids.
 static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* pos_of) {
   const uint32_t nblocks = (uint32_t)((L.nwords + kCompactBlock - 1) / kCompactBlock);
-  k_bits_count<<<nblocks, kCompactBlock, 0, L.stream>>>(mode, L.st, L.act_bits, L.pool_bits,
+  launch_pdl(k_bits_count, nblocks, kCompactBlock, 0, L.stream, mode, L.st, L.act_bits, L.pool_bits,
                                                         L.lab_bits, L.nwords, L.blk_counts);
   ++L.launches;
   // blk_counts[nblocks] is kept 0, so the exclusive scan's last entry is the total
-  k_scan_blocks<<<1, 1024, 0, L.stream>>>(L.blk_counts, nblocks + 1, L.blk_counts + nblocks + 1);
+  launch_pdl(k_scan_blocks, 1, 1024, 0, L.stream, L.blk_counts, nblocks + 1, L.blk_counts + nblocks + 1);
   ++L.launches;
-  k_bits_write<<<nblocks, kCompactBlock, 0, L.stream>>>(
+  launch_pdl(k_bits_write, nblocks, kCompactBlock, 0, L.stream, 
       mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
       nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank);
   ++L.launches;
@@ -462,12 +480,12 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
   XK_TRY(ensure_mt_cache());
   // pool_bits, act_bits, lab_bits are one allocation
   XK_CUDA(cudaMemsetAsync(pool_bits, 0, 3 * nwords * sizeof(uint32_t), stream));
-  k_zero_sel<<<1, 1, 0, stream>>>(st);
+  launch_pdl(k_zero_sel, 1, 1, 0, stream, st);
   XK_LAUNCH();
 
   // (1) pool of this shard: union of its slices for every batch label (knn_softmax.cpp:122-132),
   //     candidate best rank / occurrences, and the labels this shard owns
-  k_mark_pool<<<grid_for((uint64_t)B * 32, 256), 256, 0, stream>>>(
+  launch_pdl(k_mark_pool, grid_for((uint64_t)B * 32, 256), 256, 0, stream, 
       labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
       st, err, 0);
   XK_LAUNCH();
@@ -475,20 +493,20 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
   XK_TRY(compact_bits(*this, 0, pool_list, nullptr));
   if (world > 1)
     XK_NCCL(ncclAllGather(pool_counts + 2 * rank, pool_counts, 2, ncclUint64, comm, stream));
-  k_plan<<<1, 1, 0, stream>>>(st, pool_counts, world, rank, n, m, begin, nw, err);
+  launch_pdl(k_plan, 1, 1, 0, stream, st, pool_counts, world, rank, n, m, begin, nw, err);
   XK_LAUNCH();
 
   // (3a) padding branch (|pool| < M): picks from the cached stream, Fisher-Yates chains
   if (m > 0) {
-    k_picks<<<grid_for(m, 256), 256, 0, stream>>>(st, mt_cache, pick_key);
+    launch_pdl(k_picks, grid_for(m, 256), 256, 0, stream, st, mt_cache, pick_key);
     XK_LAUNCH();
-    k_picks_replay<<<1, 1, 0, stream>>>(st, mt_cache, mt_len, pick_key, err);
+    launch_pdl(k_picks_replay, 1, 1, 0, stream, st, mt_cache, mt_len, pick_key, err);
     XK_LAUNCH();
-    k_link<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pick_head, pick_val, lw);
+    launch_pdl(k_link, grid_for(m, 256), 256, 0, stream, st, pick_key, pick_head, pick_val, lw);
     XK_LAUNCH();
-    k_resolve<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pick_head, pick_val, pred, lw);
+    launch_pdl(k_resolve, grid_for(m, 256), 256, 0, stream, st, pick_key, pick_head, pick_val, pred, lw);
     XK_LAUNCH();
-    k_pad_map<<<grid_for(m, 256), 256, 0, stream>>>(st, pick_key, pred, lw, pool_list, begin,
+    launch_pdl(k_pad_map, grid_for(m, 256), 256, 0, stream, st, pick_key, pred, lw, pool_list, begin,
                                                      act_bits, pick_head);
     XK_LAUNCH();
   }
@@ -500,30 +518,30 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
     uint32_t* h_rank = hist;
     uint32_t* h_occ = hist + nb_rank;
     XK_CUDA(cudaMemsetAsync(hist, 0, (nb_rank + nb_occ) * sizeof(uint32_t), stream));
-    k_of_hist_rank<<<grid_for(nw, 256), 256, 0, stream>>>(st, pool_list, begin, lab_bits,
+    launch_pdl(k_of_hist_rank, grid_for(nw, 256), 256, 0, stream, st, pool_list, begin, lab_bits,
                                                           sel_best, h_rank);
     XK_LAUNCH();
     if (world > 1) XK_NCCL(ncclAllReduce(h_rank, h_rank, nb_rank, ncclUint32, ncclSum, comm, stream));
-    k_of_plan_rank<<<1, 1, 0, stream>>>(st, h_rank, nb_rank);
+    launch_pdl(k_of_plan_rank, 1, 1, 0, stream, st, h_rank, nb_rank);
     XK_LAUNCH();
-    k_of_hist_occ<<<grid_for(nw, 256), 256, 0, stream>>>(st, pool_list, begin, lab_bits,
+    launch_pdl(k_of_hist_occ, grid_for(nw, 256), 256, 0, stream, st, pool_list, begin, lab_bits,
                                                          sel_best, sel_occ, h_occ);
     XK_LAUNCH();
     if (world > 1) XK_NCCL(ncclAllReduce(h_occ, h_occ, nb_occ, ncclUint32, ncclSum, comm, stream));
-    k_of_plan_occ<<<1, 1, 0, stream>>>(st, h_occ, nb_occ);
+    launch_pdl(k_of_plan_occ, 1, 1, 0, stream, st, h_occ, nb_occ);
     XK_LAUNCH();
-    k_of_tie_count<<<1, 1024, 0, stream>>>(st, pool_list, begin, lab_bits, sel_best, sel_occ,
+    launch_pdl(k_of_tie_count, 1, 1024, 0, stream, st, pool_list, begin, lab_bits, sel_best, sel_occ,
                                            tie_counts, rank);
     XK_LAUNCH();
     if (world > 1)
       XK_NCCL(ncclAllGather(tie_counts + rank, tie_counts, 1, ncclUint64, comm, stream));
-    k_of_select<<<1, 1024, 0, stream>>>(st, pool_list, begin, lab_bits, sel_best, sel_occ,
+    launch_pdl(k_of_select, 1, 1024, 0, stream, st, pool_list, begin, lab_bits, sel_best, sel_occ,
                                         tie_counts, rank, nb_rank, act_bits);
     XK_LAUNCH();
   }
   // (4) this shard's ActiveSet slice, sorted by construction; label -> column map
   XK_TRY(compact_bits(*this, 1, active, pos_of));
-  k_label_cols<<<grid_for(std::max<uint64_t>(B, (uint64_t)B * g_kmax), 256), 256, 0, stream>>>(
+  launch_pdl(k_label_cols, grid_for(std::max<uint64_t>(B, (uint64_t)B * g_kmax), 256), 256, 0, stream, 
       st, labels_all, B, active, pos_of, begin, end, label_col, pool_list, sel_best, sel_occ);
   XK_LAUNCH();
   return XKNN_OK;

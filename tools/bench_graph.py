@@ -19,7 +19,7 @@ import torch  # noqa: E402
 import paper_2102_06025_b200 as X  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--classes", type=int, default=1_000_000)
 ap.add_argument("--k", type=int, default=100)
 ap.add_argument("--kprime", type=int, default=200)
 a = ap.parse_args()
@@ -34,7 +34,7 @@ if world > 1:
     uid = [X.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = X.nccl_comm_init(uid[0], world, rank)
-b, e = X.ShardLayout(a.n, world).class_range(rank)
+b, e = X.ShardLayout(a.classes, world).class_range(rank)
 g = torch.Generator(device="cuda")
 g.manual_seed(1000 + rank)
 w = torch.empty(e - b, 512, device="cuda")
@@ -52,7 +52,7 @@ if world > 1:
 t0 = time.perf_counter()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ev0.record()
-out, unc, steps = X.graph_ring(w, a.n, a.k, a.kprime, rank, world, comm)
+out, unc, steps = X.graph_ring(w, a.classes, a.k, a.kprime, rank, world, comm)
 ev1.record()
 ev1.synchronize()
 sec = ev0.elapsed_time(ev1) / 1e3
@@ -65,9 +65,9 @@ if world > 1:
     unc = int(ut.item())
 if rank == 0:
     peaks = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))
-    pairs = float(a.n) * a.n
+    pairs = float(a.classes) * a.classes
     tf = 2.0 * pairs * 512 / sec / 1e12
-    print(json.dumps({"metric": "exact KNN graph rebuild pairs/s", "n": a.n, "k": a.k,
+    print(json.dumps({"metric": "exact KNN graph rebuild pairs/s", "n": a.classes, "k": a.k,
                       "kprime": a.kprime, "n_gpus": world, "seconds": round(sec, 3),
                       "pairs_per_s": pairs / sec, "tflops_equiv": round(tf, 1),
                       "frac_of_tensor_peak": round(tf / (world * peaks["bf16_tflops_sustained"]), 4),
