@@ -31,6 +31,11 @@ __device__ __forceinline__ void raise_error(unsigned long long* err, int code, u
 __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// lets the next PDL kernel launch now (it still waits for this grid's completion in its own
+// griddep_wait): small kernels call it right away so a chain of them runs back to back
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -86,6 +86,7 @@ __global__ void k_gemm_nn_exact(const float* __restrict__ G, const float* __rest
 __global__ void k_rowmax(const float* __restrict__ L, uint64_t rows, const unsigned int* cols_dev,
                          float* __restrict__ rowmax) {
   griddep_wait();
+  griddep_launch();
   const uint64_t cols = *cols_dev;
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
@@ -103,6 +104,7 @@ __global__ void k_rowsum(const float* __restrict__ L, uint64_t rows, const unsig
                          const float* __restrict__ rowmax, const int32_t* __restrict__ label_col,
                          double* __restrict__ red) {
   griddep_wait();
+  griddep_launch();
   const uint64_t cols = *cols_dev;
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
@@ -125,6 +127,7 @@ __global__ void k_rowsum(const float* __restrict__ L, uint64_t rows, const unsig
 __global__ void k_loss(const double* __restrict__ red, uint64_t rows, double* loss,
                        SelState* st, unsigned long long* err) {
   griddep_wait();
+  griddep_launch();
   __shared__ double part[256];
   double s = 0.0;
   // fixed-order blocked sum: thread t sums rows [t*c, (t+1)*c) sequentially

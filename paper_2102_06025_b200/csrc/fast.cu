@@ -666,6 +666,7 @@ __global__ void k_rowreduce(const SelState* st, const float* __restrict__ partia
                             const float* __restrict__ labelterm, const int32_t* __restrict__ lcol,
                             uint32_t B, uint32_t bpad, double* __restrict__ red) {
   griddep_wait();
+  griddep_launch();
   __shared__ double part[32][33];
   const uint32_t nt = 2 * ((st->active_count + 255) / 256);
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // row in block, tile group
@@ -692,6 +693,7 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
                         uint32_t bpad, uint32_t d, float scale, __nv_bfloat16* __restrict__ Pt,
                         uint64_t ldp, __nv_bfloat16* __restrict__ Xs) {
   griddep_wait();
+  griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < bpad;
        b += (gridDim.x * blockDim.x) >> 5) {
@@ -724,6 +726,7 @@ __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __r
                             uint32_t B, uint32_t nbt, uint32_t splits, uint32_t rows_per_unit,
                             float scale, float* __restrict__ out) {
   griddep_wait();
+  griddep_launch();
   const uint64_t total = (uint64_t)B * 128;  // float4 units (D = 512)
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -747,6 +750,7 @@ __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __r
 __global__ void k_zero_rows_bf16(const SelState* st, __nv_bfloat16* W16, uint32_t cap_rows,
                                  uint32_t d) {
   griddep_wait();
+  griddep_launch();
   // rows [count, round_up(count, 256)) of W_sub must be zero for the K loop of GEMM-dX
   const uint32_t c = st->active_count;
   const uint32_t e = min(cap_rows, (c + 255) / 256 * 256);

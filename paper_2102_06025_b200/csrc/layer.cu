@@ -169,7 +169,8 @@ xknn_status_t Layer::ensure_mt_cache() {
 }
 
 __global__ void k_set_f32(float* p, float v) {
-  griddep_wait(); *p = v; }
+  griddep_wait();
+  griddep_launch(); *p = v; }
 
 void Layer::mark(int i, cudaStream_t on) {
   if (!prof_on) return;

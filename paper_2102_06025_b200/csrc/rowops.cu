@@ -155,6 +155,7 @@ __global__ void k_feature_backward(const float* __restrict__ X, const float* __r
                                    const float* __restrict__ G, uint64_t rows, uint32_t d,
                                    float* __restrict__ out) {
   griddep_wait();
+  griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {

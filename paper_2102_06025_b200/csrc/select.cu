@@ -38,6 +38,7 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
                             uint32_t* pool_bits, uint32_t* lab_bits, uint32_t* best, uint32_t* occ,
                             SelState* st, unsigned long long* err, int reset) {
   griddep_wait();
+  griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -85,6 +86,7 @@ __device__ __forceinline__ uint32_t final_word(int mode, const SelState* st, con
 // exclusive scan of the per-block counts (nblocks + 1 entries, last is the total), one CTA
 __global__ void k_scan_blocks(const uint32_t* __restrict__ in, uint32_t n, uint32_t* __restrict__ out) {
   griddep_wait();
+  griddep_launch();
   using BS = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ uint32_t carry;
@@ -106,6 +108,7 @@ __global__ void k_bits_count(int mode, SelState* st, const uint32_t* __restrict_
                              const uint32_t* __restrict__ pool, const uint32_t* __restrict__ lab,
                              uint64_t nwords, uint32_t* blk_counts) {
   griddep_wait();
+  griddep_launch();
   using BR = cub::BlockReduce<uint32_t, kCompactBlock>;
   __shared__ typename BR::TempStorage tmp;
   __shared__ typename BR::TempStorage tmp2;
@@ -130,6 +133,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
                              uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
                              int rank) {
   griddep_wait();
+  griddep_launch();
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
   __shared__ typename BS::TempStorage tmp;
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
@@ -164,6 +168,7 @@ __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int 
                        uint64_t n, uint64_t m, uint64_t begin, uint64_t nw,
                        unsigned long long* err) {
   griddep_wait();
+  griddep_launch();
   unsigned long long total = 0, before = 0, nd = 0;
   for (int s = 0; s < world; ++s) {
     total += pool_counts[2 * s];
@@ -195,6 +200,7 @@ __global__ void k_plan(SelState* st, const unsigned long long* pool_counts, int 
 // ---- padding: Lemire draws from the cached mt19937_64 stream
 __global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint32_t* __restrict__ key) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kPad) return;
   const uint64_t need = st->need, csize = st->csize;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < need;
@@ -215,6 +221,7 @@ __global__ void k_picks(SelState* st, const uint64_t* __restrict__ mt, uint32_t*
 __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, uint64_t mt_len,
                                uint32_t* key, unsigned long long* err) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kPad || st->first_rej == kNone) return;
   const uint64_t need = st->need, csize = st->csize;
   uint64_t pos = st->first_rej;
@@ -241,6 +248,7 @@ __global__ void k_picks_replay(SelState* st, const uint64_t* __restrict__ mt, ui
 __global__ void k_link(const SelState* st, const uint32_t* __restrict__ key, uint32_t* head,
                        uint32_t* __restrict__ nxt, uint32_t* __restrict__ lw) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
@@ -256,6 +264,7 @@ __global__ void k_resolve(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ head, const uint32_t* __restrict__ nxt,
                           uint32_t* __restrict__ pred, uint32_t* __restrict__ lw) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kPad) return;
   const uint32_t need = (uint32_t)st->need;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < need; i += gridDim.x * blockDim.x) {
@@ -279,6 +288,7 @@ __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ pool_list, uint64_t begin,
                           uint32_t* act_bits, uint32_t* head) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kPad) return;
   const uint64_t need = st->need, cbase = st->cbase, cl = st->compl_local;
   const uint32_t npool = st->pool_count;
@@ -310,6 +320,7 @@ __global__ void k_of_hist_rank(const SelState* st, const uint32_t* __restrict__ 
                                uint64_t begin, const uint32_t* __restrict__ lab_bits,
                                const uint32_t* __restrict__ best, uint32_t* hist) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) return;
   const uint32_t np = st->pool_count;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -321,6 +332,7 @@ __global__ void k_of_hist_rank(const SelState* st, const uint32_t* __restrict__ 
 
 __global__ void k_of_plan_rank(SelState* st, const uint32_t* hist, uint32_t nbins) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) return;
   const unsigned long long t = st->take;
   unsigned long long cum = 0;
@@ -338,6 +350,7 @@ __global__ void k_of_hist_occ(const SelState* st, const uint32_t* __restrict__ p
                               const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
                               uint32_t* hist) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) return;
   const uint32_t np = st->pool_count, rs = st->r_star;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -349,6 +362,7 @@ __global__ void k_of_hist_occ(const SelState* st, const uint32_t* __restrict__ p
 
 __global__ void k_of_plan_occ(SelState* st, const uint32_t* hist, uint32_t nbins) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) return;
   const unsigned long long t = st->tie_quota;
   unsigned long long cum = 0;
@@ -367,6 +381,7 @@ __global__ void k_of_tie_count(SelState* st, const uint32_t* __restrict__ pool_l
                                const uint32_t* __restrict__ best, const uint32_t* __restrict__ occ,
                                unsigned long long* tie_counts, int rank) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) { if (threadIdx.x == 0 && blockIdx.x == 0) tie_counts[rank] = 0; return; }
   const uint32_t np = st->pool_count, rs = st->r_star, os = st->o_star;
   __shared__ unsigned int cnt;
@@ -388,6 +403,7 @@ __global__ void k_of_select(SelState* st, const uint32_t* __restrict__ pool_list
                             const uint32_t* __restrict__ occ, const unsigned long long* tie_counts,
                             int rank, uint32_t nbins_rank, uint32_t* act_bits) {
   griddep_wait();
+  griddep_launch();
   if (st->branch != kOverfull) return;
   using BS = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
@@ -430,6 +446,7 @@ __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ la
                              int32_t* label_col, const uint32_t* __restrict__ pool_list,
                              uint32_t* best, uint32_t* occ) {
   griddep_wait();
+  griddep_launch();
   const uint32_t na = st->active_count, np = st->pool_count;
   // reset the candidate ranks of this step's pool (every touched class is in the pool)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
@@ -450,6 +467,7 @@ __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ la
 
 __global__ void k_zero_sel(SelState* st) {
   griddep_wait();
+  griddep_launch();
   st->labels_local = 0;
   st->labels_found = 0;
   st->pool_count = 0;
