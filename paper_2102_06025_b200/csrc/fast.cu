@@ -106,15 +106,19 @@ struct Unit2 {
   bool valid;
 };
 
-template <int KIND>
+// Work units of one CTA pair.  With MCP = 2 the two pairs of a 4-CTA cluster take sibling
+// units in lockstep -- different 256-row A tiles (batch tiles / query blocks), the same B stream
+// -- and every B tile is fetched once per cluster and multicast to both pairs.
+template <int KIND, int MCP>
 __device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
   if (KIND == kDW) return (mw + 255) / 256;
-  if (KIND == kG) return (a.nrows + 255) / 256;
-  return a.nbt * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per pair-tile
+  if (KIND == kG) return (a.nrows + 256 * MCP - 1) / (256 * MCP);
+  return a.nbt / MCP * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per tile
 }
 
-template <int KIND>
-__device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32_t u) {
+template <int KIND, int MCP>
+__device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32_t u,
+                                          uint32_t pc) {
   Unit2 x{};
   x.id = u;
   if (KIND == kDW) {
@@ -123,13 +127,15 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
     return x;
   }
   if (KIND == kG) {  // one 256-row query block against every 256-column tile of the block
-    x.row0 = u * 256;
+    x.row0 = (u * MCP + pc) * 256;
     x.t0 = 0;
     x.t1 = (a.ncols + 255) / 256;
     x.valid = true;
     return x;
   }
-  const uint32_t bp = u % a.nbt, r = u / a.nbt;
+  const uint32_t nbc = a.nbt / MCP;
+  const uint32_t bp = (u % nbc) * MCP + pc, r = u / nbc;
+  x.id = bp + r * a.nbt;  // the pair-tile unit index (dX partial slots)
   const uint32_t nt = KIND == kF ? (mw + 255) / 256 : (mw + 31) / 32;
   x.row0 = bp * 256;
   x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
@@ -276,8 +282,8 @@ __device__ __noinline__ void merge_candidates(float2* __restrict__ list, uint32_
 
 // Region full: the new cut is the kprime-th largest score; keep the entries strictly above it.
 // Every dropped (and every later rejected) column has approx score <= the returned cut.
-template <int KIND>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+template <int KIND, int MCP = 1>
+__global__ void __launch_bounds__(384, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ CUtensorMap tmOut, GemmArgs a) {
   using C = Cfg2<KIND>;
@@ -298,14 +304,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t cta = tc::cluster_ctarank();
+  // cluster of 2 * MCP CTAs: MCP CTA pairs; cta = rank in the pair, pc = pair in the cluster
+  const uint32_t crank = tc::cluster_ctarank();
+  const uint32_t cta = crank & 1, pc = crank >> 1, lead = crank & ~1u;
   const bool leader = cta == 0;
-  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint16_t pmask = (uint16_t)(3u << (2 * pc));        // this pair's CTAs
+  const uint16_t cmask = (uint16_t)((1u << (2 * MCP)) - 1);  // every CTA of the cluster
+  const uint16_t bmask = (uint16_t)((1u << cta) | (1u << (cta + 2)));  // B multicast (MCP = 2)
+  // unit stream: one per cluster (its pairs take sibling units)
+  const uint32_t pair = blockIdx.x / (2 * MCP), npairs = gridDim.x / (2 * MCP);
 
   if (warp == 0 && lane == 0) {
     for (uint32_t s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], MCP);  // a stage is free once every pair's MMAs consumed it
     }
     for (uint32_t s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
@@ -327,14 +339,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   griddep_wait();  // the setup above overlapped the previous kernel's tail (PDL)
 
   const uint32_t mw = KIND == kG ? a.nrows : a.st->active_count;
-  const uint32_t nunits = num_units2<KIND>(a, mw);
+  const uint32_t nunits = num_units2<KIND, MCP>(a, mw);
 
   if (warp == 0) {
     // ================= TMA producer (both CTAs load their half) =================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, aphase = 0;
       for (uint32_t u = pair; u < nunits; u += npairs) {
-        const Unit2 x = unit2_of<KIND>(a, mw, u);
+        const Unit2 x = unit2_of<KIND, MCP>(a, mw, u, pc);
         if (!x.valid) continue;
         const int32_t myrow = (int32_t)(x.row0 + cta * 128);
         uint32_t nk;
@@ -358,8 +370,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           uint8_t* dB = sB + stage * C::B_BYTES;
           if (KIND == kF || KIND == kG) {
             const uint32_t ct = x.t0 + k / 8, kc = k % 8;
-            tc::tma_load_2d_2sm(dB, &tmB, &full[stage], (int32_t)(kc * 64),
-                                (int32_t)(ct * 256 + cta * 128));
+            if (MCP == 1)
+              tc::tma_load_2d_2sm(dB, &tmB, &full[stage], (int32_t)(kc * 64),
+                                  (int32_t)(ct * 256 + cta * 128));
+            else  // this pair fetches 64 of the 128 rows for both pairs (tmB box: 64 rows)
+              tc::tma_load_2d_2sm_mc(dB + pc * 8192, &tmB, &full[stage], (int32_t)(kc * 64),
+                                     (int32_t)(ct * 256 + cta * 128 + pc * 64), bmask);
           } else {
             const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * 32);
             if (KIND == kDX) {
@@ -369,12 +385,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               for (int j = 0; j < 2; ++j)  // P~ᵀ: this CTA's 128 classes at batch rows kk..
                 tc::tma_load_2d_2sm(dA + j * 4096, &tmA, &full[stage], myrow + j * 64, kk);
             }
+            if (MCP == 1 || KIND == kDW) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+              for (int j = 0; j < 2; ++j)
 #pragma unroll
-              for (int h = 0; h < 2; ++h)  // this CTA's half of each 256-wide N instruction
-                tc::tma_load_2d_2sm(dB + (j * 2 + h) * 4096, &tmB, &full[stage],
-                                    (int32_t)(256 * j + 128 * cta + 64 * h), kk);
+                for (int h = 0; h < 2; ++h)  // this CTA's half of each 256-wide N instruction
+                  tc::tma_load_2d_2sm(dB + (j * 2 + h) * 4096, &tmB, &full[stage],
+                                      (int32_t)(256 * j + 128 * cta + 64 * h), kk);
+            } else {  // pair pc fetches the h = pc pieces for both pairs
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tc::tma_load_2d_2sm_mc(dB + (j * 2 + pc) * 4096, &tmB, &full[stage],
+                                       (int32_t)(256 * j + 128 * cta + 64 * pc), kk, bmask);
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -385,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if (leader && lane == 0) {
       uint32_t stage = 0, phase = 0, buf = 0, tphase = 0, aphase = 0;
       for (uint32_t u = pair; u < nunits; u += npairs) {
-        const Unit2 x = unit2_of<KIND>(a, mw, u);
+        const Unit2 x = unit2_of<KIND, MCP>(a, mw, u, pc);
         if (!x.valid) continue;
         const uint32_t ntile = (KIND == kF || KIND == kG) ? x.t1 - x.t0 : 1;
         if (KIND == kF || KIND == kG) {
@@ -427,14 +450,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                                    id, (k | kk) != 0);
               }
             }
-            tc::mma_commit_2sm(&empty[stage]);
+            tc::mma_commit_2sm(&empty[stage], cmask);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          if (nk) tc::mma_commit_2sm(&tfull[buf]);
-          else { tc::mbar_arrive_remote(&tfull[buf], 0); tc::mbar_arrive_remote(&tfull[buf], 1); }
+          if (nk) tc::mma_commit_2sm(&tfull[buf], pmask);
+          else { tc::mbar_arrive_remote(&tfull[buf], lead); tc::mbar_arrive_remote(&tfull[buf], lead + 1); }
           if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
         }
-        if (KIND == kF || KIND == kG) tc::mma_commit_2sm(aempty);  // resident A may be replaced
+        if (KIND == kF || KIND == kG) tc::mma_commit_2sm(aempty, pmask);  // A may be replaced
       }
     }
   } else if (warp >= 4) {
@@ -457,12 +480,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       __syncwarp();
     };
     for (uint32_t u = pair; u < nunits; u += npairs) {
-      const Unit2 x = unit2_of<KIND>(a, mw, u);
+      const Unit2 x = unit2_of<KIND, MCP>(a, mw, u, pc);
       if (!x.valid) continue;
       const uint32_t ntile = (KIND == kF || KIND == kG) ? x.t1 - x.t0 : 1;
       // kG: this thread's (row, column half) candidate region state for the whole unit
       const uint32_t grow = x.row0 + cta * 128 + row;
-      const uint32_t slot = pair * 256 + cta * 128 + row;
+      const uint32_t slot = (blockIdx.x >> 1) * 256 + cta * 128 + row;
       float2* creg = KIND == kG ? a.cand + ((uint64_t)slot * 2 + h) * a.ch : nullptr;
       uint32_t ccnt = 0;
       float ctau = -INFINITY;
@@ -544,7 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], lead);
           if (t + 1 == ntile) {
             a.cnt[slot * 2 + h] = ccnt;
             a.tau[slot * 2 + h] = ctau;
@@ -598,7 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], lead);
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
         } else {
@@ -627,7 +650,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], lead);
         }
         if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
       }
@@ -641,7 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const uint32_t gr = x.row0 + cta * 128 + r;
           if (gr < a.nrows)
             merge_candidates(a.list, a.lcnt, a.lcut, a.cand, a.cnt, a.tau, a.ch, a.kprime, gr,
-                             pair * 256 + cta * 128 + r, lane);
+                             (blockIdx.x >> 1) * 256 + cta * 128 + r, lane);
         }
         epilogue_bar();  // regions free for the next unit
       }
@@ -799,22 +822,46 @@ struct FastState {
   float* partial_dx = nullptr;      // [units][256][512]
   __nv_bfloat16* dW16 = nullptr;    // [mwpad][512] weight gradient, compact active order
   CUtensorMap mF_A, mF2_B, mDX_A, mDX_B, mDW_A, mDW_B;
-  CUtensorMap mPt_st, mDXP_st, mDW_st;
+  CUtensorMap mPt_st, mDXP_st, mDW_st, mF2_B64;
 };
 
 // splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
 // whole waves: the fewest splits with >= 95% wave efficiency (else the most efficient), at most
 // max_units units
-static uint32_t pair_splits(uint32_t nbp, uint32_t max_units) {
+static uint32_t pair_splits(uint32_t nbp, uint32_t max_units, uint32_t streams = 74) {
   uint32_t best = 1;
   double best_eff = -1;
-  for (uint32_t s = 1; s <= 74 && (uint64_t)nbp * s <= max_units; ++s) {
+  for (uint32_t s = 1; s <= streams && (uint64_t)nbp * s <= max_units; ++s) {
     const uint32_t u = nbp * s;
-    const double eff = (double)u / ((double)((u + 73) / 74) * 74);
+    const double eff =
+        (double)u / ((double)((u + streams - 1) / streams) * streams);
     if (eff >= 0.95) return s;
     if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
   }
   return best;
+}
+
+// CTAs of a persistent GEMM launched in clusters of `cluster`: whole clusters that can be
+// co-resident (4-CTA clusters do not tile every GPC of the 148 SMs)
+template <typename K>
+static unsigned cluster_grid(K kernel, unsigned cluster, size_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kNumSMs);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    return kNumSMs / cluster * cluster;
+  }
+  return std::min<unsigned>((unsigned)n * cluster, kNumSMs / cluster * cluster);
 }
 
 xknn_status_t Layer::init_fast() {
@@ -833,13 +880,14 @@ xknn_status_t Layer::init_fast() {
   XK_CUDA(cudaMemsetAsync(Pt, 0, (uint64_t)f->bpad * ldp * 2, stream));
   XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
   XK_CUDA(dalloc(&f->labelterm, f->bpad));
-  f->dx_units_cap = (uint64_t)(f->bpad / 256) * pair_splits(f->bpad / 256, 148) * 256;
+  f->dx_units_cap = 148ull * 256;  // pair-tile units x 256 rows (at most 148 units)
   XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
   XK_CUDA(dalloc(&f->dW16, (uint64_t)f->mwpad * d));
   XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
   bool ok = true;
   ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mF2_B, Wsub16, d, f->mwpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mF2_B64, Wsub16, d, f->mwpad, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
   ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -852,6 +900,10 @@ xknn_status_t Layer::init_fast() {
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes2<kF>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kDX>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm2<kF, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kF>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDX, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes2<kDX>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kDW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes2<kDW>()));
@@ -898,8 +950,20 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   const uint32_t nbp = (uint32_t)((B + 255) / 256);
   ga.partial = f->partial_f;
   ga.nbt = nbp;
-  ga.splits = pair_splits(nbp, 1u << 30);
-  launch_pdl(k_gemm2<kF>, kNumSMs, 384, smem_bytes2<kF>(), stream, f->mF_A, f->mF2_B, f->mPt_st, ga);
+  // an even number of batch pair tiles: 4-CTA clusters, the class tiles multicast to 2 pairs
+  // (opt-in, XKNN_MULTICAST=1: measured slower at C2 -- 4-CTA clusters fit on fewer SMs)
+  const bool mc = (nbp % 2 == 0) && getenv("XKNN_MULTICAST");
+  static const unsigned grid_f4 = cluster_grid(k_gemm2<kF, 2>, 4, smem_bytes2<kF>());
+  static const unsigned grid_dx4 = cluster_grid(k_gemm2<kDX, 2>, 4, smem_bytes2<kDX>());
+  if (mc) {
+    ga.splits = pair_splits(nbp / 2, 1u << 30, grid_f4 / 4);
+    launch_pdl_cluster(k_gemm2<kF, 2>, grid_f4, 384, smem_bytes2<kF>(), stream, 4u, f->mF_A,
+                       f->mF2_B64, f->mPt_st, ga);
+  } else {
+    ga.splits = pair_splits(nbp, 1u << 30);
+    launch_pdl_cluster(k_gemm2<kF>, kNumSMs, 384, smem_bytes2<kF>(), stream, 2u, f->mF_A,
+                       f->mF2_B, f->mPt_st, ga);
+  }
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over class shards -> loss
@@ -916,15 +980,22 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   mark(5);
   // (e) GEMM-dW -> bf16 dW rows (compact active order)
   ga.out16 = f->dW16;
-  launch_pdl(k_gemm2<kDW>, kNumSMs, 384, smem_bytes2<kDW>(), stream, f->mDW_A, f->mDW_B, f->mDW_st, ga);
+  launch_pdl_cluster(k_gemm2<kDW>, kNumSMs, 384, smem_bytes2<kDW>(), stream, 2u, f->mDW_A,
+                     f->mDW_B, f->mDW_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
   ga.partial = f->partial_dx;
-  const uint32_t dx_splits = pair_splits(nbp, 148);
+  const uint32_t dx_splits =
+      mc ? pair_splits(nbp / 2, 74, grid_dx4 / 4) : pair_splits(nbp, 148);
   ga.nbt = nbp;
   ga.splits = dx_splits;
-  launch_pdl(k_gemm2<kDX>, kNumSMs, 384, smem_bytes2<kDX>(), stream, f->mDX_A, f->mDX_B, f->mDXP_st, ga);
+  if (mc)
+    launch_pdl_cluster(k_gemm2<kDX, 2>, grid_dx4, 384, smem_bytes2<kDX>(), stream, 4u, f->mDX_A,
+                       f->mDX_B, f->mDXP_st, ga);
+  else
+    launch_pdl_cluster(k_gemm2<kDX>, kNumSMs, 384, smem_bytes2<kDX>(), stream, 2u, f->mDX_A,
+                       f->mDX_B, f->mDXP_st, ga);
   XK_LAUNCH();
   mark(7);
   launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred, (uint32_t)B,
@@ -968,14 +1039,19 @@ cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t 
                                     float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
                                     cudaStream_t s) {
   CUtensorMap mA, mB;
+  // 4-CTA clusters: two query blocks per cluster share every class tile (multicast)
+  const bool mc = nrows > 256 && getenv("XKNN_MULTICAST");
   const uint64_t apad = (nrows + 255) / 256 * 256, bpad = (ncols + 255) / 256 * 256;
   if (!make_map(&mA, own, 512, apad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mB, held, 512, bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+      !make_map(&mB, held, 512, bpad, 64, mc ? 64 : 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm2<kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem_bytes2<kG>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_gemm2<kG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes2<kG>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -993,7 +1069,11 @@ cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t 
   ga.ch = ch;
   ga.kprime = kprime;
   ga.dim = 512;
-  launch_pdl(k_gemm2<kG>, kNumSMs, 384, smem_bytes2<kG>(), s, mA, mB, mA, ga);
+  if (mc)
+    launch_pdl_cluster(k_gemm2<kG, 2>, cluster_grid(k_gemm2<kG, 2>, 4, smem_bytes2<kG>()), 384,
+                       smem_bytes2<kG>(), s, 4u, mA, mB, mA, ga);
+  else
+    launch_pdl_cluster(k_gemm2<kG>, kNumSMs, 384, smem_bytes2<kG>(), s, 2u, mA, mB, mA, ga);
   return cudaGetLastError();
 }
 

@@ -145,6 +145,19 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
       "l"(0x1000000000000000ull)
       : "memory");
 }
+// ... multicast to the CTAs of ctamask (same smem offset in each); every destination pair's
+// leader barrier is signalled for the bytes landing in that pair
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* m,
+                                                   uint64_t* bar, int32_t c0, int32_t c1,
+                                                   uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "h"(ctamask), "l"(0x1000000000000000ull)
+      : "memory");
+}
 template <uint32_t NCOLS>
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* slot) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -167,12 +180,13 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, u
       ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u)
       : "memory");
 }
-// commit this thread's prior 2-SM MMAs to the barrier at the same offset in both CTAs
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+// commit this thread's prior 2-SM MMAs to the barrier at the same offset in the CTAs of
+// ctamask (default: the pair of cluster ranks 0 and 1)
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t ctamask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(ctamask)
       : "memory");
 }
 
