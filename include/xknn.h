@@ -241,6 +241,35 @@ xknn_status_t xknn_layer_get_graph(xknn_layer_t* h, uint32_t* k_per_class, uint6
 xknn_status_t xknn_layer_classify(xknn_layer_t* h, const float* queries_dev, uint64_t n_queries,
                                   uint32_t* out_class_dev, float* out_score_dev);
 
+/* ---- DGC gradient sparsification (the paper's Table 6 path, beside the fc layer) ---------- */
+
+/* topk_divide_conquer (sparsify.cpp:41-80): exact top-k of values_dev (len fp32) by |value|
+   descending, ties to the lower index, in that selection order -- the reference's result is the
+   same for every chunk count, so there is no chunk parameter.  KTooLarge (k > len),
+   InvalidArgument (k == 0).  out_idx_dev / out_val_dev: k each.  Synchronizes `stream`. */
+xknn_status_t xknn_topk(const float* values_dev, uint64_t len, uint64_t k, uint64_t* out_idx_dev,
+                        float* out_val_dev, void* stream);
+
+/* selected_count (sparsify.cpp:98-103): clamp(ceil((1 - ratio) * len), 1, len), 0 for len 0. */
+uint64_t xknn_dgc_selected_count(double sparsity_ratio, uint64_t len);
+
+/* CompressionState (sparsify.hpp:46-75) with the per-layer velocity and residual in HBM. */
+typedef struct xknn_dgc xknn_dgc_t;
+xknn_status_t xknn_dgc_create(double sparsity_ratio, float momentum, void* stream,
+                              xknn_dgc_t** out);
+xknn_status_t xknn_dgc_set_sparsity(xknn_dgc_t* h, double sparsity_ratio);
+/* compress_step (sparsify.cpp:120-161): velocity = momentum*velocity + grad, residual +=
+   velocity, emit the top selected_count(ratio, len) residual entries (indices strictly
+   increasing, u64) and zero residual and velocity there.  *count = entries written.  Errors:
+   InvalidArgument (empty gradient), ShapeMismatch (a layer's length changed).  Synchronizes. */
+xknn_status_t xknn_dgc_compress(xknn_dgc_t* h, uint32_t layer_id, const float* grad_dev,
+                                uint64_t len, uint64_t* out_idx_dev, float* out_val_dev,
+                                uint64_t* count);
+/* residual() / velocity() of a layer (zeros before its first compress_step), device copies. */
+xknn_status_t xknn_dgc_state(xknn_dgc_t* h, uint32_t layer_id, float* residual_dev,
+                             float* velocity_dev, uint64_t len);
+xknn_status_t xknn_dgc_destroy(xknn_dgc_t* h);
+
 /* Kernel launch counter (all kernels this library launched on this layer since creation). */
 uint64_t xknn_layer_kernel_launches(const xknn_layer_t* h);
 

@@ -20,6 +20,7 @@
 #include "xcls/matrix.hpp"
 #include "xcls/parallel.hpp"
 #include "xcls/softmax.hpp"
+#include "xcls/sparsify.hpp"
 
 using namespace xcls;
 
@@ -113,6 +114,49 @@ int ref_build_graph_ring(uint64_t n, uint64_t d, const float* w, uint64_t p, uin
     std::memcpy(out, g.flat.data(), n * k * sizeof(uint32_t));
   })
 }
+
+// topk_divide_conquer / CompressionState (sparsify.cpp)
+int ref_topk(uint64_t len, const float* t, uint64_t k, uint64_t m_chunks, uint64_t* out_idx,
+             float* out_val) {
+  GUARD({
+    auto r = topk_divide_conquer(std::span<const float>(t, len), k, m_chunks);
+    std::memcpy(out_idx, r.indices.data(), r.indices.size() * sizeof(uint64_t));
+    std::memcpy(out_val, r.values.data(), r.values.size() * sizeof(float));
+  })
+}
+
+void* ref_dgc_create(double ratio, float momentum) {
+  try {
+    return new CompressionState(ratio, momentum);
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int ref_dgc_step(void* h, uint32_t layer, uint64_t len, const float* g, uint64_t m_chunks,
+                 uint64_t* out_idx, float* out_val, uint64_t* count) {
+  GUARD({
+    auto s = static_cast<CompressionState*>(h)->compress_step(
+        layer, std::span<const float>(g, len), m_chunks);
+    std::memcpy(out_idx, s.indices.data(), s.indices.size() * sizeof(uint64_t));
+    std::memcpy(out_val, s.values.data(), s.values.size() * sizeof(float));
+    *count = s.indices.size();
+  })
+}
+
+int ref_dgc_set_sparsity(void* h, double r) {
+  GUARD({ static_cast<CompressionState*>(h)->set_sparsity_ratio(r); })
+}
+
+int ref_dgc_residual(void* h, uint32_t layer, uint64_t len, float* out) {
+  GUARD({
+    auto r = static_cast<CompressionState*>(h)->residual(layer);
+    if (r.size() != len) throw ShapeMismatch("residual length");
+    std::memcpy(out, r.data(), len * sizeof(float));
+  })
+}
+
+void ref_dgc_destroy(void* h) { delete static_cast<CompressionState*>(h); }
 
 // save_graph / load_graph (knn_graph.cpp:276-311).  load: *n and *k out; flat (>= n*k) may be
 // NULL to query the sizes only.

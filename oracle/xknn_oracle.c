@@ -713,3 +713,87 @@ out_w:
   free(lo);
   return rc;
 }
+
+/* ------------------------------------------------------------------------- */
+/* DGC sparsification (sparsify.cpp), beside the fc path                      */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  float v;
+  uint64_t i;
+} OrEntry;
+
+/* `precedes` (sparsify.cpp:19-24): |value| descending, index ascending */
+static int or_precedes_cmp(const void* a, const void* b) {
+  const OrEntry* x = (const OrEntry*)a;
+  const OrEntry* y = (const OrEntry*)b;
+  const float mx = fabsf(x->v), my = fabsf(y->v);
+  if (mx != my) return mx > my ? -1 : 1;
+  return x->i < y->i ? -1 : (x->i > y->i ? 1 : 0);
+}
+
+/* topk_divide_conquer (sparsify.cpp:41-80): exact top-k under `precedes`, in that order.  The
+   reference's chunked selection equals a full selection for every chunk count (its header,
+   sparsify.hpp:22-28), so this restates it as one sort. */
+int or_topk(uint64_t len, const float* t, uint64_t k, uint64_t* out_idx, float* out_val) {
+  if (k > len) return OR_ERR_K_TOO_LARGE;
+  if (k == 0) return OR_ERR_INVALID_ARGUMENT;
+  OrEntry* e = (OrEntry*)malloc(len * sizeof(OrEntry));
+  for (uint64_t i = 0; i < len; ++i) {
+    e[i].v = t[i];
+    e[i].i = i;
+  }
+  qsort(e, len, sizeof(OrEntry), or_precedes_cmp);
+  for (uint64_t j = 0; j < k; ++j) {
+    out_idx[j] = e[j].i;
+    out_val[j] = e[j].v;
+  }
+  free(e);
+  return OR_OK;
+}
+
+/* selected_count (sparsify.cpp:98-103) */
+uint64_t or_selected_count(double ratio, uint64_t len) {
+  if (len == 0) return 0;
+  const double keep = (1.0 - ratio) * (double)len;
+  uint64_t k = (uint64_t)ceil(keep);
+  if (k < 1) k = 1;
+  if (k > len) k = len;
+  return k;
+}
+
+static int or_u64_cmp(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* CompressionState::compress_step (sparsify.cpp:120-161) on one layer's state, in place:
+   velocity = momentum*velocity + grad; residual += velocity; emit the top selected_count
+   residual entries in increasing index order; zero residual and velocity there. */
+int or_dgc_step(uint64_t len, const float* g, float* vel, float* res, double ratio, float mom,
+                uint64_t* out_idx, float* out_val, uint64_t* count) {
+  if (len == 0) return OR_ERR_INVALID_ARGUMENT;
+  for (uint64_t i = 0; i < len; ++i) {
+    vel[i] = mom * vel[i] + g[i];
+    res[i] += vel[i];
+  }
+  const uint64_t k = or_selected_count(ratio, len);
+  uint64_t* idx = (uint64_t*)malloc(k * sizeof(uint64_t));
+  float* val = (float*)malloc(k * sizeof(float));
+  int rc = or_topk(len, res, k, idx, val);
+  if (rc == OR_OK) {
+    qsort(idx, k, sizeof(uint64_t), or_u64_cmp);
+    for (uint64_t j = 0; j < k; ++j) {
+      out_idx[j] = idx[j];
+      out_val[j] = res[idx[j]];
+    }
+    for (uint64_t j = 0; j < k; ++j) {
+      res[idx[j]] = 0.0f;
+      vel[idx[j]] = 0.0f;
+    }
+    *count = k;
+  }
+  free(idx);
+  free(val);
+  return rc;
+}

@@ -49,6 +49,10 @@ void or_sgd_step_rows(uint64_t cols, float* params, const float* grad_rows, floa
 int or_build_graph_bruteforce(uint64_t n, uint64_t d, const float* w, uint64_t k, uint32_t* out);
 int or_classify_retrieval(uint64_t nq, uint64_t n, uint64_t d, const float* q, const float* w,
                           uint32_t* out_class, float* out_score);
+int or_topk(uint64_t len, const float* t, uint64_t k, uint64_t* out_idx, float* out_val);
+uint64_t or_selected_count(double ratio, uint64_t len);
+int or_dgc_step(uint64_t len, const float* g, float* vel, float* res, double ratio, float mom,
+                uint64_t* out_idx, float* out_val, uint64_t* count);
 int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k, uint32_t* out);
 int or_fc_train_step(uint64_t n, uint64_t d, uint64_t p, float* w, float* velocity,
                      const float* x, const uint32_t* labels, uint64_t b,

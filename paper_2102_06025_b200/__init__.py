@@ -115,6 +115,12 @@ for _name, _args in {
                              C.POINTER(C.c_uint32)],
     "xknn_layer_get_graph": [VP, VP, VP, VP, U64, C.POINTER(U64), C.c_int],
     "xknn_layer_classify": [VP, VP, U64, VP, VP],
+    "xknn_topk": [VP, U64, U64, VP, VP, VP],
+    "xknn_dgc_create": [C.c_double, C.c_float, VP, C.POINTER(VP)],
+    "xknn_dgc_set_sparsity": [VP, C.c_double],
+    "xknn_dgc_compress": [VP, C.c_uint32, VP, U64, VP, VP, C.POINTER(U64)],
+    "xknn_dgc_state": [VP, C.c_uint32, VP, VP, U64],
+    "xknn_dgc_destroy": [VP],
 }.items():
     getattr(_lib, _name).argtypes = _args
     getattr(_lib, _name).restype = C.c_int
@@ -218,6 +224,80 @@ def load_graph_rows(path: str, num_classes: int, begin: int = 0, end: int | None
     _check(_lib.xknn_graph_load_rows(path.encode(), num_classes, begin, end, rows.ctypes.data,
                                      rows.size, 0, C.byref(k)))
     return k.value, rows
+
+
+_lib.xknn_dgc_selected_count.restype = U64
+_lib.xknn_dgc_selected_count.argtypes = [C.c_double, U64]
+
+
+def selected_count(sparsity_ratio: float, length: int) -> int:
+    """selected_count (sparsify.cpp:98-103)."""
+    return int(_lib.xknn_dgc_selected_count(sparsity_ratio, length))
+
+
+def topk(values, k: int):
+    """topk_divide_conquer (sparsify.cpp:41-80) on device: (indices int64, values) of the k
+    largest |values| (ties to the lower index) in selection order."""
+    import torch
+
+    t = values.contiguous()
+    idx = torch.empty(k, dtype=torch.int64, device=t.device)
+    val = torch.empty(k, dtype=torch.float32, device=t.device)
+    _check(_lib.xknn_topk(t.data_ptr(), t.numel(), k, idx.data_ptr(), val.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream))
+    return idx, val
+
+
+class CompressionState:
+    """CompressionState (sparsify.hpp:46-75): momentum-corrected top-k with residual
+    accumulation and factor masking, state in HBM."""
+
+    def __init__(self, sparsity_ratio: float, momentum: float):
+        import torch
+
+        self._torch = torch
+        h = VP()
+        _check(_lib.xknn_dgc_create(sparsity_ratio, momentum,
+                                    torch.cuda.current_stream().cuda_stream, C.byref(h)))
+        self.h = h.value
+        self._len = {}
+
+    def set_sparsity_ratio(self, r: float) -> None:
+        _check(_lib.xknn_dgc_set_sparsity(self.h, r))
+
+    def compress_step(self, layer_id: int, grad):
+        """-> (indices int64 increasing, values) of the emitted entries."""
+        torch = self._torch
+        g = grad.contiguous()
+        n = g.numel()
+        cap = max(n, 1)
+        idx = torch.empty(cap, dtype=torch.int64, device=g.device)
+        val = torch.empty(cap, dtype=torch.float32, device=g.device)
+        cnt = U64()
+        torch.cuda.current_stream().synchronize()
+        _check(_lib.xknn_dgc_compress(self.h, layer_id, g.data_ptr(), n, idx.data_ptr(),
+                                      val.data_ptr(), C.byref(cnt)))
+        self._len[layer_id] = n
+        return idx[: cnt.value], val[: cnt.value]
+
+    def state(self, layer_id: int, length: int):
+        """(residual, velocity) of a layer."""
+        torch = self._torch
+        r = torch.empty(length, dtype=torch.float32, device="cuda")
+        v = torch.empty(length, dtype=torch.float32, device="cuda")
+        _check(_lib.xknn_dgc_state(self.h, layer_id, r.data_ptr(), v.data_ptr(), length))
+        return r, v
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.xknn_dgc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _ptr(t) -> int:

@@ -78,6 +78,20 @@ def main():
     # an XKNN graph file written by the reference's save_graph (knn_graph.cpp:276-291)
     g = O.random_graph(50, 5, 31)
     assert O.ref_save_graph(os.path.join(HERE, "graph_small.xknn"), g) == 0
+    # DGC: topk_divide_conquer and three compress_step calls of the reference
+    rng = np.random.default_rng(11)
+    t = rng.standard_normal(3000).astype(np.float32)
+    t[rng.integers(0, 3000, 500)] = 0.25
+    rc, i, v = O.topk("ref", t, 100, 5)
+    assert rc == 0
+    grads = np.stack([rng.standard_normal(2000).astype(np.float32) for _ in range(3)])
+    dg, out = O.RefDgc(0.98, 0.9), {}
+    for s in range(3):
+        rc, ii, vv = dg.step(0, grads[s])
+        assert rc == 0
+        out[f"idx_{s}"], out[f"val_{s}"] = ii, vv
+    np.savez_compressed(os.path.join(HERE, "dgc.npz"), t=t, k=100, topk_idx=i, topk_val=v,
+                        ratio=0.98, momentum=0.9, grads=grads, **out)
 
 
 if __name__ == "__main__":

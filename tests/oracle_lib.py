@@ -322,3 +322,82 @@ def classify_retrieval(q: np.ndarray, w: np.ndarray):
     fn.argtypes = [U64, U64, U64, f32p, f32p, u32p, f32p]
     rc = fn(q.shape[0], w.shape[0], q.shape[1], q, w, out, sc)
     return rc, out, sc
+
+
+def topk(lib_kind: str, t: np.ndarray, k: int, m_chunks: int = 0):
+    """topk_divide_conquer: (rc, indices u64, values) from the oracle or the reference."""
+    t = np.ascontiguousarray(t, np.float32)
+    idx = np.zeros(max(k, 1), np.uint64)
+    val = np.zeros(max(k, 1), np.float32)
+    if lib_kind == "ref":
+        fn = ref().ref_topk
+        fn.restype = C.c_int
+        fn.argtypes = [U64, f32p, U64, U64, u64p, f32p]
+        rc = fn(t.size, t, k, m_chunks, idx, val)
+    else:
+        fn = oracle().or_topk
+        fn.restype = C.c_int
+        fn.argtypes = [U64, f32p, U64, u64p, f32p]
+        rc = fn(t.size, t, k, idx, val)
+    return rc, idx[:k], val[:k]
+
+
+class OracleDgc:
+    """CompressionState restated in oracle/ (or_dgc_step), one state per layer."""
+
+    def __init__(self, ratio: float, momentum: float):
+        self.ratio, self.momentum, self.state = ratio, momentum, {}
+
+    def step(self, layer: int, g: np.ndarray):
+        g = np.ascontiguousarray(g, np.float32)
+        vel, res = self.state.setdefault(layer, (np.zeros(g.size, np.float32),
+                                                 np.zeros(g.size, np.float32)))
+        idx = np.zeros(g.size, np.uint64)
+        val = np.zeros(g.size, np.float32)
+        cnt = U64()
+        fn = oracle().or_dgc_step
+        fn.restype = C.c_int
+        fn.argtypes = [U64, f32p, f32p, f32p, C.c_double, C.c_float, u64p, f32p, C.POINTER(U64)]
+        rc = fn(g.size, g, vel, res, self.ratio, self.momentum, idx, val, C.byref(cnt))
+        assert rc == 0
+        return idx[: cnt.value], val[: cnt.value]
+
+
+class RefDgc:
+    """The reference's CompressionState through oracle/_ref."""
+
+    def __init__(self, ratio: float, momentum: float):
+        lib = ref()
+        lib.ref_dgc_create.restype = C.c_void_p
+        lib.ref_dgc_create.argtypes = [C.c_double, C.c_float]
+        lib.ref_dgc_step.restype = C.c_int
+        lib.ref_dgc_step.argtypes = [C.c_void_p, C.c_uint32, U64, f32p, U64, u64p, f32p,
+                                     C.POINTER(U64)]
+        lib.ref_dgc_residual.restype = C.c_int
+        lib.ref_dgc_residual.argtypes = [C.c_void_p, C.c_uint32, U64, f32p]
+        lib.ref_dgc_set_sparsity.restype = C.c_int
+        lib.ref_dgc_set_sparsity.argtypes = [C.c_void_p, C.c_double]
+        lib.ref_dgc_destroy.argtypes = [C.c_void_p]
+        self.lib, self.h = lib, lib.ref_dgc_create(ratio, momentum)
+
+    def set_sparsity(self, r: float) -> int:
+        return self.lib.ref_dgc_set_sparsity(self.h, r)
+
+    def step(self, layer: int, g: np.ndarray, m_chunks: int = 0):
+        g = np.ascontiguousarray(g, np.float32)
+        idx = np.zeros(g.size, np.uint64)
+        val = np.zeros(g.size, np.float32)
+        cnt = U64()
+        rc = self.lib.ref_dgc_step(self.h, layer, g.size, g, m_chunks, idx, val, C.byref(cnt))
+        return rc, idx[: cnt.value], val[: cnt.value]
+
+    def residual(self, layer: int, n: int) -> np.ndarray:
+        out = np.zeros(n, np.float32)
+        assert self.lib.ref_dgc_residual(self.h, layer, n, out) == 0
+        return out
+
+    def __del__(self):
+        try:
+            self.lib.ref_dgc_destroy(self.h)
+        except Exception:
+            pass
