@@ -28,7 +28,7 @@ def _ngpus():
 def test_multi_gpu_step(p, m, precision, tol_loss, tol_g, tmp_path):
     if _ngpus() < p:
         pytest.skip(f"needs {p} GPUs")
-    n, b, k, steps = 40_000, 256, 10, 2
+    n, b, k, steps = 40_003, 256, 10, 2  # shards of unequal size (ShardLayout remainder)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + p + (m % 97)}",
            os.path.join(HERE, "mp_worker.py"), "--out", str(tmp_path), "--num-classes", str(n), "--batch",
