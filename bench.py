@@ -312,28 +312,39 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
     loss_v = float(loss.item())
 
     # ---- e2e: host buffers through the public API, copies inside the timed region ----
+    # A pipelined training loop: every step's features and labels are copied from pinned host
+    # memory on a copy stream (overlapping the previous step), the step runs on the layer
+    # stream, and every step's loss is copied back to pinned host memory; the loop is timed by
+    # the host wall clock until the last loss has arrived.
     hx = [bt[0].cpu().pin_memory() for bt in batches]
     hy = [bt[1].cpu().pin_memory() for bt in batches]
-    dx = torch.empty(b_local, D, device="cuda")
-    dy = torch.empty(b_local, dtype=torch.int32, device="cuda")
-    hloss = torch.zeros(1, dtype=torch.float64).pin_memory()
+    dxs = [torch.empty(b_local, D, device="cuda") for _ in range(2)]
+    dys = [torch.empty(b_local, dtype=torch.int32, device="cuda") for _ in range(2)]
+    hloss = torch.zeros(args.steps, dtype=torch.float64).pin_memory()
+    copy_stream = torch.cuda.Stream()
+    ev_copied = [torch.cuda.Event() for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]
     barrier()
     t0 = time.perf_counter()
-    e2e_ev0 = torch.cuda.Event(enable_timing=True)
-    e2e_ev1 = torch.cuda.Event(enable_timing=True)
-    e2e_ev0.record(stream)
-    with torch.cuda.stream(stream):
-        for i in range(args.steps):
-            dx.copy_(hx[i % len(hx)], non_blocking=True)
-            dy.copy_(hy[i % len(hy)], non_blocking=True)
-            layer.train_step(dx, dy, LR, grad_features_local=gfeat, loss_out=loss, sync=False)
-            hloss.copy_(loss, non_blocking=True)
-            stream.synchronize()  # the caller reads the step's loss
-    e2e_ev1.record(stream)
-    e2e_ev1.synchronize()
+    for i in range(args.steps):
+        s_ = i % 2
+        with torch.cuda.stream(copy_stream):
+            if i >= 2:
+                copy_stream.wait_event(ev_used[s_])  # step i-2 is done reading this buffer
+            dxs[s_].copy_(hx[i % len(hx)], non_blocking=True)
+            dys[s_].copy_(hy[i % len(hy)], non_blocking=True)
+            ev_copied[s_].record(copy_stream)
+        stream.wait_event(ev_copied[s_])
+        with torch.cuda.stream(stream):
+            layer.train_step(dxs[s_], dys[s_], LR, grad_features_local=gfeat, loss_out=loss,
+                             sync=False)
+            ev_used[s_].record(stream)
+            hloss[i].copy_(loss[0], non_blocking=True)  # the caller reads every step's loss
+    stream.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
-    e2e_ms = e2e_ev0.elapsed_time(e2e_ev1)
     layer.sync()
+    assert np.isfinite(hloss.numpy()).all()
 
     # ---- max over ranks ----
     if world > 1:
@@ -394,7 +405,10 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                        "l2": "per-step working set > 126 MB L2 (weight shard, P~ bf16)"},
             "e2e": {"value": round(b / (e2e_ms / args.steps / 1e3), 1), "unit": "samples/s",
                     "h2d_bytes_per_step": int(b_local * D * 4 + b_local * 4),
-                    "d2h_bytes_per_step": 8},
+                    "d2h_bytes_per_step": 8,
+                    "how": "host wall clock over a pipelined loop: per step H2D of the rank's "
+                           "features+labels from pinned memory on a copy stream, the step, D2H "
+                           "of its loss"},
             "gpu_launches": int(launches),
             "roofline": roof,
             "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4),
