@@ -695,8 +695,16 @@ __global__ void k_rowreduce(const SelState* st, const float* __restrict__ partia
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // row in block, tile group
   const uint32_t b = blockIdx.x * 32 + tx;
   double s = 0.0;
-  if (b < B)
-    for (uint32_t t = ty; t < nt; t += 32) s += (double)partial[(uint64_t)t * bpad + b];
+  if (b < B) {  // 4 independent loads in flight per thread (fixed order: deterministic)
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    uint32_t t = ty;
+    for (; t + 96 < nt; t += 128) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s4[j] += (double)partial[(uint64_t)(t + 32 * j) * bpad + b];
+    }
+    for (; t < nt; t += 32) s4[0] += (double)partial[(uint64_t)t * bpad + b];
+    s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
   part[ty][tx] = s;
   __syncthreads();
   if (ty == 0 && b < B) {
