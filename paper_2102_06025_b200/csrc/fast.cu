@@ -506,6 +506,13 @@ __global__ void __launch_bounds__(384, 1)
             float v[32];
             tc::tmem_ld32(tb + col, v);
             const uint32_t c0 = t * 256 + col;
+            // the common case late in the scan: nothing in the warp's 32x32 chunk beats its
+            // cut -- one max tree and a vote instead of 32 compares per lane
+            float mx = v[0];
+#pragma unroll
+            for (int j = 1; j < 31; j += 2) mx = fmaxf(mx, fmaxf(v[j], v[j + 1]));
+            mx = fmaxf(mx, v[31]);
+            if (!__any_sync(XKNN_FULL_MASK, vrow && mx > ctau)) continue;
             uint32_t mask = 0;  // columns of this chunk above the current cut
 #pragma unroll
             for (int j = 0; j < 32; ++j) mask |= (v[j] > ctau ? 1u : 0u) << j;
