@@ -73,6 +73,7 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   lab_bits = pool_bits + 2 * nwords;
   XK_CUDA(dalloc(&pos_of, nw));
   XK_CUDA(dalloc(&pool_list, nw));
+  XK_CUDA(dalloc(&pool_samp, nw / 64 + 2));
   XK_CUDA(dalloc(&active, mw_cap + 32));
   const uint64_t nblocks = (nwords + 255) / 256;
   XK_CUDA(dalloc(&blk_counts, 2 * (nblocks + 2)));
@@ -128,7 +129,7 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
 
 void Layer::free_all() {
   void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, pos_of,
-                  pool_list, active, blk_counts, mt_cache, pick_key, pick_val, pick_head,
+                  pool_list, pool_samp, active, blk_counts, mt_cache, pick_key, pick_val, pick_head,
                   pred, lw, labels_all, label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
                   Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
                   dXpart, loss_dev};

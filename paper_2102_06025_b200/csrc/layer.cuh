@@ -84,6 +84,7 @@ struct Layer {
   uint32_t* lab_bits = nullptr;
   uint64_t nwords = 0;
   uint32_t* pool_list = nullptr;      // sorted local pool (global ids), cap nw
+  uint32_t* pool_samp = nullptr;      // every 64th pool position p: (pool_list[p]-begin) - p
   uint32_t* pos_of = nullptr;         // local class -> position in `active` (valid if active)
   uint32_t* active = nullptr;         // sorted local active (global ids), cap mw_cap
   uint64_t mw_cap = 0;

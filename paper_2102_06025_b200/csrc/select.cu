@@ -36,7 +36,7 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
                             uint64_t begin, uint64_t nw, const uint32_t* __restrict__ kpc,
                             const uint64_t* __restrict__ off, const uint32_t* __restrict__ flat,
                             uint32_t* pool_bits, uint32_t* lab_bits, uint32_t* best, uint32_t* occ,
-                            SelState* st, unsigned long long* err, int reset) {
+                            SelState* st, unsigned long long* err, int track) {
   griddep_wait();
   griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
@@ -46,10 +46,10 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
   for (uint32_t i = warp; i < batch; i += nwarps) {
     const uint32_t y = labels[i];
     if (y >= n) {
-      if (lane == 0 && !reset) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
+      if (lane == 0) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
       continue;
     }
-    if (!reset && lane == 0 && y >= begin && y - begin < nw) {
+    if (lane == 0 && y >= begin && y - begin < nw) {
       const uint64_t lc = y - begin;
       const uint32_t bit = 1u << (lc & 31);
       if (!(atomicOr(&lab_bits[lc >> 5], bit) & bit)) ++newlab;
@@ -59,11 +59,8 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
     for (uint32_t r = lane; r < kk; r += 32) {
       const uint64_t lc = (uint64_t)flat[o + r] - begin;
       if (lc >= nw) continue;  // validated at set_graph time
-      if (reset) {
-        best[lc] = kNone;
-        occ[lc] = 0;
-      } else {
-        atomicOr(&pool_bits[lc >> 5], 1u << (lc & 31));
+      atomicOr(&pool_bits[lc >> 5], 1u << (lc & 31));
+      if (track) {  // candidate rank / occurrences: only the over-full branch ranks by them
         atomicMin(&best[lc], r);
         atomicAdd(&occ[lc], 1u);
       }
@@ -131,7 +128,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
                              uint64_t nwords, const uint32_t* __restrict__ blk_off,
                              uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
                              uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
-                             int rank) {
+                             int rank, uint32_t* __restrict__ samp) {
   griddep_wait();
   griddep_launch();
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
@@ -147,6 +144,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
     const uint32_t lc = (uint32_t)(w * 32 + bit);
     out[pos] = base + lc;
     if (pos_of) pos_of[lc] = pos;
+    if (samp && (pos & 63) == 0) samp[pos >> 6] = lc - pos;  // g(pos) for k_pad_map
     ++pos;
     word &= word - 1;
   }
@@ -285,7 +283,8 @@ __global__ void k_resolve(const SelState* st, const uint32_t* __restrict__ key,
 // out[i] = C0[src(i)]; the shard owning complement position src marks the class
 __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
                           const uint32_t* __restrict__ pred, const uint32_t* __restrict__ lw,
-                          const uint32_t* __restrict__ pool_list, uint64_t begin,
+                          const uint32_t* __restrict__ pool_list,
+                          const uint32_t* __restrict__ samp, uint64_t begin,
                           uint32_t* act_bits, uint32_t* head) {
   griddep_wait();
   griddep_launch();
@@ -305,7 +304,16 @@ __global__ void k_pad_map(const SelState* st, const uint32_t* __restrict__ key,
     }
     if (src < cbase || src >= cbase + cl) continue;
     const uint64_t q = src - cbase;  // q-th class of [begin,end) outside the pool
-    uint32_t lo = 0, hi = npool;
+    // first pool position p with g(p) = (pool_list[p] - begin) - p > q: over the every-64th
+    // samples of g (small, cache-resident), then within one 64-entry stretch of pool_list
+    const uint32_t nsamp = (npool + 63) / 64;
+    uint32_t lo = 0, hi = nsamp;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((uint64_t)samp[mid] <= q) lo = mid + 1; else hi = mid;
+    }
+    hi = min(lo * 64, npool);
+    lo = lo ? (lo - 1) * 64 : 0;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       if ((uint64_t)(pool_list[mid] - begin) - mid <= q) lo = mid + 1; else hi = mid;
@@ -444,10 +452,10 @@ __global__ void k_label_cols(const SelState* st, const uint32_t* __restrict__ la
                              uint32_t batch, const uint32_t* __restrict__ active,
                              const uint32_t* __restrict__ pos_of, uint64_t begin, uint64_t end,
                              int32_t* label_col, const uint32_t* __restrict__ pool_list,
-                             uint32_t* best, uint32_t* occ) {
+                             uint32_t* best, uint32_t* occ, int track) {
   griddep_wait();
   griddep_launch();
-  const uint32_t na = st->active_count, np = st->pool_count;
+  const uint32_t na = st->active_count, np = track ? st->pool_count : 0;
   // reset the candidate ranks of this step's pool (every touched class is in the pool)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
     const uint32_t lc = pool_list[i] - (uint32_t)begin;
@@ -487,7 +495,8 @@ static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* p
   ++L.launches;
   launch_pdl(k_bits_write, nblocks, kCompactBlock, 0, L.stream, 
       mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
-      nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank);
+      nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank,
+      mode == 0 ? L.pool_samp : nullptr);
   ++L.launches;
   return L.cuda_ok(cudaGetLastError(), __FILE__, __LINE__, "k_bits_write");
 }
@@ -503,9 +512,12 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
 
   // (1) pool of this shard: union of its slices for every batch label (knn_softmax.cpp:122-132),
   //     candidate best rank / occurrences, and the labels this shard owns
+  // the over-full ranking (and its per-candidate rank/occurrence tracking) is only reachable
+  // when the pool can exceed M; the default M = 10% N never lets it
+  const bool overfull_possible = (uint64_t)B * g_kmax > m;
   launch_pdl(k_mark_pool, grid_for((uint64_t)B * 32, 256), 256, 0, stream, 
       labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
-      st, err, 0);
+      st, err, overfull_possible ? 1 : 0);
   XK_LAUNCH();
   // (2) sorted local pool; [pool size, distinct labels] exchanged between shards
   XK_TRY(compact_bits(*this, 0, pool_list, nullptr));
@@ -524,12 +536,11 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
     XK_LAUNCH();
     launch_pdl(k_resolve, grid_for(m, 256), 256, 0, stream, st, pick_key, pick_head, pick_val, pred, lw);
     XK_LAUNCH();
-    launch_pdl(k_pad_map, grid_for(m, 256), 256, 0, stream, st, pick_key, pred, lw, pool_list, begin,
-                                                     act_bits, pick_head);
+    launch_pdl(k_pad_map, grid_for(m, 256), 256, 0, stream, st, pick_key, pred, lw, pool_list,
+               pool_samp, begin, act_bits, pick_head);
     XK_LAUNCH();
   }
   // (3b) over-full branch: only reachable when B * k could exceed M
-  const bool overfull_possible = (uint64_t)B * g_kmax > m;
   if (overfull_possible) {
     const uint32_t nb_rank = g_kmax ? g_kmax : 1;
     const uint32_t nb_occ = B + 1;
@@ -559,8 +570,10 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
   }
   // (4) this shard's ActiveSet slice, sorted by construction; label -> column map
   XK_TRY(compact_bits(*this, 1, active, pos_of));
-  launch_pdl(k_label_cols, grid_for(std::max<uint64_t>(B, (uint64_t)B * g_kmax), 256), 256, 0, stream, 
-      st, labels_all, B, active, pos_of, begin, end, label_col, pool_list, sel_best, sel_occ);
+  launch_pdl(k_label_cols,
+             grid_for(overfull_possible ? std::max<uint64_t>(B, (uint64_t)B * g_kmax) : B, 256),
+             256, 0, stream, st, labels_all, B, active, pos_of, begin, end, label_col, pool_list,
+             sel_best, sel_occ, overfull_possible ? 1 : 0);
   XK_LAUNCH();
   return XKNN_OK;
 }
