@@ -587,18 +587,15 @@ __global__ void __launch_bounds__(384, 1)
           const float k2 = a.scale * 1.4426950408889634f;
           float sum = 0.f, lab = 0.f;
           bool has = false;
-#pragma unroll 1
-          for (uint32_t ch = 0; ch < 4; ++ch) {
+          auto process = [&](const uint32_t (&r)[32], uint32_t ch) {
             const uint32_t col = h * 128 + ch * 32;
-            float v[32];
-            tc::tmem_ld32(tb + col, v);
             const uint32_t c0 = ct * 256 + col;
             uint32_t pk[16];
             if (vrow && c0 + 32 <= mw) {  // interior chunk: 1 FFMA + 1 MUFU.EX2 + 1 FADD each
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
-                const float e0 = ex2_approx(fmaf(v[j], k2, -k2));
-                const float e1 = ex2_approx(fmaf(v[j + 1], k2, -k2));
+                const float e0 = ex2_approx(fmaf(__uint_as_float(r[j]), k2, -k2));
+                const float e1 = ex2_approx(fmaf(__uint_as_float(r[j + 1]), k2, -k2));
                 sum += e0;
                 sum += e1;
                 pk[j / 2] = pack_bf16(e0, e1);
@@ -607,8 +604,9 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
                 const bool ok0 = vrow && c0 + j < mw, ok1 = vrow && c0 + j + 1 < mw;
-                const float e0 = ok0 ? ex2_approx(fmaf(v[j], k2, -k2)) : 0.f;
-                const float e1 = ok1 ? ex2_approx(fmaf(v[j + 1], k2, -k2)) : 0.f;
+                const float e0 = ok0 ? ex2_approx(fmaf(__uint_as_float(r[j]), k2, -k2)) : 0.f;
+                const float e1 =
+                    ok1 ? ex2_approx(fmaf(__uint_as_float(r[j + 1]), k2, -k2)) : 0.f;
                 sum += e0;
                 sum += e1;
                 pk[j / 2] = pack_bf16(e0, e1);
@@ -618,17 +616,32 @@ __global__ void __launch_bounds__(384, 1)
               const int32_t idx = lc - (int32_t)c0;
               float sel = 0.f;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) sel = (j == idx) ? v[j] : sel;
+              for (int j = 0; j < 32; ++j) sel = (j == idx) ? __uint_as_float(r[j]) : sel;
               lab = sel * a.scale;
               has = true;
             }
             stage_bf16(stg, lane, pk);
             __syncwarp();
             store_bf16_block(stg, a.Pt + (uint64_t)grow0 * a.ldp + c0, a.ldp, lane);
-          }
+          };
+          // the next chunk's TMEM load is in flight while this one is exponentiated and
+          // stored; TMEM is released as soon as the last chunk is in registers
+          uint32_t ra[32], rb[32];
+          tc::tmem_ld32_issue(tb + h * 128, ra);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 32, rb);
+          process(ra, 0);
+          tc::tmem_ld_wait(rb);
+          tc::tmem_ld32_issue(tb + h * 128 + 64, ra);
+          process(rb, 1);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 96, rb);
+          process(ra, 2);
+          tc::tmem_ld_wait(rb);
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], lead);
+          process(rb, 3);
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
         } else {
