@@ -44,6 +44,7 @@ namespace {
 // 2 * 2^-11 (+ subnormal terms 2e-6), fp32 accumulation of 512 products (512 * 2^-23), the
 // reference's own sequential fp32 sum (512 * 2^-24 + 2^-24); 1.07e-3 in total, with margin:
 constexpr float kEps = 0.00125f;
+constexpr size_t kRescoreSmem = 8 * (512 + 32 * 33) * sizeof(float);  // 8 warps per block
 
 __global__ void k_to_f16(const float* __restrict__ w, uint64_t n, uint64_t npad, uint32_t d,
                          __half* __restrict__ out) {
@@ -154,16 +155,51 @@ __global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
                           const uint32_t* __restrict__ flag, uint32_t kp,
                           const float* __restrict__ held, uint32_t cb, uint32_t nc,
                           float* __restrict__ ex) {
-  const uint32_t lane = threadIdx.x & 31;
+  // D = 512.  Lane l carries candidate l of a group of 32 through the reference's sequential
+  // sum; the 32 candidate rows stream through shared memory in 128-B column chunks loaded by
+  // the whole warp (four row segments per instruction) instead of 32 scattered row walks.
+  extern __shared__ float rs_smem[];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* qrow = rs_smem + (uint64_t)w * (512 + 32 * 33);  // the own row
+  float* stg = qrow + 512;                                // 32 rows x 32 floats (+1 pad)
   for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
        j += (gridDim.x * blockDim.x) >> 5) {
     if (flag[j]) continue;
     const uint32_t m = lcnt[j];
     const float2* L = list + (uint64_t)j * kp;
-    for (uint32_t e = lane; e < m; e += 32) {
-      const uint32_t id = __float_as_uint(L[e].y);
-      if (id - cb < nc)
-        ex[(uint64_t)j * kp + e] = exact_dot(own + (uint64_t)j * d, held + (uint64_t)(id - cb) * d, d);
+    __syncwarp();
+    for (uint32_t c = lane; c < 128; c += 32)
+      reinterpret_cast<float4*>(qrow)[c] = reinterpret_cast<const float4*>(own + (uint64_t)j * 512)[c];
+    for (uint32_t base = 0; base < m; base += 32) {
+      const uint32_t e = base + lane;
+      const uint32_t id = e < m ? __float_as_uint(L[e].y) : 0xffffffffu;
+      const bool mine = e < m && id - cb < nc;
+      const uint32_t act = __ballot_sync(XKNN_FULL_MASK, mine);
+      if (!act) continue;
+      const uint64_t rbase = mine ? (uint64_t)(id - cb) * 512 : 0;
+      float acc = 0.0f;
+      for (uint32_t c = 0; c < 16; ++c) {  // 32-column chunk c of every candidate row
+        __syncwarp();
+#pragma unroll
+        for (uint32_t i = 0; i < 8; ++i) {
+          const uint32_t r = 4 * i + (lane >> 3);  // row (candidate lane) of this load
+          const uint64_t rb = __shfl_sync(XKNN_FULL_MASK, rbase, r);
+          const bool on = (act >> r) & 1u;
+          const float4 v = on ? reinterpret_cast<const float4*>(held + rb + c * 32)[lane & 7]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          float* dst = stg + r * 33 + (lane & 7) * 4;
+          dst[0] = v.x;
+          dst[1] = v.y;
+          dst[2] = v.z;
+          dst[3] = v.w;
+        }
+        __syncwarp();
+        const float* mine_row = stg + lane * 33;
+        const float* q = qrow + c * 32;
+#pragma unroll
+        for (uint32_t t = 0; t < 32; ++t) acc = __fadd_rn(acc, __fmul_rn(q[t], mine_row[t]));
+      }
+      if (mine) ex[(uint64_t)j * kp + e] = acc;
     }
   }
 }
@@ -582,7 +618,9 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
       G_CUDA(new_event(&ev_recv));
       G_CUDA(cudaEventRecord(ev_recv, cs));
     }
-    k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(wn, n, 512, list, lcnt, flag, kp,
+    G_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kRescoreSmem));
+    k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, kRescoreSmem, s>>>(wn, n, 512, list, lcnt, flag, kp,
                                                               held32, (uint32_t)cb, nc, ex);
     G_CUDA(cudaGetLastError());
     for (uint32_t u = 0; u < nu; ++u) {  // rows without a certificate: exact scan of the block
@@ -685,7 +723,9 @@ xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn
     G_CUDA(cudaGetLastError());
     G_CUDA(cudaMemcpyAsync(&nu, unc, 4, cudaMemcpyDeviceToHost, s));
     G_CUDA(cudaStreamSynchronize(s));
-    k_rescore<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(qn, nq, 512, list, lcnt, flag, kp,
+    G_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kRescoreSmem));
+    k_rescore<<<grid_for((uint64_t)nq * 32, 256), 256, kRescoreSmem, s>>>(qn, nq, 512, list, lcnt, flag, kp,
                                                                wn, col_base, nw, ex);
     G_CUDA(cudaGetLastError());
   } else {  // exact scans for every query

@@ -14,6 +14,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("XKNN_PKG_DIR"):  # A/B runs against another build of the package
+    sys.path.insert(0, os.environ["XKNN_PKG_DIR"])
 import torch  # noqa: E402
 
 import paper_2102_06025_b200 as X  # noqa: E402
@@ -49,13 +51,17 @@ X.graph_ring(ws, ws.shape[0] * world if world > 1 else ws.shape[0], 8, 16, rank,
 torch.cuda.synchronize()
 if world > 1:
     dist.barrier()
-t0 = time.perf_counter()
-ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ev0.record()
-out, unc, steps = X.graph_ring(w, a.classes, a.k, a.kprime, rank, world, comm)
-ev1.record()
-ev1.synchronize()
-sec = ev0.elapsed_time(ev1) / 1e3
+# two full-size builds; the second is timed (the first pays the allocator's first touches)
+for rep in range(2):
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    out, unc, steps = X.graph_ring(w, a.classes, a.k, a.kprime, rank, world, comm)
+    ev1.record()
+    ev1.synchronize()
+    sec = ev0.elapsed_time(ev1) / 1e3
+    del out
 if world > 1:
     t = torch.tensor([sec, float(unc)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
