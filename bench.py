@@ -255,11 +255,21 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def step(i):
-        x, y = batches[i % len(batches)]
+    # every step hands the next batch's labels to xknn_prepare right after it is enqueued, so
+    # the next selection overlaps this step's tail (a training loop knows its next batch)
+    nb = len(batches)
+    it = {"i": 0}
+
+    def step(_i=None):
+        i = it["i"]
+        it["i"] = i + 1
+        x, y = batches[i % nb]
         with torch.cuda.stream(stream):
             layer.train_step(x, y, LR, grad_features_local=gfeat, loss_out=loss, sync=False)
+            layer.prepare(batches[(i + 1) % nb][1])
 
+    with torch.cuda.stream(stream):
+        layer.prepare(batches[0][1])
     for i in range(args.warmup):
         step(i)
     layer.sync()
@@ -324,22 +334,32 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
     copy_stream = torch.cuda.Stream()
     ev_copied = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
-    barrier()
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        s_ = i % 2
+    i0 = it["i"]  # the pending prepare holds batch i0's labels
+
+    def copy_in(j):
+        s_, i = j % 2, i0 + j
         with torch.cuda.stream(copy_stream):
-            if i >= 2:
-                copy_stream.wait_event(ev_used[s_])  # step i-2 is done reading this buffer
+            if j >= 2:
+                copy_stream.wait_event(ev_used[s_])  # step j-2 is done reading this buffer
             dxs[s_].copy_(hx[i % len(hx)], non_blocking=True)
             dys[s_].copy_(hy[i % len(hy)], non_blocking=True)
             ev_copied[s_].record(copy_stream)
+
+    barrier()
+    t0 = time.perf_counter()
+    copy_in(0)
+    for j in range(args.steps):
+        s_ = j % 2
         stream.wait_event(ev_copied[s_])
         with torch.cuda.stream(stream):
             layer.train_step(dxs[s_], dys[s_], LR, grad_features_local=gfeat, loss_out=loss,
                              sync=False)
             ev_used[s_].record(stream)
-            hloss[i].copy_(loss[0], non_blocking=True)  # the caller reads every step's loss
+            hloss[j].copy_(loss[0], non_blocking=True)  # the caller reads every step's loss
+        if j + 1 < args.steps:
+            copy_in(j + 1)
+            with torch.cuda.stream(stream):
+                layer.prepare(dys[(j + 1) % 2], ready_stream=copy_stream)
     stream.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
@@ -407,8 +427,9 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                     "h2d_bytes_per_step": int(b_local * D * 4 + b_local * 4),
                     "d2h_bytes_per_step": 8,
                     "how": "host wall clock over a pipelined loop: per step H2D of the rank's "
-                           "features+labels from pinned memory on a copy stream, the step, D2H "
-                           "of its loss"},
+                           "features+labels from pinned memory on a copy stream, the next step's "
+                           "selection prepared as soon as its labels land, the step, D2H of its "
+                           "loss"},
             "gpu_launches": int(launches),
             "roofline": roof,
             "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4),

@@ -141,6 +141,16 @@ xknn_status_t xknn_step(xknn_layer_t* h, const float* features_local_dev,
                         const uint32_t* labels_local_dev, uint64_t batch_local, float lr,
                         double* loss_dev, float* grad_features_local_dev);
 
+/* Pipelined selection: starts the NEXT step's label all-gather and active-class selection on
+   the layer's side stream now, so that it overlaps the step still in flight (its GEMMs and the
+   HBM-bound row update) -- selection depends only on the labels and the graph.  The next
+   xknn_step with the same batch size uses the result and skips its own selection; its
+   labels_local must hold the labels given here.  ready_stream (may be NULL): the stream on which
+   labels_local becomes valid (its current work is waited for); NULL = already valid.
+   Collective when world > 1 (uses a communicator split from the layer's). */
+xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local_dev,
+                           uint64_t batch_local, void* ready_stream);
+
 /* Synchronizes the layer stream, returns the first device-side error of the preceding
    asynchronous calls (label range, ZeroNormRow, MTooSmall, ...) and clears it. */
 xknn_status_t xknn_layer_sync(xknn_layer_t* h);

@@ -102,6 +102,7 @@ for _name, _args in {
     "xknn_layer_set_graph_csr": [VP, VP, VP, VP, U64, C.c_int],
     "xknn_select": [VP, VP, U64, VP, C.POINTER(U64), C.POINTER(C.c_int)],
     "xknn_step": [VP, VP, VP, U64, C.c_float, VP, VP],
+    "xknn_prepare": [VP, VP, U64, VP],
     "xknn_layer_sync": [VP],
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_last_logits": [VP, VP, U64],
@@ -457,6 +458,16 @@ class KnnSoftmaxLayer:
                                 C.byref(ca)))
         self._leave()
         return out[: cnt.value].clone(), bool(ca.value)
+
+    def prepare(self, labels_local, ready_stream=None) -> None:
+        """Start the next train_step's selection now, overlapping the step in flight (the next
+        train_step must get the same labels).  ready_stream: the torch stream on which
+        labels_local becomes valid (None: it already is)."""
+        torch = self._torch
+        lab = labels_local if labels_local.dtype == torch.int32 else labels_local.to(torch.int32)
+        self._prep_keep = lab  # the buffer must outlive the asynchronous all-gather / copy
+        _check(_lib.xknn_prepare(self.h, lab.data_ptr(), lab.numel(),
+                                 ready_stream.cuda_stream if ready_stream is not None else None))
 
     def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
                    loss_out=None, sync: bool = True):

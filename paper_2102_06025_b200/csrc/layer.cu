@@ -74,7 +74,13 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(dalloc(&pos_of, nw));
   XK_CUDA(dalloc(&pool_list, nw));
   XK_CUDA(dalloc(&pool_samp, nw / 64 + 2));
-  XK_CUDA(dalloc(&active, mw_cap + 32));
+  for (int q = 0; q < 2; ++q) {
+    XK_CUDA(dalloc(&ss[q].active, mw_cap + 32));
+    XK_CUDA(dalloc(&ss[q].st, 1));
+    XK_CUDA(cudaMemsetAsync(ss[q].st, 0, sizeof(SelState), stream));
+    XK_CUDA(dalloc(&ss[q].label_col, bmax));
+  }
+  use_set(0);
   const uint64_t nblocks = (nwords + 255) / 256;
   XK_CUDA(dalloc(&blk_counts, 2 * (nblocks + 2)));
   XK_CUDA(cudaMemsetAsync(blk_counts, 0, 2 * (nblocks + 2) * sizeof(uint32_t), stream));
@@ -86,11 +92,8 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(dalloc(&pred, m));
   XK_CUDA(dalloc(&lw, m));
   XK_CUDA(dalloc(&labels_all, bmax));
-  XK_CUDA(dalloc(&label_col, bmax));
   XK_CUDA(dalloc(&pool_counts, 2 * world));
   XK_CUDA(dalloc(&tie_counts, world));
-  XK_CUDA(dalloc(&st, 1));
-  XK_CUDA(cudaMemsetAsync(st, 0, sizeof(SelState), stream));
   XK_CUDA(dalloc(&err, 1));
   XK_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned long long), stream));
   XK_CUDA(dalloc(&loss_dev, 1));
@@ -100,6 +103,9 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   XK_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
   XK_CUDA(cudaEventCreateWithFlags(&ev_feat, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_sel_done, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_prep, cudaEventDisableTiming));
+  XK_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
 
   // cub temp: max over the sorts/scans/selects we run
   size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
@@ -129,16 +135,23 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
 
 void Layer::free_all() {
   void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, pos_of,
-                  pool_list, pool_samp, active, blk_counts, mt_cache, pick_key, pick_val, pick_head,
-                  pred, lw, labels_all, label_col, pool_counts, tie_counts, hist, cub_tmp, st, err, X, Xhat, Xhat16,
+                  pool_list, pool_samp, blk_counts, mt_cache, pick_key, pick_val, pick_head,
+                  pred, lw, labels_all, pool_counts, tie_counts, hist, cub_tmp, err, X, Xhat, Xhat16,
                   Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
                   dXpart, loss_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto e : prof_ev) cudaEventDestroy(e);
   prof_ev.clear();
-  if (graph_exec) cudaGraphExecDestroy(graph_exec);
-  graph_exec = nullptr;
+  drop_graphs();
+  for (auto& q : ss) {
+    void* pp[] = {q.st, q.active, q.label_col};
+    for (void* p : pp)
+      if (p) cudaFree(p);
+    q = SelSet{};
+  }
+  for (cudaEvent_t e : {ev_sel_done, ev_prep, ev_ready})
+    if (e) cudaEventDestroy(e);
   if (lr_dev) cudaFree(lr_dev);
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -222,8 +235,12 @@ void Layer::prof_collect(bool all) {
 xknn_status_t Layer::run_core(uint64_t B) {
   const uint32_t D = (uint32_t)d;
   const uint64_t bl = B / world;
-  // (1) Algorithm 1 selection -> this shard's sorted active rows
-  XK_TRY(run_selection(B));
+  // (1) Algorithm 1 selection -> this shard's sorted active rows (or xknn_prepare's result)
+  if (core_prepared)
+    XK_TRY(wait_external(ev_prep, stream));
+  else
+    XK_TRY(run_selection(B));
+  XK_TRY(record_external(ev_sel_done, stream));  // the next prepare may reuse the scratch
   mark(2);
   unsigned int* cnt = &st->active_count;
   // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
@@ -295,9 +312,11 @@ xknn_status_t Layer::wait_features() {
 }
 
 xknn_status_t Layer::ensure_graph(uint64_t B) {
-  if (graph_exec && graph_b == B && graph_prof == prof_on) return XKNN_OK;
-  if (graph_exec) cudaGraphExecDestroy(graph_exec);
-  graph_exec = nullptr;
+  const int p = par, q = core_prepared ? 1 : 0;
+  cudaGraphExec_t& gx = core_graph[p][q];
+  if (gx && core_graph_b[p][q] == B && core_graph_prof[p][q] == prof_on) return XKNN_OK;
+  if (gx) cudaGraphExecDestroy(gx);
+  gx = nullptr;
   XK_TRY(ensure_mt_cache());
   const uint64_t l0 = launches;
   cudaGraph_t g = nullptr;
@@ -309,13 +328,113 @@ xknn_status_t Layer::ensure_graph(uint64_t B) {
     return s;
   }
   XK_CUDA(e);
-  e = cudaGraphInstantiate(&graph_exec, g, 0);
+  e = cudaGraphInstantiate(&gx, g, 0);
   cudaGraphDestroy(g);
   XK_CUDA(e);
-  graph_b = B;
-  graph_prof = prof_on;
-  graph_launches = launches - l0;
+  core_graph_b[p][q] = B;
+  core_graph_prof[p][q] = prof_on;
+  core_graph_launches[p][q] = launches - l0;
   launches = l0;
+  return XKNN_OK;
+}
+
+void Layer::drop_graphs() {
+  for (auto& row : core_graph)
+    for (auto& g : row) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  for (auto& g : sel_graph) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
+
+void Layer::use_set(int p) {
+  st = ss[p].st;
+  active = ss[p].active;
+  label_col = ss[p].label_col;
+}
+
+// an event record / wait that becomes an external event node when `on` is being captured
+xknn_status_t Layer::record_external(cudaEvent_t ev, cudaStream_t on) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  XK_CUDA(cudaStreamIsCapturing(on, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    XK_CUDA(cudaEventRecordWithFlags(ev, on, cudaEventRecordExternal));
+  else
+    XK_CUDA(cudaEventRecord(ev, on));
+  return XKNN_OK;
+}
+xknn_status_t Layer::wait_external(cudaEvent_t ev, cudaStream_t on) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  XK_CUDA(cudaStreamIsCapturing(on, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    XK_CUDA(cudaStreamWaitEvent(on, ev, cudaEventWaitExternal));
+  else
+    XK_CUDA(cudaStreamWaitEvent(on, ev, 0));
+  return XKNN_OK;
+}
+
+// xknn_prepare: the next step's label all-gather and selection on the side stream, into the
+// selection set that step will use, after the last step's selection released the scratch.
+xknn_status_t Layer::run_prepare(const uint32_t* labels_local, uint64_t bl, cudaStream_t ready) {
+  const uint64_t B = bl * world;
+  if (prepared) XK_CUDA(cudaStreamWaitEvent(stream, ev_prep, 0));  // superseded: keep order
+  if (world > 1 && !comm_ag) XK_NCCL(ncclCommSplit(comm, 0, rank, &comm_ag, nullptr));
+  XK_TRY(ensure_mt_cache());
+  use_set(par);
+  if (ready) {
+    XK_CUDA(cudaEventRecord(ev_ready, ready));
+    XK_CUDA(cudaStreamWaitEvent(side, ev_ready, 0));
+  }
+  XK_CUDA(cudaStreamWaitEvent(side, ev_sel_done, 0));
+  if (world > 1)
+    XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm_ag, side));
+  else
+    XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, side));
+  // the selection itself, on the side stream and the split communicator (the layer stream and
+  // its communicator may be busy with the previous step), captured once per set and batch size
+  cudaStream_t s0 = stream;
+  ncclComm_t c0 = comm;
+  stream = side;
+  comm = world > 1 ? comm_ag : comm;
+  xknn_status_t st_ = XKNN_OK;
+  const bool use_graph = graph_mode || (!(cfg.flags & XKNN_FLAG_NO_GRAPH) && s0 != nullptr);
+  if (use_graph) {
+    cudaGraphExec_t& gx = sel_graph[par];
+    if (!gx || sel_graph_b[par] != B) {
+      if (gx) cudaGraphExecDestroy(gx);
+      gx = nullptr;
+      const uint64_t l0 = launches;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(side, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        st_ = run_selection(B);
+        e = cudaStreamEndCapture(side, &g);
+        if (st_ == XKNN_OK && e == cudaSuccess) e = cudaGraphInstantiate(&gx, g, 0);
+        if (g) cudaGraphDestroy(g);
+      }
+      if (st_ == XKNN_OK && e != cudaSuccess) st_ = cuda_ok(e, __FILE__, __LINE__, "prepare");
+      sel_graph_b[par] = B;
+      sel_graph_launches[par] = launches - l0;
+      launches = l0;
+    }
+    if (st_ == XKNN_OK) {
+      cudaError_t e = cudaGraphLaunch(gx, side);
+      if (e != cudaSuccess) st_ = cuda_ok(e, __FILE__, __LINE__, "prepare launch");
+      launches += sel_graph_launches[par];
+    }
+  } else {
+    st_ = run_selection(B);
+  }
+  stream = s0;
+  comm = c0;
+  XK_TRY(st_);
+  XK_CUDA(cudaEventRecord(ev_prep, side));
+  prepared = true;
+  prepared_b = B;
   return XKNN_OK;
 }
 
@@ -327,21 +446,30 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   graph_mode = !(cfg.flags & XKNN_FLAG_NO_GRAPH) && stream != nullptr;
   if (prof_on) prof_collect(false);
   mark(0);
+  // this step's selection set; a prepared selection (xknn_prepare) for this batch size is used
+  // instead of selecting again (its labels are the caller's promise)
+  const int p = par;
+  use_set(p);
+  core_prepared = prepared && prepared_b == B;
+  if (prepared && !core_prepared) XK_CUDA(cudaStreamWaitEvent(stream, ev_prep, 0));
+  prepared = false;
   // (2) feature and label all-gather, rank-major (parallel.cpp:447-453, :544).  The labels go
   //     first on the layer stream (selection needs them); the features travel on the side
   //     stream over a split communicator while the selection runs, and the core waits for them
   //     right before the first kernel that reads X.
   if (world > 1) {
     if (!comm_ag) XK_NCCL(ncclCommSplit(comm, 0, rank, &comm_ag, nullptr));  // collective
-    XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
+    if (!core_prepared)
+      XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
     XK_CUDA(cudaEventRecord(ev_in, stream));
     XK_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
     XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm_ag, side));
     XK_CUDA(cudaEventRecord(ev_feat, side));
   } else {
     XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
-    XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
-                            stream));
+    if (!core_prepared)
+      XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, stream));
   }
   // the learning rate travels through device memory so the captured core stays valid
   launch_pdl(k_set_f32, 1, 1, 0, stream, lr_dev, lr);
@@ -349,11 +477,14 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   mark(1);
   if (graph_mode) {
     XK_TRY(ensure_graph(B));
-    XK_CUDA(cudaGraphLaunch(graph_exec, stream));
-    launches += graph_launches;
+    const int q = core_prepared ? 1 : 0;
+    XK_CUDA(cudaGraphLaunch(core_graph[p][q], stream));
+    launches += core_graph_launches[p][q];
   } else {
     XK_TRY(run_core(B));
   }
+  last_par = p;
+  par = 1 - p;
   // (6) feature normalize-backward on this rank's rows (parallel.cpp:574-585)
   if (gfeat_local) {
     XK_CUDA(launch_feature_backward(X + (uint64_t)rank * bl * d, xnorm + (uint64_t)rank * bl, dX,
@@ -493,8 +624,7 @@ xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg) {
   L.cfg.weight_decay = cfg->weight_decay;
   L.cfg.rng_seed = cfg->rng_seed;
   L.cfg.flags = cfg->flags;
-  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);
-  L.graph_exec = nullptr;
+  L.drop_graphs();
   return XKNN_OK;
 }
 
@@ -567,8 +697,7 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   L.g_off = nullptr;
   L.g_flat = nullptr;
   L.has_graph = false;
-  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);  // graph buffers are baked into the graph
-  L.graph_exec = nullptr;
+  L.drop_graphs();  // graph buffers are baked into the graphs
   XK_CUDA_H(xknn::dalloc(&L.g_kpc, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_off, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_flat, flat_len));
@@ -620,6 +749,11 @@ xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t 
   Layer& L = h->L;
   if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "knn mode without shard graphs");
   if (batch == 0 || batch > L.bmax) return fail(XKNN_ERR_INVALID_ARGUMENT, "batch outside (0, max_batch]");
+  if (L.prepared) {  // a pending prepared selection is superseded
+    XK_CUDA_H(cudaStreamWaitEvent(L.stream, L.ev_prep, 0));
+    L.prepared = false;
+  }
+  L.use_set(L.par);
   XK_CUDA_H(cudaMemcpyAsync(L.labels_all, labels_dev, batch * 4, cudaMemcpyDeviceToDevice, L.stream));
   xknn_status_t s = L.run_selection(batch);
   if (s != XKNN_OK) return s;
@@ -634,6 +768,16 @@ xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t 
   if (count_host) *count_host = hs.active_count;
   if (contains_all) *contains_all = hs.labels_found == hs.labels_local;
   return XKNN_OK;
+}
+
+xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local, uint64_t bl,
+                           void* ready_stream) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "prepare: knn mode without shard graphs");
+  if (bl == 0 || bl * L.world > L.bmax)
+    return fail(XKNN_ERR_INVALID_ARGUMENT, "prepare: batch size must be a positive multiple of P (<= max_batch)");
+  return L.run_prepare(labels_local, bl, static_cast<cudaStream_t>(ready_stream));
 }
 
 xknn_status_t xknn_step(xknn_layer_t* h, const float* feats, const uint32_t* labels,
@@ -667,7 +811,8 @@ xknn_status_t xknn_layer_last_active(xknn_layer_t* h, uint64_t* total, uint64_t*
   GUARD_H(h);
   Layer& L = h->L;
   xknn::SelState hs;
-  XK_CUDA_H(cudaMemcpyAsync(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost, L.stream));
+  XK_CUDA_H(cudaMemcpyAsync(&hs, L.ss[L.last_par].st, sizeof(hs), cudaMemcpyDeviceToHost,
+                            L.stream));
   XK_CUDA_H(cudaStreamSynchronize(L.stream));
   if (total) *total = hs.active_total;
   if (local) *local = hs.active_count;
@@ -700,8 +845,7 @@ xknn_status_t xknn_layer_profile(xknn_layer_t* h, int enable) {
   }
   L.prof_collect(true);
   L.prof_on = enable != 0;
-  if (L.graph_exec) cudaGraphExecDestroy(L.graph_exec);  // re-capture with/without the marks
-  L.graph_exec = nullptr;
+  L.drop_graphs();  // re-capture with/without the marks
   L.prof_ms.assign(Layer::kMarks, 0.0);
   L.prof_steps = L.prof_done = 0;
   return XKNN_OK;

@@ -129,10 +129,36 @@ struct Layer {
   uint64_t dxpart_splits = 0;
   double* loss_dev = nullptr;         // [1]
   float* lr_dev = nullptr;            // [1] learning rate of the current step
-  // CUDA graph of run_core per batch size
-  cudaGraphExec_t graph_exec = nullptr;
-  uint64_t graph_b = 0, graph_launches = 0;
-  bool graph_mode = false, graph_prof = false;
+  // CUDA graphs of run_core per batch size: [selection set][selection prepared]
+  cudaGraphExec_t core_graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t core_graph_b[2][2] = {{0, 0}, {0, 0}}, core_graph_launches[2][2] = {{0, 0}, {0, 0}};
+  bool core_graph_prof[2][2] = {{false, false}, {false, false}};
+  bool graph_mode = false;
+  void drop_graphs();
+
+  // ---- pipelined selection (xknn_prepare).  The selection of step t+1 needs only its labels and
+  // the graph, so xknn_prepare runs it on the side stream while step t is still busy (its GEMMs
+  // and the HBM-bound row update).  Its outputs that the rest of a step reads live in two sets;
+  // the step after a prepare waits on ev_prep and skips its own selection.
+  struct SelSet {
+    SelState* st = nullptr;
+    uint32_t* active = nullptr;
+    int32_t* label_col = nullptr;
+  };
+  SelSet ss[2];
+  int par = 0;                        // the set the next step (or prepare) uses
+  int last_par = 0;                   // the set of the last step
+  bool prepared = false;
+  uint64_t prepared_b = 0;
+  bool core_prepared = false;         // run_core: the selection was done by xknn_prepare
+  cudaEvent_t ev_sel_done = nullptr;  // the last step's selection finished (scratch reusable)
+  cudaEvent_t ev_prep = nullptr, ev_ready = nullptr;
+  cudaGraphExec_t sel_graph[2] = {nullptr, nullptr};
+  uint64_t sel_graph_b[2] = {0, 0}, sel_graph_launches[2] = {0, 0};
+  void use_set(int p);
+  xknn_status_t run_prepare(const uint32_t* labels_local, uint64_t batch_local, cudaStream_t ready);
+  xknn_status_t record_external(cudaEvent_t ev, cudaStream_t on);
+  xknn_status_t wait_external(cudaEvent_t ev, cudaStream_t on);
   uint64_t last_b = 0;
 
   std::string last_msg;

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--m-active", dest="m", type=int, default=4_000)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--precision", default="bf16")
+    ap.add_argument("--prepare", action="store_true", help="pipelined selection (xknn_prepare)")
     args = ap.parse_args()
 
     import torch
@@ -65,6 +66,8 @@ def main():
         res[f"contains_{s}"] = ca
         xs = torch.from_numpy(x[rank * bl:(rank + 1) * bl].copy()).cuda()
         ys = torch.from_numpy(lab[rank * bl:(rank + 1) * bl].view(np.int32).copy()).cuda()
+        if args.prepare:
+            layer.prepare(ys)
         gf = torch.empty(bl, d, device="cuda")
         res[f"loss_{s}"] = layer.train_step(xs, ys, 0.1, grad_features_local=gf)
         res[f"gf_{s}"] = gf.cpu().numpy()

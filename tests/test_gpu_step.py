@@ -143,3 +143,46 @@ def test_step_errors_leave_parameters(precision):
     assert abs(loss - loss_or) <= tol * abs(loss_or)
     layer.close()
     small.close()
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_step_with_prepared_selection(precision):
+    """xknn_prepare: the next step's selection runs on the side stream while the current step is
+    in flight; results equal the oracle's (and the unprepared path), including steps that are not
+    prepared and a prepared selection superseded by xknn_select."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    prec = X.PREC_BF16 if precision == "bf16" else X.PREC_FP32_EXACT
+    n, b, k, m = 30_000, 256, 10, 3_000
+    rng = np.random.default_rng(4)
+    w = (rng.standard_normal((n, 512)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 6)
+    shards = [O.compress(g, 1, 0)]
+    layer = make_layer(n, 512, 1, 0, m, b, w, g, precision=prec, seed=42)
+    xs = [rng.standard_normal((b, 512)).astype(np.float32) for _ in range(6)]
+    labs = [rng.integers(0, n, b).astype(np.uint32) for _ in range(6)]
+    dev_lab = [torch.from_numpy(l.view(np.int32)).cuda() for l in labs]
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    plan = [True, True, False, True, True, True]  # step 2 runs its own selection
+    layer.prepare(dev_lab[0])
+    for s in range(6):
+        if s == 4:  # a superseded prepare: xknn_select in between, then prepare again
+            got, _ = layer.select_active_classes(dev_lab[s])
+            rc, want, _ = O.select_shards("oracle", n, shards, labs[s], m, 42)
+            assert rc == 0 and np.array_equal(got.cpu().numpy().view(np.uint32), want)
+            layer.prepare(dev_lab[s])
+        layer.train_step(torch.from_numpy(xs[s]).cuda(), dev_lab[s], 0.1, sync=False)
+        if s + 1 < 6 and plan[s + 1]:
+            layer.prepare(dev_lab[s + 1])
+        layer.sync()
+        loss = float(layer._loss.item())
+        rc, loss_or, act, _, _ = O.fc_train_step(w_or, v_or, xs[s], labs[s], shards, m, 42)
+        assert rc == 0
+        tol = 2e-4 if precision == "bf16" else 1e-5
+        assert abs(loss - loss_or) <= tol * abs(loss_or), (s, loss, loss_or)
+        t, l = layer.last_active()
+        assert l == act.size
+    wg = layer.weights().cpu().numpy()
+    assert rel_err(wg - w, w_or - w) <= (1e-2 if precision == "bf16" else 1e-5)
+    layer.close()
