@@ -200,6 +200,12 @@ xknn_status_t xknn_graph_ring(const float* w_norm_local_dev, uint64_t num_classe
                              void* stream, uint32_t* out_rows_dev, uint64_t* uncertified_rows,
                              uint64_t* transfer_steps);
 
+/* The graph builds (xknn_graph_ring / _bruteforce / xknn_layer_rebuild_graph / classify) take
+   their scratch from the device's default CUDA memory pool and leave it cached there for the
+   next build (no driver map/unmap of GBs per rebuild).  This returns the cached blocks to the
+   driver (cf. torch.cuda.empty_cache()).  Synchronizes the device.  No reference counterpart. */
+xknn_status_t xknn_graph_release_cache(void);
+
 /* compress_graph (knn_graph.cpp:235-266) + HybridSim::set_shard_graphs (parallel.cpp:381-388)
    from the row-distributed full graph: every rank passes its rows [begin, end) x k (global ids,
    device), entries are exchanged all-to-all by owning shard, and each layer installs its

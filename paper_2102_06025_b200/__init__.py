@@ -107,6 +107,7 @@ for _name, _args in {
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_last_logits": [VP, VP, U64],
     "xknn_graph_bruteforce": [VP, U64, U64, C.c_uint32, C.c_uint32, VP, VP, C.POINTER(U64)],
+    "xknn_graph_release_cache": [],
     "xknn_graph_ring": [VP, U64, U64, C.c_uint32, C.c_uint32, C.c_int, C.c_int, VP, VP, VP,
                         C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_set_graph_rows": [VP, VP, C.c_uint32],
@@ -198,6 +199,11 @@ def graph_ring(w_norm_local, num_classes: int, k: int, kprime: int, rank: int, w
                                 torch.cuda.current_stream().cuda_stream, out.data_ptr(),
                                 C.byref(unc), C.byref(steps)))
     return out, unc.value, steps.value
+
+
+def release_graph_cache() -> None:
+    """Return the graph builds' cached device scratch to the driver (xknn_graph_release_cache)."""
+    _check(_lib.xknn_graph_release_cache())
 
 
 def save_graph_rows(path: str, num_classes: int, begin: int, rows, create: bool) -> None:

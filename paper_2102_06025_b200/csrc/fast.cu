@@ -42,13 +42,14 @@ struct GemmArgs {
   // graph build (kG): own rows (A, global ids row_base..) against a held block of ncols
   // columns (B, global ids col_base..).  Per in-flight unit slot (pair * 256 + row): two
   // candidate regions [slot][half][ch] of (approx score, column id) with counts/cuts; per own
-  // row: the persistent candidate list [row][kprime], its length and cut (every column not in
+  // row: the persistent candidate list [row][kcap], its length and cut (every column not in
   // the list has approx score <= cut), merged at the end of each unit.
   float2* cand;
   uint32_t* cnt;
   float* tau;
-  uint32_t ch, kprime, nrows, ncols;
+  uint32_t ch, kprime, kcap, nrows, ncols;  // kcap: list capacity (row stride) >= kprime
   uint32_t row_base, col_base;
+  uint32_t gchunk;  // kG: class tiles per column chunk (the L2-resident slice all pairs share)
   float2* list;
   uint32_t* lcnt;
   float* lcut;
@@ -96,7 +97,8 @@ struct Cfg2<kG> {
 template <int KIND>
 constexpr uint32_t smem_bytes2() {
   using C = Cfg2<KIND>;
-  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * C::NSTG * C::STG + 1024 + 256;
+  return C::ARES_BYTES + C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * C::NSTG * C::STG + 1024 + 256 +
+         (KIND == kG ? 1024 : 0);
 }
 
 struct Unit2 {
@@ -112,7 +114,12 @@ struct Unit2 {
 template <int KIND, int MCP>
 __device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
   if (KIND == kDW) return (mw + 255) / 256;
-  if (KIND == kG) return (a.nrows + 256 * MCP - 1) / (256 * MCP);
+  if (KIND == kG) {  // chunk-major: every pair's row blocks against chunk 0, then chunk 1, ...
+    const uint32_t npairs = gridDim.x / (2 * MCP);
+    const uint32_t nrb = (a.nrows + 256 * MCP - 1) / (256 * MCP);
+    const uint32_t nchunk = ((a.ncols + 255) / 256 + a.gchunk - 1) / a.gchunk;
+    return nchunk * ((nrb + npairs - 1) / npairs) * npairs;
+  }
   return a.nbt / MCP * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per tile
 }
 
@@ -126,11 +133,20 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
     x.valid = true;
     return x;
   }
-  if (KIND == kG) {  // one 256-row query block against every 256-column tile of the block
-    x.row0 = (u * MCP + pc) * 256;
-    x.t0 = 0;
-    x.t1 = (a.ncols + 255) / 256;
-    x.valid = true;
+  if (KIND == kG) {
+    // one 256-row query block against one column chunk.  A pair owns the row blocks
+    // rb = pair (mod npairs) and visits them chunk by chunk, so (i) a row's list is only ever
+    // merged by one pair, in chunk order, and (ii) all pairs stream the same chunk at about the
+    // same time: it is read from HBM once and served from L2 to every pair
+    const uint32_t npairs = gridDim.x / (2 * MCP);
+    const uint32_t nrb = (a.nrows + 256 * MCP - 1) / (256 * MCP);
+    const uint32_t nrbp = (nrb + npairs - 1) / npairs;
+    const uint32_t j = u / npairs, rb = (j % nrbp) * npairs + u % npairs;
+    const uint32_t nt = (a.ncols + 255) / 256;
+    x.row0 = (rb * MCP + pc) * 256;
+    x.t0 = (j / nrbp) * a.gchunk;
+    x.t1 = min(nt, x.t0 + a.gchunk);
+    x.valid = rb < nrb && x.t1 > x.t0;
     return x;
   }
   const uint32_t nbc = a.nbt / MCP;
@@ -205,15 +221,51 @@ __device__ __forceinline__ uint32_t warp_cut_key(Get get, uint32_t total, uint32
 
 // A cut T over the n entries rp[] (all scoring above lo) with kp/2 <= #(> T) <= kp when the
 // scores allow (bisection in score space; at most kp entries above T in every case), so that
-// compactions free at least half the region while keeping the best kp/2.  Warp-cooperative.
+// compactions free at least half the region while keeping the best kp/2.  Warp-cooperative;
+// regions of up to 32 * kCutRegs entries are bisected in registers (one pass over memory).
+constexpr int kCutRegs = 16;
 __device__ __noinline__ float warp_cut_band(const float2* __restrict__ rp, uint32_t n, float lo,
                                             uint32_t kp, uint32_t lane) {
+  if (n <= 32u * kCutRegs) {
+    float r[kCutRegs];
+    float hi = -INFINITY, mn = INFINITY;
+#pragma unroll
+    for (int i = 0; i < kCutRegs; ++i) {
+      const uint32_t e = lane + 32u * i;
+      r[i] = e < n ? rp[e].x : -INFINITY;
+      hi = fmaxf(hi, r[i]);
+      if (e < n) mn = fminf(mn, r[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      hi = fmaxf(hi, __shfl_xor_sync(XKNN_FULL_MASK, hi, o));
+      mn = fminf(mn, __shfl_xor_sync(XKNN_FULL_MASK, mn, o));
+    }
+    // invariant: #(> lo) > kp, #(> hi) <= kp; the first compaction of a unit starts from the
+    // region's minimum
+    if (!(lo > -INFINITY)) lo = nextafterf(mn, -INFINITY);
+#pragma unroll 1
+    for (int it = 0; it < 40; ++it) {
+      const float mid = 0.5f * (lo + hi);
+      if (!(mid > lo && mid < hi)) break;  // adjacent floats
+      uint32_t c = 0;
+#pragma unroll
+      for (int i = 0; i < kCutRegs; ++i) c += r[i] > mid;
+      c = warp_sum(c);
+      if (c > kp) {
+        lo = mid;
+      } else {
+        hi = mid;
+        if (2 * c >= kp) break;
+      }
+    }
+    return hi;
+  }
   float hi = -INFINITY;
   for (uint32_t e = lane; e < n; e += 32) hi = fmaxf(hi, rp[e].x);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(XKNN_FULL_MASK, hi, o));
-  // invariant: #(> lo) > kp, #(> hi) <= kp
-  if (!(lo > -INFINITY)) {  // first compaction of a unit: start from the region's minimum
+  if (!(lo > -INFINITY)) {
     float mn = INFINITY;
     for (uint32_t e = lane; e < n; e += 32) mn = fminf(mn, rp[e].x);
 #pragma unroll
@@ -223,7 +275,7 @@ __device__ __noinline__ float warp_cut_band(const float2* __restrict__ rp, uint3
 #pragma unroll 1
   for (int it = 0; it < 40; ++it) {
     const float mid = 0.5f * (lo + hi);
-    if (!(mid > lo && mid < hi)) break;  // adjacent floats
+    if (!(mid > lo && mid < hi)) break;
     uint32_t c = 0;
     for (uint32_t e = lane; e < n; e += 32) c += rp[e].x > mid;
     c = warp_sum(c);
@@ -237,32 +289,69 @@ __device__ __noinline__ float warp_cut_band(const float2* __restrict__ rp, uint3
   return hi;
 }
 
+constexpr int kMergeRegs = 36;  // merges of up to 32 * 36 entries bisect in registers
+
 // Merge of one row's persistent candidate list with the two regions of its unit slot: the cut
-// becomes the largest of the three cuts (every column left out of any of them scores <= it);
-// above it at most kprime entries are kept, raising the cut to the (kprime+1)-th largest score
-// if needed.  Invariant: every column not in the list has approx score <= lcut[row].
+// becomes the largest of the three cuts (every column left out of any of them scores <= it).
+// Common case (late column chunks): neither region raised its cut and the new entries fit the
+// list's spare capacity -- they are appended.  Otherwise the entries above the cut are kept,
+// and if more than kcap remain the cut rises to the (kprime+1)-th largest score (at most kprime
+// kept), leaving kcap - kprime slots for the next appends.
+// Invariant: every column not in the list has approx score <= lcut[row].
 __device__ __noinline__ void merge_candidates(float2* __restrict__ list, uint32_t* __restrict__ lcnt,
                                               float* __restrict__ lcut,
                                               const float2* __restrict__ cand,
                                               const uint32_t* __restrict__ cnt,
                                               const float* __restrict__ tau, uint32_t ch,
-                                              uint32_t kp, uint32_t row, uint32_t slot,
-                                              uint32_t lane) {
+                                              uint32_t kp, uint32_t kcap, uint32_t row,
+                                              uint32_t slot, uint32_t lane) {
   const uint32_t n0 = cnt[slot * 2], n1 = cnt[slot * 2 + 1];
   if (n0 + n1 == 0) return;  // nothing new: the regions' cuts never rose above lcut
-  float2* L = list + (uint64_t)row * kp;
+  float2* L = list + (uint64_t)row * kcap;
   const float2* R0 = cand + (uint64_t)slot * 2 * ch;
   const float2* R1 = R0 + ch;
   const uint32_t nl = lcnt[row];
-  float T = fmaxf(lcut[row], fmaxf(tau[slot * 2], tau[slot * 2 + 1]));
+  const float lc = lcut[row];
+  float T = fmaxf(lc, fmaxf(tau[slot * 2], tau[slot * 2 + 1]));
   const uint32_t total = nl + n0 + n1;
+  if (T == lc && total <= kcap) {  // every region entry scores > lc: append
+    for (uint32_t e = lane; e < n0 + n1; e += 32) L[nl + e] = e < n0 ? R0[e] : R1[e - n0];
+    if (lane == 0) lcnt[row] = total;
+    return;
+  }
   auto get = [&](uint32_t e) -> float2 {
     return e < nl ? L[e] : (e < nl + n0 ? R0[e - nl] : R1[e - nl - n0]);
   };
-  uint32_t above = 0;
-  for (uint32_t e = lane; e < total; e += 32) above += get(e).x > T;
-  above = warp_sum(above);
-  if (above > kp) T = funkey(warp_cut_key(get, total, kp, lane));
+  if (total <= 32u * kMergeRegs) {  // keys in registers: one pass over memory, then bisection
+    uint32_t key[kMergeRegs];
+    const uint32_t tk = fkey(T);
+    uint32_t above = 0;
+#pragma unroll
+    for (int i = 0; i < kMergeRegs; ++i) {
+      const uint32_t e = lane + 32u * i;
+      key[i] = e < total ? fkey(get(e).x) : 0u;  // 0: below every score's key
+      above += key[i] > tk;
+    }
+    above = warp_sum(above);
+    if (above > kcap) {  // largest key lo with #(>= lo) > kp; keep the entries above it
+      uint32_t lo = tk, hi = 0xffffffffu;
+#pragma unroll 1
+      while (lo < hi) {
+        const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < kMergeRegs; ++i) c += key[i] >= mid;
+        c = warp_sum(c);
+        if (c > kp) lo = mid; else hi = mid - 1;
+      }
+      T = funkey(lo);
+    }
+  } else {
+    uint32_t above = 0;
+    for (uint32_t e = lane; e < total; e += 32) above += get(e).x > T;
+    above = warp_sum(above);
+    if (above > kcap) T = funkey(warp_cut_key(get, total, kp, lane));
+  }
   uint32_t w = 0;
   for (uint32_t base = 0; base < total; base += 32) {
     const uint32_t e = base + lane;
@@ -302,6 +391,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* afull = tempty + 2;
   uint64_t* aempty = afull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
+  // kG: each column half's current cut per row, [half][row]; the other half may use it too
+  float* shcut = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
+  if (KIND == kG) shcut[threadIdx.x & 255] = -INFINITY;  // 384 threads cover the 256 slots
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // cluster of 2 * MCP CTAs: MCP CTA pairs; cta = rank in the pair, pc = pair in the cluster
@@ -500,19 +592,21 @@ __global__ void __launch_bounds__(384, 1)
           // when the region fills, raise the cut to its kprime-th largest score and compact
           const bool vrow = grow < a.nrows;
           const uint32_t cap = a.ch, kp = a.kprime;
-#pragma unroll 1
-          for (uint32_t chk = 0; chk < 4; ++chk) {
+          auto gproc = [&](const uint32_t (&r)[32], uint32_t chk) {
             const uint32_t col = h * 128 + chk * 32;
             float v[32];
-            tc::tmem_ld32(tb + col, v);
-            const uint32_t c0 = t * 256 + col;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            const uint32_t c0 = (x.t0 + t) * 256 + col;
             // the common case late in the scan: nothing in the warp's 32x32 chunk beats its
             // cut -- one max tree and a vote instead of 32 compares per lane
+            // the other half's cut is a valid cut for this half too (the merge takes the max)
+            ctau = fmaxf(ctau, shcut[(h ^ 1) * 128 + row]);
             float mx = v[0];
 #pragma unroll
             for (int j = 1; j < 31; j += 2) mx = fmaxf(mx, fmaxf(v[j], v[j + 1]));
             mx = fmaxf(mx, v[31]);
-            if (!__any_sync(XKNN_FULL_MASK, vrow && mx > ctau)) continue;
+            if (!__any_sync(XKNN_FULL_MASK, vrow && mx > ctau)) return;
             uint32_t mask = 0;  // columns of this chunk above the current cut
 #pragma unroll
             for (int j = 0; j < 32; ++j) mask |= (v[j] > ctau ? 1u : 0u) << j;
@@ -521,7 +615,7 @@ __global__ void __launch_bounds__(384, 1)
             if (c0 + 32 > a.ncols) mask &= a.ncols > c0 ? (0xffffffffu >> (32 - (a.ncols - c0))) : 0u;
             const uint32_t selfc = a.row_base + grow - a.col_base - c0;  // self column in chunk
             if (selfc < 32) mask &= ~(1u << selfc);
-            if (!__any_sync(XKNN_FULL_MASK, mask != 0)) continue;
+            if (!__any_sync(XKNN_FULL_MASK, mask != 0)) return;
             float sc[32];  // spill-friendly copy for the dynamic-index inserts
 #pragma unroll
             for (int j = 0; j < 32; ++j) sc[j] = v[j];
@@ -568,13 +662,29 @@ __global__ void __launch_bounds__(384, 1)
                 if ((int)lane == f) {
                   ctau = T;
                   ccnt = w;
+                  shcut[h * 128 + row] = T;
                 }
               }
             }
-          }
+          };
+          // the next chunk's TMEM load is in flight while this one is scanned; TMEM is released
+          // as soon as the last chunk is in registers
+          uint32_t ra[32], rb[32];
+          tc::tmem_ld32_issue(tb + h * 128, ra);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 32, rb);
+          gproc(ra, 0);
+          tc::tmem_ld_wait(rb);
+          tc::tmem_ld32_issue(tb + h * 128 + 64, ra);
+          gproc(rb, 1);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 96, rb);
+          gproc(ra, 2);
+          tc::tmem_ld_wait(rb);
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], lead);
+          gproc(rb, 3);
           if (t + 1 == ntile) {
             a.cnt[slot * 2 + h] = ccnt;
             a.tau[slot * 2 + h] = ctau;
@@ -683,9 +793,10 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t r = q * 32 + 2 * i + h;
           const uint32_t gr = x.row0 + cta * 128 + r;
           if (gr < a.nrows)
-            merge_candidates(a.list, a.lcnt, a.lcut, a.cand, a.cnt, a.tau, a.ch, a.kprime, gr,
+            merge_candidates(a.list, a.lcnt, a.lcut, a.cand, a.cnt, a.tau, a.ch, a.kprime, a.kcap, gr,
                              (blockIdx.x >> 1) * 256 + cta * 128 + r, lane);
         }
+        shcut[h * 128 + row] = -INFINITY;  // the next unit's rows start from their lists' cuts
         epilogue_bar();  // regions free for the next unit
       }
     }
@@ -1064,8 +1175,8 @@ namespace xknn {
 cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t row_base,
                                     const __half* held, uint32_t ncols, uint32_t col_base,
                                     float2* list, uint32_t* lcnt, float* lcut, uint32_t kprime,
-                                    float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
-                                    cudaStream_t s) {
+                                    uint32_t kcap, float2* cand, uint32_t* cnt, float* tau,
+                                    uint32_t ch, cudaStream_t s) {
   CUtensorMap mA, mB;
   // 4-CTA clusters: two query blocks per cluster share every class tile (multicast)
   const bool mc = nrows > 256 && getenv("XKNN_MULTICAST");
@@ -1096,7 +1207,14 @@ cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t 
   ga.tau = tau;
   ga.ch = ch;
   ga.kprime = kprime;
+  ga.kcap = kcap;
   ga.dim = 512;
+  static const uint32_t gchunk = [] {
+    const char* e = getenv("XKNN_GCHUNK");  // tuning knob (class tiles per chunk)
+    const long v = e ? atol(e) : 0;
+    return v > 0 ? (uint32_t)v : 128u;
+  }();
+  ga.gchunk = gchunk;
   if (mc)
     launch_pdl_cluster(k_gemm2<kG, 2>, cluster_grid(k_gemm2<kG, 2>, 4, smem_bytes2<kG>()), 384,
                        smem_bytes2<kG>(), s, 4u, mA, mB, mA, ga);

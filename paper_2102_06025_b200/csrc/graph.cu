@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <vector>
 
 #include "graph.cuh"
@@ -35,8 +36,8 @@ namespace xknn {
 cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t row_base,
                                     const __half* held, uint32_t ncols, uint32_t col_base,
                                     float2* list, uint32_t* lcnt, float* lcut, uint32_t kprime,
-                                    float2* cand, uint32_t* cnt, float* tau, uint32_t ch,
-                                    cudaStream_t s);
+                                    uint32_t kcap, float2* cand, uint32_t* cnt, float* tau,
+                                    uint32_t ch, cudaStream_t s);
 
 namespace {
 
@@ -54,6 +55,18 @@ __global__ void k_to_f16(const float* __restrict__ w, uint64_t n, uint64_t npad,
     const uint64_t row = (2 * e) / d;
     float2 v = row < n ? reinterpret_cast<const float2*>(w)[e] : make_float2(0.f, 0.f);
     reinterpret_cast<__half2*>(out)[e] = __floats2half2_rn(v.x, v.y);
+  }
+}
+
+// every stride-th own row (fp16) -> a pilot block of ns rows (zero rows up to a multiple of 256)
+__global__ void k_sample_rows(const __half* __restrict__ own, uint32_t stride, uint32_t ns,
+                              uint32_t nspad, __half* __restrict__ out) {
+  const uint64_t total = (uint64_t)nspad * 64;  // 16-B units, 64 per 512-wide row
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e / 64, c = e % 64;
+    reinterpret_cast<uint4*>(out)[e] =
+        r < ns ? reinterpret_cast<const uint4*>(own)[(r * stride) * 64 + c] : make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -96,15 +109,50 @@ __device__ __forceinline__ bool before(float sa, uint32_t ia, float sb, uint32_t
   return ia < ib;
 }
 
+// Pilot seed, one warp per row: after the pilot pass against a strided sample of the own block,
+// the row's cut starts at the j-th best approximate sample score (the list is emptied; every
+// column is scanned again by the main pass).  A cut is only ever a bound on what was left out,
+// so any starting value is correct; a too-high one shows up as an uncertified row (exact
+// fallback).  With 1 in `stride` columns sampled, the seed lies above the row's (k-1)-th best
+// + 2 eps (about its 125th best on random unit rows) only if j of those fell in the sample:
+// a Poisson(125 / 32) tail, ~1e-7 at j = 18.  The seed sits near the row's j*stride-th best,
+// so the main pass inserts few more than k' entries per row.
+__global__ void k_seed_cut(const float2* __restrict__ list, uint32_t* __restrict__ lcnt,
+                           float* __restrict__ lcut, uint32_t n, uint32_t kc, uint32_t j) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    const float2* L = list + (uint64_t)r * kc;
+    const uint32_t m = lcnt[r];
+    float seed = -INFINITY;
+    if (m >= j) {  // j-th largest: largest key with #(>= key) >= j
+      uint32_t lo = 0, hi = 0xffffffffu;
+      while (lo < hi) {
+        const uint32_t mid = (uint32_t)(((uint64_t)lo + hi + 1) >> 1);
+        uint32_t c = 0;
+        for (uint32_t e = lane; e < m; e += 32) c += fkey(L[e].x) >= mid;
+        c = warp_sum(c);
+        if (c >= j) lo = mid; else hi = mid - 1;
+      }
+      seed = funkey(lo);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      lcnt[r] = 0;
+      lcut[r] = seed;
+    }
+  }
+}
+
 // Step 2, one warp per row: certificate and candidate window (see the file comment).
 __global__ void k_window(float2* __restrict__ list, uint32_t* __restrict__ lcnt,
-                         const float* __restrict__ lcut, uint32_t n, uint32_t kp, uint32_t need,
+                         const float* __restrict__ lcut, uint32_t n, uint32_t kc, uint32_t need,
                          uint32_t* __restrict__ flag, uint32_t* __restrict__ unc_count,
                          uint32_t* __restrict__ unc_list) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n;
        j += (gridDim.x * blockDim.x) >> 5) {
-    float2* L = list + (uint64_t)j * kp;
+    float2* L = list + (uint64_t)j * kc;
     const uint32_t m = lcnt[j];
     const float T = lcut[j];
     bool cert = false;
@@ -152,7 +200,7 @@ __global__ void k_window(float2* __restrict__ list, uint32_t* __restrict__ lcnt,
 // [cb, cb + nc) (fp32 rows `held`).  ex[row][e] parallels list[row][e].
 __global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
                           const float2* __restrict__ list, const uint32_t* __restrict__ lcnt,
-                          const uint32_t* __restrict__ flag, uint32_t kp,
+                          const uint32_t* __restrict__ flag, uint32_t kc,
                           const float* __restrict__ held, uint32_t cb, uint32_t nc,
                           float* __restrict__ ex) {
   // D = 512.  Lane l carries candidate l of a group of 32 through the reference's sequential
@@ -166,7 +214,7 @@ __global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
        j += (gridDim.x * blockDim.x) >> 5) {
     if (flag[j]) continue;
     const uint32_t m = lcnt[j];
-    const float2* L = list + (uint64_t)j * kp;
+    const float2* L = list + (uint64_t)j * kc;
     __syncwarp();
     for (uint32_t c = lane; c < 128; c += 32)
       reinterpret_cast<float4*>(qrow)[c] = reinterpret_cast<const float4*>(own + (uint64_t)j * 512)[c];
@@ -199,7 +247,7 @@ __global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
 #pragma unroll
         for (uint32_t t = 0; t < 32; ++t) acc = __fadd_rn(acc, __fmul_rn(q[t], mine_row[t]));
       }
-      if (mine) ex[(uint64_t)j * kp + e] = acc;
+      if (mine) ex[(uint64_t)j * kc + e] = acc;
     }
   }
 }
@@ -233,7 +281,7 @@ __global__ void k_take(const uint32_t* __restrict__ keys, const uint32_t* __rest
 
 // Step 4, one warp per row: sort the row's exactly scored candidates under `better` (warp
 // bitonic in shared memory), write self + the k-1 best.
-__global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t kp, uint32_t cap,
+__global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t kc, uint32_t cap,
                            const float2* __restrict__ list, const uint32_t* __restrict__ lcnt,
                            const float* __restrict__ ex, const uint32_t* __restrict__ flag,
                            const float2* __restrict__ ubuf, uint32_t ulen,
@@ -255,8 +303,8 @@ __global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t k
           s = v.x;
           i = __float_as_uint(v.y);
         } else {
-          s = ex[(uint64_t)j * kp + e];
-          i = __float_as_uint(list[(uint64_t)j * kp + e].y);
+          s = ex[(uint64_t)j * kc + e];
+          i = __float_as_uint(list[(uint64_t)j * kc + e].y);
         }
       }
       ss[e] = s;
@@ -292,7 +340,7 @@ __global__ void k_finalize(uint32_t n, uint32_t row_base, uint32_t k, uint32_t k
 
 // classify: one warp per query, the best exactly scored candidate (higher score, then lower
 // class id) of its window, or its exact scan's winner when uncertified
-__global__ void k_top1(uint32_t n, uint32_t kp, const float2* __restrict__ list,
+__global__ void k_top1(uint32_t n, uint32_t kc, const float2* __restrict__ list,
                        const uint32_t* __restrict__ lcnt, const float* __restrict__ ex,
                        const uint32_t* __restrict__ flag, const float2* __restrict__ ubuf,
                        float* __restrict__ best_score, uint32_t* __restrict__ best_id) {
@@ -310,8 +358,8 @@ __global__ void k_top1(uint32_t n, uint32_t kp, const float2* __restrict__ list,
       }
     } else {
       for (uint32_t e = lane; e < lcnt[j]; e += 32) {
-        const float sc = ex[(uint64_t)j * kp + e];
-        const uint32_t id = __float_as_uint(list[(uint64_t)j * kp + e].y);
+        const float sc = ex[(uint64_t)j * kc + e];
+        const uint32_t id = __float_as_uint(list[(uint64_t)j * kc + e].y);
         if (before(sc, id, bs, bi)) {
           bs = sc;
           bi = id;
@@ -380,23 +428,37 @@ static cudaError_t exact_rows(const float* wn, uint32_t n, uint32_t d, uint32_t 
 }
 
 namespace {
-struct Dev {  // RAII device scratch
+// RAII device scratch, stream-ordered from the device's default memory pool.  Freed blocks stay
+// mapped in the pool (like a caching allocator): the next build -- the layer's periodic rebuild
+// -- reuses them without mapping or unmapping GBs through the driver (which costs 0.1-1 s per
+// build at 1M rows).  xknn_graph_release_cache() returns them (cf. torch.cuda.empty_cache()).
+struct Dev {
+  cudaStream_t s;
   std::vector<void*> p;
+  explicit Dev(cudaStream_t st) : s(st) {
+    int dev = 0;
+    cudaMemPool_t pool = nullptr;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   ~Dev() {
-    for (void* q : p) cudaFree(q);
+    for (void* q : p)
+      if (q) cudaFreeAsync(q, s);
   }
   template <typename T>
   cudaError_t get(T** out, uint64_t count) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(T));
+    cudaError_t e = cudaMallocAsync(&q, std::max<uint64_t>(count, 1) * sizeof(T), s);
     if (e == cudaSuccess) p.push_back(q);
     *out = static_cast<T*>(q);
     return e;
   }
-  void release(void* q) {
+  void release(void* q) {  // after every use of q enqueued so far on s (or joined into s)
     for (auto& x : p)
       if (x == q) {
-        cudaFree(x);
+        cudaFreeAsync(x, s);
         x = nullptr;
       }
   }
@@ -427,6 +489,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   if (n_total < (uint64_t)world) return fail_msg(XKNN_ERR_EMPTY_SHARD, "build_graph_ring: a shard is empty");
   if (world > 1 && !comm) return fail_msg(XKNN_ERR_INVALID_ARGUMENT, "graph ring: NCCL communicator required");
   const uint32_t d = (uint32_t)d64;
+  const auto host_t0 = std::chrono::steady_clock::now();
   uint64_t b64, e64;
   shard_range_of(n_total, world, rank, &b64, &e64);
   const uint32_t row_base = (uint32_t)b64, n = (uint32_t)(e64 - b64);
@@ -458,6 +521,8 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   // certificate holds for almost every row
   const uint32_t kp = std::max<uint32_t>({kprime, 2 * k, k + 32});
   const uint32_t ch = (2 * kp + 31) / 32 * 32;  // region capacity per (slot, half)
+  // list capacity (row stride of list / ex): k' plus room for the appends of later column chunks
+  const uint32_t kc = (kp + 48 + 31) / 32 * 32;
   uint64_t maxrows = 0;
   for (int r = 0; r < world; ++r) {
     uint64_t rb, re;
@@ -465,12 +530,12 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
     maxrows = std::max(maxrows, re - rb);
   }
   const uint64_t npad = (n + 255) / 256 * 256, mpad = (maxrows + 255) / 256 * 256;
-  Dev mem;
+  Dev mem(s);
   float2 *list = nullptr, *cand = nullptr;
   uint32_t *lcnt = nullptr, *ccnt = nullptr, *flag = nullptr, *unc = nullptr;
   float *lcut = nullptr, *ctau = nullptr, *ex = nullptr;
   __half *own16 = nullptr, *buf16[2] = {nullptr, nullptr};
-  G_CUDA(mem.get(&list, (uint64_t)n * kp));
+  G_CUDA(mem.get(&list, (uint64_t)n * kc));
   G_CUDA(mem.get(&lcnt, n));
   G_CUDA(mem.get(&lcut, n));
   G_CUDA(mem.get(&cand, (uint64_t)kNumSMs / 2 * 256 * 2 * ch));
@@ -500,19 +565,52 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   const int next = (rank + 1) % world, prev = (rank + world - 1) % world;
 
   // optional phase timing (XKNN_GRAPH_TIMING=1): candidates, window, exact ring, finalize
-  const bool timing = getenv("XKNN_GRAPH_TIMING") != nullptr;
-  cudaEvent_t tev[5] = {};
+  const bool timing = getenv("XKNN_GRAPH_TIMING") || getenv("XKNN_GRAPH_SCAN_ONLY");
+  cudaEvent_t tev[6] = {};
   if (timing)
     for (auto& ev : tev) {
       G_CUDA(cudaEventCreate(&ev));
       evs.push_back(ev);
     }
-  if (timing) G_CUDA(cudaEventRecord(tev[0], s));
+  if (timing) {
+    G_CUDA(cudaEventRecord(tev[0], s));
+    fprintf(stderr, "[xknn graph] host prologue %.2f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count());
+  }
   // ---- 1. candidate ring (fp16) ----
   k_to_f16<<<grid_for(npad * 256, 256), 256, 0, s>>>(wn, n, npad, 512, own16);
   G_CUDA(cudaGetLastError());
   k_list_init<<<grid_for(n, 256), 256, 0, s>>>(lcnt, lcut, n);
   G_CUDA(cudaGetLastError());
+  {
+    // pilot: seed every row's cut from a strided sample of the own block (k_seed_cut)
+    const uint32_t stride = 32, jseed = 18;
+    const uint32_t ns = n / stride;
+    if (ns >= 4096 && !getenv("XKNN_NO_PILOT")) {
+      const uint32_t nspad = (ns + 255) / 256 * 256;
+      __half* s16 = nullptr;
+      G_CUDA(mem.get(&s16, (uint64_t)nspad * 512));
+      k_sample_rows<<<grid_for((uint64_t)nspad * 64, 256), 256, 0, s>>>(own16, stride, ns, nspad,
+                                                                         s16);
+      G_CUDA(cudaGetLastError());
+      // sample ids lie above every class id: the row itself is not masked (its score only
+      // lowers the seed by one rank)
+      G_CUDA(launch_graph_candidates(own16, n, row_base, s16, ns, 0xffffffffu - ns - n, list,
+                                     lcnt, lcut, 32, kc, cand, ccnt, ctau, ch, s));
+      k_seed_cut<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(list, lcnt, lcut, n, kc, jseed);
+      G_CUDA(cudaGetLastError());
+      mem.release(s16);
+    }
+  }
+  if (timing) G_CUDA(cudaEventRecord(tev[5], s));
+  // diagnostic (XKNN_GRAPH_SCAN_ONLY=<cut>): every row's cut starts at <cut>; the build stops
+  // after the candidate pass (scan cost without inserts for a cut above every score)
+  const char* scan_only = n >= 100000 ? getenv("XKNN_GRAPH_SCAN_ONLY") : nullptr;
+  if (scan_only) {
+    std::vector<float> hc(n, (float)atof(scan_only));
+    G_CUDA(cudaMemcpyAsync(lcut, hc.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    G_CUDA(cudaStreamSynchronize(s));
+  }
   const __half* held = own16;
   for (int h = 0; h < world; ++h) {
     const int o = (rank - h + world) % world;
@@ -537,7 +635,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
       G_CUDA(cudaEventRecord(ev_recv, cs));
     }
     G_CUDA(launch_graph_candidates(own16, n, row_base, held, (uint32_t)(ce - cb), (uint32_t)cb,
-                                   list, lcnt, lcut, kp, cand, ccnt, ctau, ch, s));
+                                   list, lcnt, lcut, kp, kc, cand, ccnt, ctau, ch, s));
     if (h + 1 < world) {
       G_CUDA(cudaStreamWaitEvent(s, ev_recv, 0));
       held = buf16[h % 2];
@@ -560,10 +658,17 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
 
   // ---- 2. certificate + window ----
   if (timing) G_CUDA(cudaEventRecord(tev[1], s));
+  if (scan_only) {
+    G_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, tev[5], tev[1]);
+    fprintf(stderr, "[xknn graph] scan only (cut %s): candidates %.2f ms\n", scan_only, ms);
+    return fail_msg(XKNN_ERR_UNSUPPORTED, "XKNN_GRAPH_SCAN_ONLY diagnostic");
+  }
   G_CUDA(mem.get(&flag, n));
   G_CUDA(mem.get(&unc, (uint64_t)n + 1));
   G_CUDA(cudaMemsetAsync(unc, 0, 4, s));
-  k_window<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(list, lcnt, lcut, n, kp, need, flag, unc,
+  k_window<<<grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(list, lcnt, lcut, n, kc, need, flag, unc,
                                                            unc + 1);
   G_CUDA(cudaGetLastError());
   uint32_t nu = 0;
@@ -575,7 +680,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
 
   // ---- 3. exact ring (fp32) ----
   if (timing) G_CUDA(cudaEventRecord(tev[2], s));
-  G_CUDA(mem.get(&ex, (uint64_t)n * kp));
+  G_CUDA(mem.get(&ex, (uint64_t)n * kc));
   float* buf32[2] = {nullptr, nullptr};
   if (world > 1) {
     G_CUDA(mem.get(&buf32[0], maxrows * 512));
@@ -620,7 +725,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
     }
     G_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kRescoreSmem));
-    k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, kRescoreSmem, s>>>(wn, n, 512, list, lcnt, flag, kp,
+    k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, kRescoreSmem, s>>>(wn, n, 512, list, lcnt, flag, kc,
                                                               held32, (uint32_t)cb, nc, ex);
     G_CUDA(cudaGetLastError());
     for (uint32_t u = 0; u < nu; ++u) {  // rows without a certificate: exact scan of the block
@@ -644,26 +749,27 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   if (timing) G_CUDA(cudaEventRecord(tev[3], s));
   {
     uint32_t cap = 1;
-    while (cap < std::max(kp, nu ? ulen : 1u)) cap <<= 1;
+    while (cap < std::max(kc, nu ? ulen : 1u)) cap <<= 1;
     const uint32_t warps = 4;
     const size_t smem = (size_t)warps * cap * 8;
     if (smem > 48 * 1024)
       G_CUDA(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     k_finalize<<<grid_for((uint64_t)n * 32, warps * 32, 148u * 32u), warps * 32, smem, s>>>(
-        n, row_base, k, kp, cap, list, lcnt, ex, flag, ubuf, ulen, out);
+        n, row_base, k, kc, cap, list, lcnt, ex, flag, ubuf, ulen, out);
     G_CUDA(cudaGetLastError());
   }
   if (timing) G_CUDA(cudaEventRecord(tev[4], s));
   G_CUDA(cudaStreamSynchronize(s));
   if (cs) G_CUDA(cudaStreamSynchronize(cs));
   if (timing) {
-    float ms[4];
+    float ms[5];
     for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], tev[i], tev[i + 1]);
+    cudaEventElapsedTime(&ms[4], tev[0], tev[5]);
     fprintf(stderr,
-            "[xknn graph] rank %d rows %u k %u k' %u: candidates %.2f ms, window %.2f ms, "
-            "exact ring %.2f ms, finalize %.2f ms, uncertified %u\n",
-            rank, n, k, kp, ms[0], ms[1], ms[2], ms[3], nu);
+            "[xknn graph] rank %d rows %u k %u k' %u: candidates %.2f ms (pilot %.2f), window %.2f "
+            "ms, exact ring %.2f ms, finalize %.2f ms, uncertified %u\n",
+            rank, n, k, kp, ms[0], ms[4], ms[1], ms[2], ms[3], nu);
   }
 #undef G_CUDA
 #undef G_NCCL
@@ -687,17 +793,17 @@ xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn
   } while (0)
   if ((uint64_t)col_base + nw + nq >= 0xffffffffull)
     return fail_msg(XKNN_ERR_UNSUPPORTED, "classify: class ids + queries must fit u32");
-  const uint32_t kp = 32, ch = 64;
-  Dev mem;
+  const uint32_t kp = 32, kc = 64, ch = 64;
+  Dev mem(s);
   float2* list = nullptr;
   uint32_t *lcnt = nullptr, *flag = nullptr, *unc = nullptr;
   float *lcut = nullptr, *ex = nullptr;
-  G_CUDA(mem.get(&list, (uint64_t)nq * kp));
+  G_CUDA(mem.get(&list, (uint64_t)nq * kc));
   G_CUDA(mem.get(&lcnt, nq));
   G_CUDA(mem.get(&lcut, nq));
   G_CUDA(mem.get(&flag, nq));
   G_CUDA(mem.get(&unc, (uint64_t)nq + 1));
-  G_CUDA(mem.get(&ex, (uint64_t)nq * kp));
+  G_CUDA(mem.get(&ex, (uint64_t)nq * kc));
   G_CUDA(cudaMemsetAsync(unc, 0, 4, s));
   uint32_t nu = 0;
   if (d == 512) {
@@ -717,15 +823,15 @@ xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn
     G_CUDA(cudaGetLastError());
     // queries are not classes: their "self" ids lie above every class id
     G_CUDA(launch_graph_candidates(q16, nq, 0xffffffffu - nq, w16, nw, col_base, list, lcnt, lcut,
-                                   kp, cand, ccnt, ctau, ch, s));
-    k_window<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(list, lcnt, lcut, nq, kp, 1, flag,
+                                   kp, kc, cand, ccnt, ctau, ch, s));
+    k_window<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(list, lcnt, lcut, nq, kc, 1, flag,
                                                               unc, unc + 1);
     G_CUDA(cudaGetLastError());
     G_CUDA(cudaMemcpyAsync(&nu, unc, 4, cudaMemcpyDeviceToHost, s));
     G_CUDA(cudaStreamSynchronize(s));
     G_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kRescoreSmem));
-    k_rescore<<<grid_for((uint64_t)nq * 32, 256), 256, kRescoreSmem, s>>>(qn, nq, 512, list, lcnt, flag, kp,
+    k_rescore<<<grid_for((uint64_t)nq * 32, 256), 256, kRescoreSmem, s>>>(qn, nq, 512, list, lcnt, flag, kc,
                                                                wn, col_base, nw, ex);
     G_CUDA(cudaGetLastError());
   } else {  // exact scans for every query
@@ -762,7 +868,7 @@ xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn
       G_CUDA(cudaGetLastError());
     }
   }
-  k_top1<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(nq, kp, list, lcnt, ex, flag, ubuf,
+  k_top1<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(nq, kc, list, lcnt, ex, flag, ubuf,
                                                           best_score, best_id);
   G_CUDA(cudaGetLastError());
   G_CUDA(cudaStreamSynchronize(s));
@@ -782,6 +888,16 @@ extern "C" xknn_status_t xknn_graph_bruteforce(const float* w_norm_dev, uint64_t
                                       static_cast<cudaStream_t>(stream), out_dev, &st);
   if (uncertified_rows) *uncertified_rows = st.uncertified_rows;
   return r;
+}
+
+extern "C" xknn_status_t xknn_graph_release_cache(void) {
+  int dev = 0;
+  cudaMemPool_t pool = nullptr;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+  return e == cudaSuccess ? XKNN_OK : xknn::fail_msg(XKNN_ERR_CUDA, cudaGetErrorString(e));
 }
 
 extern "C" xknn_status_t xknn_graph_ring(const float* w_norm_local_dev, uint64_t num_classes,
