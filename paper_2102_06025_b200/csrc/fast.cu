@@ -616,6 +616,19 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t selfc = a.row_base + grow - a.col_base - c0;  // self column in chunk
             if (selfc < 32) mask &= ~(1u << selfc);
             if (!__any_sync(XKNN_FULL_MASK, mask != 0)) return;
+            if (__reduce_max_sync(XKNN_FULL_MASK, (uint32_t)__popc(mask)) >= 8 &&
+                __all_sync(XKNN_FULL_MASK, ccnt + __popc(mask) <= cap)) {
+              // dense chunk (early in a scan), every lane's columns fit its region: one
+              // predicated store per column instead of a divergent per-lane loop whose trip
+              // count is the warp's largest popcount
+              float2* dst = creg + ccnt;
+              uint32_t wi = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((mask >> j) & 1u) dst[wi++] = make_float2(v[j], __uint_as_float(a.col_base + c0 + j));
+              ccnt += wi;
+              return;
+            }
             float sc[32];  // spill-friendly copy for the dynamic-index inserts
 #pragma unroll
             for (int j = 0; j < 32; ++j) sc[j] = v[j];
