@@ -135,7 +135,7 @@ xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t 
    distributed softmax cross-entropy, updates its active weight rows with momentum SGD at
    learning rate lr, and writes d loss / d features for its own B/P rows (through the row
    normalization, the tensor handed to mlp_backward at parallel.cpp:585-586) to
-   grad_features_local_dev (may be NULL).  loss_dev (device double, may be NULL) receives the
+   grad_features_local_dev (may be NULL).  loss_dev (a double in device or pinned host memory, may be NULL) receives the
    mean loss, identical on all ranks.  Asynchronous: use xknn_layer_sync to collect errors. */
 xknn_status_t xknn_step(xknn_layer_t* h, const float* features_local_dev,
                         const uint32_t* labels_local_dev, uint64_t batch_local, float lr,

@@ -377,8 +377,9 @@ __global__ void __launch_bounds__(384, 1)
             const __grid_constant__ CUtensorMap tmOut, GemmArgs a) {
   using C = Cfg2<KIND>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on the __shared__ array, so the compiler keeps the
+  // shared address space (STS/LDS for the epilogue staging, not generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 1023u)) & 1023u);
   uint8_t* sRes = smem;                                      // F: resident A
   uint8_t* sA = sRes + C::ARES_BYTES;                        // staged A
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;                 // staged B

@@ -186,6 +186,14 @@ __global__ void k_set_f32(float* p, float v) {
   griddep_wait();
   griddep_launch(); *p = v; }
 
+// the step's loss to the caller's double (device or pinned host memory, through UVA): a kernel
+// in the stream's launch chain instead of a copy-engine node between two step graphs
+__global__ void k_copy_loss(double* dst, const double* src) {
+  griddep_wait();
+  griddep_launch();
+  *dst = *src;
+}
+
 void Layer::mark(int i, cudaStream_t on) {
   if (!prof_on) return;
   cudaStream_t stream = on ? on : this->stream;
@@ -493,8 +501,18 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   }
   mark(10);
   if (prof_on) ++prof_steps;
-  if (loss_out)
-    XK_CUDA(cudaMemcpyAsync(loss_out, loss_dev, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  if (loss_out) {
+    cudaPointerAttributes pa{};
+    double* dptr = nullptr;
+    if (cudaPointerGetAttributes(&pa, loss_out) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered)
+      dptr = static_cast<double*>(pa.devicePointer);  // pinned host memory: its mapped address
+    if (dptr) {
+      launch_pdl(k_copy_loss, 1, 1, 0, stream, dptr, (const double*)loss_dev);
+      XK_LAUNCH();
+    } else {  // pageable host memory: the driver stages it
+      XK_CUDA(cudaMemcpyAsync(loss_out, loss_dev, sizeof(double), cudaMemcpyDefault, stream));
+    }
+  }
   return XKNN_OK;
 }
 
