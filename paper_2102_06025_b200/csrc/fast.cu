@@ -867,9 +867,29 @@ template <int DV>
 __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restrict__ lcol,
                         const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
                         uint32_t bpad, uint32_t d, float scale, __nv_bfloat16* __restrict__ Pt,
-                        uint64_t ldp, __nv_bfloat16* __restrict__ Xs) {
+                        uint64_t ldp, __nv_bfloat16* __restrict__ Xs, double* __restrict__ loss,
+                        SelState* st, unsigned long long* err) {
   griddep_wait();
   griddep_launch();
+  if (blockIdx.x == 0) {
+    // the step's loss (k_loss's arithmetic, 256 threads): red is final once this grid runs
+    __shared__ double part[256];
+    double s = 0.0;
+    const uint32_t chunk = (B + blockDim.x - 1) / blockDim.x;
+    for (uint32_t i = threadIdx.x * chunk; i < min(B, (threadIdx.x + 1) * chunk); ++i) {
+      if (red[2 * B + i] != 1.0) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
+      s += log(red[i]) - red[B + i];
+    }
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (uint32_t k = 0; k < blockDim.x; ++k) t += part[k];
+      const double l = t / (double)B;
+      *loss = l;
+      st->loss = l;
+    }
+  }
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < bpad;
        b += (gridDim.x * blockDim.x) >> 5) {
@@ -1124,11 +1144,9 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
                                                      (uint32_t)B, f->bpad, rowred);
   XK_LAUNCH();
   if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
-  XK_CUDA(launch_loss(rowred, B, loss_dev, st, err, stream));
-  ++launches;
-  // (d) label-column fix-up of P~ and the row-scaled X_hat'
-  launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, 
-      rowred, label_col, X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16);
+  // (d) label-column fix-up of P~ and the row-scaled X_hat', and the loss (block 0)
+  launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, rowred, label_col,
+             X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16, loss_dev, st, err);
   XK_LAUNCH();
   mark(5);
   // (e) GEMM-dW -> bf16 dW rows (compact active order)
