@@ -128,14 +128,18 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
                              uint64_t nwords, const uint32_t* __restrict__ blk_off,
                              uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
                              uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
-                             int rank, uint32_t* __restrict__ samp) {
+                             int rank, uint32_t* __restrict__ samp,
+                             const unsigned long long* __restrict__ err) {
   griddep_wait();
   griddep_launch();
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
   __shared__ typename BS::TempStorage tmp;
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
+  // a step that already failed (MTooSmall, LabelOutOfRange, ...) gets an empty active set: the
+  // reference throws before any of it runs, and an over-full set would not fit the capacity
+  const bool dead = mode == 1 && *err != 0;
   uint32_t word = 0;
-  if (w < nwords) word = final_word(mode, st, act, pool, lab, w);
+  if (w < nwords && !dead) word = final_word(mode, st, act, pool, lab, w);
   uint32_t pos;
   BS(tmp).ExclusiveSum(__popc(word), pos);
   pos += blk_off[blockIdx.x];
@@ -156,7 +160,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
       pool_counts[2 * rank] = total;              // exchanged: [pool, distinct labels] per shard
       pool_counts[2 * rank + 1] = st->labels_local;
     } else {
-      st->active_count = total;
+      st->active_count = dead ? 0u : total;
     }
   }
 }
@@ -496,7 +500,7 @@ static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* p
   launch_pdl(k_bits_write, nblocks, kCompactBlock, 0, L.stream, 
       mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
       nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank,
-      mode == 0 ? L.pool_samp : nullptr);
+      mode == 0 ? L.pool_samp : nullptr, L.err);
   ++L.launches;
   return L.cuda_ok(cudaGetLastError(), __FILE__, __LINE__, "k_bits_write");
 }

@@ -3,7 +3,7 @@
 # the three GEMMs of one step (GEMM-F, GEMM-dW, GEMM-dX) and of the row kernels -- each only
 # after the same command has exited 0 without ncu.
 WL=${WL:-c2}
-CMD="python bench.py --steps 3 --warmup 1 --no-cpu-baseline --workload $WL"
+CMD="python bench.py --steps 3 --warmup 1 --e2e-steps 1 --no-cpu-baseline --workload $WL"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_full.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$WL.csv $CMD > gpurun_out/ncu_launches.log 2>&1
