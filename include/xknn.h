@@ -141,6 +141,19 @@ xknn_status_t xknn_step(xknn_layer_t* h, const float* features_local_dev,
                         const uint32_t* labels_local_dev, uint64_t batch_local, float lr,
                         double* loss_dev, float* grad_features_local_dev);
 
+/* xknn_step with StepOptions::micro_batches = micro_batches (parallel.cpp:444, :505-591): one
+   selection and one weight update per step, as the reference; the micro-batches (the balanced
+   split of every rank's B/P rows, min(micro_batches, B/P) of them, 0 meaning 1) share one fused
+   pass on the device -- the loss (sum of weight_c * loss_c = the batch mean) and the weight
+   gradient (sum of scale * weight_c * G_c^T F_c) are the same sums -- and grad_features rows of
+   micro-batch c are the tensor the reference hands to mlp_backward for them, whose softmax
+   gradient carries 1/m_c: the caller scales its feature-extractor gradients by
+   weight_c = m_c / B as the reference does (fe_acc.add_scaled, parallel.cpp:587). */
+xknn_status_t xknn_step_micro(xknn_layer_t* h, const float* features_local_dev,
+                              const uint32_t* labels_local_dev, uint64_t batch_local, float lr,
+                              uint32_t micro_batches, double* loss_dev,
+                              float* grad_features_local_dev);
+
 /* Pipelined selection: starts the NEXT step's label all-gather and active-class selection on
    the layer's side stream now, so that it overlaps the step still in flight (its GEMMs and the
    HBM-bound row update) -- selection depends only on the labels and the graph.  The next

@@ -353,6 +353,23 @@ int ref_sim_set_graphs(void* h, uint64_t p, const uint32_t* const* kpc, const ui
   GUARD(r->sim.set_shard_graphs(shards_of(r->n, p, kpc, off, flat)))
 }
 
+int ref_sim_step_mb(void* h, const float* x, const uint32_t* labels, uint64_t b,
+                    uint64_t m_active, uint64_t seed, float lr, uint64_t micro_batches,
+                    double* loss, uint64_t* active_classes) {
+  auto* r = static_cast<RefSim*>(h);
+  GUARD({
+    LabeledBatch batch{mat(b, r->d, x), std::vector<uint32_t>(labels, labels + b)};
+    StepOptions so;
+    so.mode = SoftmaxMode::kKnn;
+    so.lr = lr;
+    so.micro_batches = micro_batches;
+    so.selection = SelectionConfig{m_active, seed};
+    auto res = r->sim.train_step(batch, so);
+    *loss = res.loss;
+    *active_classes = res.active_classes;
+  })
+}
+
 int ref_sim_step(void* h, const float* x, const uint32_t* labels, uint64_t b, uint64_t m_active,
                  uint64_t seed, float lr, double* loss, uint64_t* active_classes) {
   auto* r = static_cast<RefSim*>(h);

@@ -714,6 +714,130 @@ out_w:
   return rc;
 }
 
+/* The fc half of HybridSim::train_step with `micro_batches` micro-batches (parallel.cpp:444,
+ * :505-591, :638-668): one selection and one normalized W_sub per step; per micro-batch c
+ * (balanced split of every worker's slice, :514-523) the rank-major micro batch of m_c = rows_c*p
+ * rows gets its own logits, distributed softmax (G carries 1/m_c), loss weighted by
+ * weight_c = float(m_c)/float(m) (:553-558), weight-side gradient scaled by scale*weight_c and
+ * accumulated into fc_acc with axpy (:564-566), and feature gradient (:568-585).  The update
+ * runs once, after the last micro-batch (:638-668).  grad_feat row i of worker w's slice is the
+ * gradient handed to mlp_backward for that row (micro-scaled: 1/m_c, not 1/m). */
+int or_fc_train_step_mb(uint64_t n, uint64_t d, uint64_t p, float* w, float* velocity,
+                        const float* x, const uint32_t* labels, uint64_t b,
+                        const uint32_t* const* k_per_class, const uint64_t* const* offsets,
+                        const uint32_t* const* flat, uint64_t m_active, uint64_t seed,
+                        float scale, float lr, float momentum, float wd, uint64_t micro_batches,
+                        double* loss_out, uint32_t* active_out, uint64_t* active_count,
+                        float* grad_feat) {
+  if (b == 0 || b % p != 0) return OR_ERR_INVALID_ARGUMENT;
+  for (uint64_t i = 0; i < b; ++i)
+    if (labels[i] >= n) return OR_ERR_LABEL_OUT_OF_RANGE;
+  const uint64_t slice = b / p;
+  uint64_t micros = micro_batches ? micro_batches : 1;
+  if (micros > slice) micros = slice;
+  int contains_all = 0;
+  int rc = or_select_active_shards(n, p, k_per_class, offsets, flat, labels, b, m_active, seed,
+                                   active_out, active_count, &contains_all);
+  if (rc != OR_OK) return rc;
+  const uint64_t na = *active_count;
+  uint64_t* lo = (uint64_t*)malloc((p + 1) * sizeof(uint64_t));
+  for (uint64_t s = 0; s <= p; ++s) {
+    uint64_t bg, en;
+    if (s < p) or_shard_range(n, p, s, &bg, &en); else bg = n;
+    uint64_t a = 0, z = na;
+    while (a < z) { uint64_t mid = (a + z) / 2; if (active_out[mid] < bg) a = mid + 1; else z = mid; }
+    lo[s] = a;
+  }
+  float* wsub = (float*)malloc((na ? na : 1) * d * sizeof(float));
+  float* wnorm = (float*)malloc((na ? na : 1) * sizeof(float));
+  float* fc_acc = (float*)calloc((na ? na : 1) * d, sizeof(float));
+  float* xm = (float*)malloc(b * d * sizeof(float));
+  float* fhat = (float*)malloc(b * d * sizeof(float));
+  float* fnorm = (float*)malloc(b * sizeof(float));
+  uint32_t* lab_m = (uint32_t*)malloc(b * sizeof(uint32_t));
+  float* fsum = (float*)malloc(b * d * sizeof(float));
+  float* tmp = (float*)malloc(b * d * sizeof(float));
+  float* gfm = (float*)malloc(b * d * sizeof(float));
+  for (uint64_t i = 0; i < na; ++i) {
+    uint64_t bad;
+    if (or_l2_normalize_rows(1, d, w + (uint64_t)active_out[i] * d, 1e-12f, wsub + i * d,
+                             wnorm + i, &bad) != OR_OK) { rc = OR_ERR_ZERO_NORM_ROW; goto out; }
+  }
+  {
+    double loss_sum = 0.0;
+    const uint64_t base = slice / micros, rem = slice % micros;
+    uint64_t off = 0;
+    for (uint64_t c = 0; c < micros && rc == OR_OK; ++c) {
+      const uint64_t rows_c = base + (c < rem ? 1 : 0), mm = rows_c * p;
+      const float weight = (float)mm / (float)b;
+      for (uint64_t wk = 0; wk < p; ++wk)
+        for (uint64_t i = 0; i < rows_c; ++i) {
+          lab_m[wk * rows_c + i] = labels[wk * slice + off + i];
+          memcpy(xm + (wk * rows_c + i) * d, x + (wk * slice + off + i) * d, d * sizeof(float));
+        }
+      uint64_t bad;
+      rc = or_l2_normalize_rows(mm, d, xm, 1e-12f, fhat, fnorm, &bad);
+      if (rc != OR_OK) break;
+      const float** lg = (const float**)malloc(p * sizeof(float*));
+      float** gr = (float**)malloc(p * sizeof(float*));
+      const uint32_t** cl = (const uint32_t**)malloc(p * sizeof(uint32_t*));
+      uint64_t* nc = (uint64_t*)malloc(p * sizeof(uint64_t));
+      for (uint64_t s = 0; s < p; ++s) {
+        nc[s] = lo[s + 1] - lo[s];
+        cl[s] = active_out + lo[s];
+        float* l = (float*)malloc((nc[s] ? nc[s] : 1) * mm * sizeof(float));
+        or_matmul_nt(mm, nc[s], d, fhat, wsub + lo[s] * d, l);
+        for (uint64_t t = 0; t < mm * nc[s]; ++t) l[t] *= scale; /* :551 */
+        lg[s] = l;
+        gr[s] = (float*)malloc((nc[s] ? nc[s] : 1) * mm * sizeof(float));
+      }
+      double loss = 0.0;
+      rc = or_distributed_softmax_xent_cols(p, mm, lg, cl, nc, lab_m, &loss, gr);
+      if (rc == OR_OK) {
+        loss_sum += (double)weight * loss; /* :558 */
+        for (uint64_t s = 0; s < p; ++s) {
+          float* gw = (float*)malloc((nc[s] ? nc[s] : 1) * d * sizeof(float));
+          or_matmul_tn(mm, nc[s], d, gr[s], fhat, gw);
+          const float sw = scale * weight; /* :565 */
+          for (uint64_t t = 0; t < nc[s] * d; ++t) gw[t] *= sw;
+          float* acc = fc_acc + lo[s] * d;
+          for (uint64_t t = 0; t < nc[s] * d; ++t) acc[t] += 1.0f * gw[t]; /* axpy :566 */
+          free(gw);
+          or_matmul_nn(mm, d, nc[s], gr[s], wsub + lo[s] * d, tmp); /* :568-569 */
+          for (uint64_t t = 0; t < mm * d; ++t) tmp[t] *= scale;
+          if (s == 0) memcpy(fsum, tmp, mm * d * sizeof(float));
+          else for (uint64_t t = 0; t < mm * d; ++t) fsum[t] += 1.0f * tmp[t]; /* :572 */
+        }
+        /* each worker's own rows back through the normalization (:574-585) */
+        or_l2_normalize_backward(mm, d, fhat, fnorm, fsum, gfm);
+        for (uint64_t wk = 0; wk < p; ++wk)
+          for (uint64_t i = 0; i < rows_c; ++i)
+            memcpy(grad_feat + (wk * slice + off + i) * d, gfm + (wk * rows_c + i) * d,
+                   d * sizeof(float));
+      }
+      for (uint64_t s = 0; s < p; ++s) { free((void*)lg[s]); free(gr[s]); }
+      free(lg); free(gr); free(cl); free(nc);
+      off += rows_c;
+    }
+    if (rc == OR_OK) {
+      *loss_out = loss_sum;
+      /* the update, once (:638-668) */
+      float* graw = (float*)malloc((na ? na : 1) * d * sizeof(float));
+      for (uint64_t s = 0; s < p; ++s) {
+        const uint64_t ns = lo[s + 1] - lo[s];
+        or_l2_normalize_backward(ns, d, wsub + lo[s] * d, wnorm + lo[s], fc_acc + lo[s] * d,
+                                 graw);
+        or_sgd_step_rows(d, w, graw, velocity, active_out + lo[s], ns, lr, momentum, wd);
+      }
+      free(graw);
+    }
+  }
+out:
+  free(lo); free(wsub); free(wnorm); free(fc_acc); free(xm); free(fhat); free(fnorm);
+  free(lab_m); free(fsum); free(tmp); free(gfm);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* DGC sparsification (sparsify.cpp), beside the fc path                      */
 /* ------------------------------------------------------------------------- */

@@ -60,6 +60,13 @@ int or_fc_train_step(uint64_t n, uint64_t d, uint64_t p, float* w, float* veloci
                      const uint32_t* const* flat, uint64_t m_active, uint64_t seed, float scale,
                      float lr, float momentum, float wd, double* loss_out, uint32_t* active_out,
                      uint64_t* active_count, float* grad_feat, float* logits_out);
+int or_fc_train_step_mb(uint64_t n, uint64_t d, uint64_t p, float* w, float* velocity,
+                        const float* x, const uint32_t* labels, uint64_t b,
+                        const uint32_t* const* k_per_class, const uint64_t* const* offsets,
+                        const uint32_t* const* flat, uint64_t m_active, uint64_t seed,
+                        float scale, float lr, float momentum, float wd, uint64_t micro_batches,
+                        double* loss_out, uint32_t* active_out, uint64_t* active_count,
+                        float* grad_feat);
 /* raw mt19937_64 / uniform_int stream, for testing the device generator */
 void or_mt64_stream(uint64_t seed, uint64_t count, uint64_t* out);
 void or_uniform_picks(uint64_t seed, uint64_t csize, uint64_t need, uint64_t* out);

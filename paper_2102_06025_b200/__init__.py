@@ -102,6 +102,7 @@ for _name, _args in {
     "xknn_layer_set_graph_csr": [VP, VP, VP, VP, U64, C.c_int],
     "xknn_select": [VP, VP, U64, VP, C.POINTER(U64), C.POINTER(C.c_int)],
     "xknn_step": [VP, VP, VP, U64, C.c_float, VP, VP],
+    "xknn_step_micro": [VP, VP, VP, U64, C.c_float, C.c_uint32, VP, VP],
     "xknn_prepare": [VP, VP, U64, VP],
     "xknn_layer_sync": [VP],
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
@@ -476,17 +477,24 @@ class KnnSoftmaxLayer:
                                  ready_stream.cuda_stream if ready_stream is not None else None))
 
     def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
-                   loss_out=None, sync: bool = True):
-        """The fc half of HybridSim::train_step (kKnn, one micro-batch) for this rank's rows.
+                   loss_out=None, sync: bool = True, micro_batches: int = 1):
+        """The fc half of HybridSim::train_step (kKnn) for this rank's rows, with
+        StepOptions::micro_batches = micro_batches (xknn_step_micro: grad_features rows of
+        micro-batch c are the reference's micro-scaled mlp_backward input).
         Returns the mean loss (float) when sync, else None (loss in loss_out/self._loss)."""
         torch = self._torch
         assert features_local.dtype == torch.float32 and features_local.is_contiguous()
         lab = labels_local if labels_local.dtype == torch.int32 else labels_local.to(torch.int32)
         loss = self._loss if loss_out is None else loss_out
         self._enter()
-        _check(_lib.xknn_step(self.h, features_local.data_ptr(), lab.data_ptr(),
-                              features_local.shape[0], float(lr), loss.data_ptr(),
-                              _ptr(grad_features_local)))
+        if micro_batches == 1:
+            _check(_lib.xknn_step(self.h, features_local.data_ptr(), lab.data_ptr(),
+                                  features_local.shape[0], float(lr), loss.data_ptr(),
+                                  _ptr(grad_features_local)))
+        else:
+            _check(_lib.xknn_step_micro(self.h, features_local.data_ptr(), lab.data_ptr(),
+                                        features_local.shape[0], float(lr), int(micro_batches),
+                                        loss.data_ptr(), _ptr(grad_features_local)))
         self._leave()
         if sync:
             _check(_lib.xknn_layer_sync(self.h))

@@ -20,7 +20,8 @@ cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
                                     const float* wnorm, const float* lr, float mu, float wd,
                                     const unsigned long long* err, cudaStream_t s);
 cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
-                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s);
+                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s,
+                                    uint32_t micros = 1);
 
 // exact.cu
 cudaError_t launch_logits_exact(const float* xhat, const float* wsub, uint64_t rows,

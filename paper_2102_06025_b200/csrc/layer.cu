@@ -447,7 +447,8 @@ xknn_status_t Layer::run_prepare(const uint32_t* labels_local, uint64_t bl, cuda
 }
 
 xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_local,
-                              uint64_t bl, float lr, double* loss_out, float* gfeat_local) {
+                              uint64_t bl, float lr, double* loss_out, float* gfeat_local,
+                              uint32_t micros) {
   const uint64_t B = bl * world;
   const uint32_t D = (uint32_t)d;
   last_b = B;
@@ -496,7 +497,7 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   // (6) feature normalize-backward on this rank's rows (parallel.cpp:574-585)
   if (gfeat_local) {
     XK_CUDA(launch_feature_backward(X + (uint64_t)rank * bl * d, xnorm + (uint64_t)rank * bl, dX,
-                                    bl, D, gfeat_local, stream));
+                                    bl, D, gfeat_local, stream, micros));
     ++launches;
   }
   mark(10);
@@ -798,14 +799,20 @@ xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local, uint64
   return L.run_prepare(labels_local, bl, static_cast<cudaStream_t>(ready_stream));
 }
 
-xknn_status_t xknn_step(xknn_layer_t* h, const float* feats, const uint32_t* labels,
-                        uint64_t bl, float lr, double* loss_dev, float* gfeat) {
+xknn_status_t xknn_step_micro(xknn_layer_t* h, const float* feats, const uint32_t* labels,
+                              uint64_t bl, float lr, uint32_t micro_batches, double* loss_dev,
+                              float* gfeat) {
   GUARD_H(h);
   Layer& L = h->L;
   if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: knn mode without shard graphs");
   if (bl == 0 || bl * L.world > L.bmax)
     return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: batch size must be a positive multiple of P (<= max_batch)");
-  return L.run_step(feats, labels, bl, lr, loss_dev, gfeat);
+  return L.run_step(feats, labels, bl, lr, loss_dev, gfeat, micro_batches);
+}
+
+xknn_status_t xknn_step(xknn_layer_t* h, const float* feats, const uint32_t* labels,
+                        uint64_t bl, float lr, double* loss_dev, float* gfeat) {
+  return xknn_step_micro(h, feats, labels, bl, lr, 1, loss_dev, gfeat);
 }
 
 xknn_status_t xknn_layer_sync(xknn_layer_t* h) {

@@ -173,7 +173,7 @@ struct Layer {
   xknn_status_t ensure_graph(uint64_t batch);
   xknn_status_t wait_features();
   xknn_status_t run_step(const float* feats_local, const uint32_t* labels_local,
-                         uint64_t batch_local, float lr, double* loss_out, float* gfeat_local);
+                         uint64_t batch_local, float lr, double* loss_out, float* gfeat_local, uint32_t micros = 1);
   xknn_status_t nccl_ok(ncclResult_t r);
   xknn_status_t cuda_ok(cudaError_t e, const char* file = "", int line = 0,
                         const char* expr = "");

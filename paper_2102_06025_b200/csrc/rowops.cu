@@ -151,14 +151,21 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
 // gfeat = l2_normalize_backward(x_hat, norms, g) for this rank's rows; x_hat recomputed from the
 // raw features exactly as the forward did.
 template <int DV>
+// micros > 1: row r of the rank's slice belongs to micro-batch c of the balanced split
+// (parallel.cpp:514-523), whose softmax gradient carries 1/m_c instead of 1/m; the gradient the
+// reference hands to mlp_backward for that row is this one times m/m_c = rows/rows_c.
 __global__ void k_feature_backward(const float* __restrict__ X, const float* __restrict__ xnorm,
                                    const float* __restrict__ G, uint64_t rows, uint32_t d,
-                                   float* __restrict__ out) {
+                                   float* __restrict__ out, uint32_t micros) {
   griddep_wait();
   griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
+  const uint64_t mb = micros > rows ? rows : (micros ? micros : 1);
+  const uint64_t mbase = rows / mb, mrem = rows % mb;
   for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
        r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t rows_c = r < mrem * (mbase + 1) ? mbase + 1 : mbase;
+    const float mf = mb > 1 ? (float)((double)rows / (double)rows_c) : 1.0f;
     const float norm = xnorm[r];
     const float inv = 1.0f / norm;
     const float4* xp = reinterpret_cast<const float4*>(X + r * d);
@@ -169,6 +176,12 @@ __global__ void k_feature_backward(const float* __restrict__ X, const float* __r
     for (int c = 0; c < DV; ++c) {
       const float4 x = xp[lane + 32 * c];
       g[c] = gp[lane + 32 * c];
+      if (mb > 1) {
+        g[c].x = __fmul_rn(g[c].x, mf);
+        g[c].y = __fmul_rn(g[c].y, mf);
+        g[c].z = __fmul_rn(g[c].z, mf);
+        g[c].w = __fmul_rn(g[c].w, mf);
+      }
       nh[c].x = __fmul_rn(x.x, inv);
       nh[c].y = __fmul_rn(x.y, inv);
       nh[c].z = __fmul_rn(x.z, inv);
@@ -237,9 +250,10 @@ cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
 }
 
 cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
-                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s) {
+                                    uint64_t rows, uint32_t d, float* out, cudaStream_t s,
+                                    uint32_t micros) {
   const unsigned grid = grid_for(rows * 32, 256);
-  XKNN_DISPATCH_D(d, k_feature_backward, grid, 256, s, X, xnorm, G, rows, d, out);
+  XKNN_DISPATCH_D(d, k_feature_backward, grid, 256, s, X, xnorm, G, rows, d, out, micros);
   return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--prepare", action="store_true", help="pipelined selection (xknn_prepare)")
+    ap.add_argument("--micro", type=int, default=1, help="StepOptions::micro_batches")
     args = ap.parse_args()
 
     import torch
@@ -69,7 +70,8 @@ def main():
         if args.prepare:
             layer.prepare(ys)
         gf = torch.empty(bl, d, device="cuda")
-        res[f"loss_{s}"] = layer.train_step(xs, ys, 0.1, grad_features_local=gf)
+        res[f"loss_{s}"] = layer.train_step(xs, ys, 0.1, grad_features_local=gf,
+                                            micro_batches=args.micro)
         res[f"gf_{s}"] = gf.cpu().numpy()
     res["w"] = layer.weights().cpu().numpy()
     np.savez(os.path.join(args.out, f"rank{rank}.npz"), **res)

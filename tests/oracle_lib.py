@@ -51,6 +51,8 @@ def ref() -> C.CDLL:
                                         f32p]
         _ref.ref_sim_step.argtypes = [C.c_void_p, f32p, u32p, U64, U64, U64, C.c_float,
                                       C.POINTER(C.c_double), C.POINTER(U64)]
+        _ref.ref_sim_step_mb.argtypes = [C.c_void_p, f32p, u32p, U64, U64, U64, C.c_float, U64,
+                                         C.POINTER(C.c_double), C.POINTER(U64)]
         _ref.ref_sim_get_weights.argtypes = [C.c_void_p, f32p]
         _ref.ref_sim_destroy.argtypes = [C.c_void_p]
         _ref.ref_sim_set_graphs.argtypes = [C.c_void_p, U64, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -187,6 +189,31 @@ def fc_train_step(w: np.ndarray, vel: np.ndarray, x: np.ndarray, labels: np.ndar
     return rc, loss.value, act, gfeat, logits
 
 
+def fc_train_step_mb(w: np.ndarray, vel: np.ndarray, x: np.ndarray, labels: np.ndarray, shards,
+                     m: int, seed: int, micro: int, scale=30.0, lr=0.1, momentum=0.9, wd=0.0):
+    """Oracle fc half of HybridSim::train_step with `micro` micro-batches (or_fc_train_step_mb).
+    Updates w and vel in place; returns (rc, loss, active, grad_feat)."""
+    n, d = w.shape
+    b = x.shape[0]
+    p = len(shards)
+    active = np.zeros(max(m, 1), np.uint32)
+    cnt = U64(0)
+    loss = C.c_double(0)
+    gfeat = np.zeros((b, d), np.float32)
+    fn = oracle().or_fc_train_step_mb
+    fn.restype = C.c_int
+    fn.argtypes = [U64, U64, U64, f32p, f32p, f32p, u32p, U64, C.c_void_p, C.c_void_p,
+                   C.c_void_p, U64, U64, C.c_float, C.c_float, C.c_float, C.c_float, U64,
+                   C.POINTER(C.c_double), u32p, C.POINTER(U64), f32p]
+    flats = [s[2] if s[2].size else np.zeros(1, np.uint32) for s in shards]
+    rc = fn(n, d, p, w, vel, np.ascontiguousarray(x, np.float32),
+            np.ascontiguousarray(labels, np.uint32), b,
+            _ptr_array([s[0] for s in shards], None), _ptr_array([s[1] for s in shards], None),
+            _ptr_array(flats, None), m, seed, scale, lr, momentum, wd, micro, C.byref(loss),
+            active, C.byref(cnt), gfeat)
+    return rc, loss.value, active[: cnt.value].copy(), gfeat
+
+
 def bruteforce_graph(lib_kind: str, w_norm: np.ndarray, k: int):
     n, d = w_norm.shape
     out = np.zeros((n, k), np.uint32)
@@ -251,6 +278,17 @@ class RefSim:
                                       _ptr_array([s[1] for s in shards], None),
                                       _ptr_array(flats, None))
         assert rc == 0
+
+    def step_mb(self, x, labels, m, seed, micro, lr=0.1, reset_fe=True):
+        """train_step with StepOptions::micro_batches = micro (parallel.cpp:444)."""
+        if reset_fe:
+            assert ref().ref_sim_reset_fe(C.c_void_p(self.h)) == 0
+        loss = C.c_double(0)
+        na = U64(0)
+        rc = ref().ref_sim_step_mb(self.h, np.ascontiguousarray(x, np.float32),
+                                   np.ascontiguousarray(labels, np.uint32), x.shape[0], m, seed,
+                                   lr, micro, C.byref(loss), C.byref(na))
+        return rc, loss.value, na.value
 
     def step(self, x, labels, m, seed, lr=0.1, reset_fe=True):
         if reset_fe:

@@ -63,6 +63,44 @@ def test_multi_gpu_step(p, m, precision, tol_loss, tol_g, tmp_path):
     assert np.array_equal(wg[untouched], w[untouched])
 
 
+@pytest.mark.parametrize("p,micro", [(2, 3), (4, 2)])
+def test_multi_gpu_micro_batches(p, micro, tmp_path):
+    """StepOptions::micro_batches over P ranks: each rank's slice splits into the same balanced
+    micro-batches (parallel.cpp:514-523); loss, weights and the micro-scaled feature gradients
+    against the oracle's micro-batch step."""
+    if _ngpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    n, b, k, m, steps = 40_003, 240, 10, 4_000, 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr=127.0.0.1", f"--master-port={29580 + p}",
+           os.path.join(HERE, "mp_worker.py"), "--out", str(tmp_path), "--num-classes", str(n),
+           "--batch", str(b), "--knn", str(k), "--m-active", str(m), "--steps", str(steps),
+           "--precision", "bf16", "--micro", str(micro)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{i}.npz")) for i in range(p)]
+
+    from mp_worker import problem
+
+    w, g = problem(n, 512, k, 7)
+    shards = [O.compress(g, p, s) for s in range(p)]
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    rng = np.random.default_rng(99)
+    for s in range(steps):
+        x = rng.standard_normal((b, 512)).astype(np.float32)
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        rc, loss_or, act, gf_or = O.fc_train_step_mb(w_or, v_or, x, lab, shards, m, 42, micro)
+        assert rc == 0
+        for r in res:
+            assert abs(float(r[f"loss_{s}"]) - loss_or) <= 2e-4 * abs(loss_or)
+        gf = np.concatenate([r[f"gf_{s}"] for r in res])
+        assert rel_err(gf, gf_or) <= 1e-2
+    wg = np.concatenate([r["w"] for r in res])
+    assert rel_err(wg - w, w_or - w) <= 1e-2
+    untouched = np.all(w_or == w, axis=1)
+    assert np.array_equal(wg[untouched], w[untouched])
+
+
 @pytest.mark.parametrize("p", [2, 4])
 def test_multi_gpu_prepared_selection(p, tmp_path):
     """xknn_prepare over P ranks (selection collectives on the split communicator, on the side

@@ -186,3 +186,49 @@ def test_step_with_prepared_selection(precision):
     wg = layer.weights().cpu().numpy()
     assert rel_err(wg - w, w_or - w) <= (1e-2 if precision == "bf16" else 1e-5)
     layer.close()
+
+
+@pytest.mark.parametrize("precision,micro,b", [("fp32", 2, 64), ("fp32", 3, 50), ("bf16", 4, 256),
+                                               ("bf16", 7, 100)])
+def test_step_micro_batches(precision, micro, b):
+    """StepOptions::micro_batches (parallel.cpp:444, :505-591) through xknn_step_micro against the
+    oracle's micro-batch step (bit-exact with the stock HybridSim, tests/test_oracle.py): loss,
+    weights, velocity, and the per-micro-batch feature gradient handed to mlp_backward."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    prec = X.PREC_FP32_EXACT if precision == "fp32" else X.PREC_BF16
+    tol_l, tol_g = (1e-5, 1e-5) if precision == "fp32" else (2e-4, 1e-2)
+    n, d, k, m, seed = 20_000, 512, 10, 2_000, 42
+    rng = np.random.default_rng(micro + b)
+    w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 3)
+    shards = [O.compress(g, 1, 0)]
+    layer = make_layer(n, d, 1, 0, m, b, w, g, precision=prec, seed=seed)
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    for _ in range(2):
+        x = rng.standard_normal((b, d)).astype(np.float32)
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        rc, loss_or, act, gf_or = O.fc_train_step_mb(w_or, v_or, x, lab, shards, m, seed, micro)
+        assert rc == 0
+        gf = torch.empty(b, d, device="cuda")
+        loss = layer.train_step(torch.from_numpy(x).cuda(),
+                                torch.from_numpy(lab.view(np.int32)).cuda(), 0.1,
+                                grad_features_local=gf, micro_batches=micro)
+        assert abs(loss - loss_or) <= tol_l * abs(loss_or), (loss, loss_or)
+        gfn = gf.cpu().numpy()
+        assert rel_err(gfn, gf_or) <= tol_g
+        # per micro-batch too: each carries its own 1/m_c
+        base, rem = divmod(b, micro)
+        off = 0
+        for c in range(micro):
+            rc_ = base + (1 if c < rem else 0)
+            assert rel_err(gfn[off:off + rc_], gf_or[off:off + rc_]) <= tol_g
+            off += rc_
+    wg = layer.weights().cpu().numpy()
+    vg = layer.velocity().cpu().numpy()
+    layer.close()
+    assert rel_err(wg - w, w_or - w) <= tol_g
+    assert rel_err(vg, v_or) <= tol_g
+    untouched = np.all(w_or == w, axis=1)
+    assert np.array_equal(wg[untouched], w[untouched])

@@ -148,6 +148,62 @@ def test_ref_fc_step_and_feature_grad(p):
         assert rc3 == 0 and loss3 == loss_o and np.array_equal(gref, gfeat)
 
 
+def _micro_rows(b, p, micro):
+    """Rank-major row lists of each micro-batch (parallel.cpp:514-523)."""
+    sl = b // p
+    mc = min(micro, sl)
+    base, rem = divmod(sl, mc)
+    out, off = [], 0
+    for c in range(mc):
+        rc = base + (1 if c < rem else 0)
+        out.append(np.array([w * sl + off + i for w in range(p) for i in range(rc)]))
+        off += rc
+    return out
+
+
+def test_oracle_micro_step_one_micro_is_the_plain_step():
+    rng = np.random.default_rng(3)
+    n, d, b, k, m, p = 3000, 64, 40, 6, 300, 2
+    w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 9)
+    shards = [O.compress(g, p, s) for s in range(p)]
+    x = rng.standard_normal((b, d)).astype(np.float32)
+    lab = rng.integers(0, n, b).astype(np.uint32)
+    w1, v1, w2, v2 = w.copy(), np.zeros_like(w), w.copy(), np.zeros_like(w)
+    rc1, l1, a1, g1, _ = O.fc_train_step(w1, v1, x, lab, shards, m, 5)
+    rc2, l2, a2, g2 = O.fc_train_step_mb(w2, v2, x, lab, shards, m, 5, 1)
+    assert rc1 == rc2 == 0 and l1 == l2 and np.array_equal(a1, a2)
+    assert np.array_equal(w1, w2) and np.array_equal(v1, v2) and np.array_equal(g1, g2)
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("p,micro", [(1, 2), (1, 5), (2, 3), (4, 2)])
+def test_ref_fc_step_micro_batches(p, micro):
+    """StepOptions::micro_batches > 1 (parallel.cpp:444, :505-591): the oracle matches the stock
+    HybridSim bit for bit in loss and weights, and its per-micro-batch feature gradient matches
+    the reference's free functions composed on each micro-batch."""
+    rng = np.random.default_rng(17 + p + micro)
+    n, d, b, k, m = 4000, 64, 48, 8, 400
+    w = (rng.standard_normal((n, d)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, p)
+    shards = [O.compress(g, p, s) for s in range(p)]
+    sim = O.RefSim(w, p)
+    sim.set_graphs(shards)
+    w2, v2 = w.copy(), np.zeros_like(w)
+    for _ in range(2):
+        x = rng.standard_normal((b, d)).astype(np.float32)
+        lab = rng.integers(0, n, b).astype(np.uint32)
+        w_before = w2.copy()
+        rc, loss_r, na = sim.step_mb(x, lab, m, 42, micro)
+        rc2, loss_o, act, gfeat = O.fc_train_step_mb(w2, v2, x, lab, shards, m, 42, micro)
+        assert rc == 0 and rc2 == 0 and na == act.size
+        assert loss_r == loss_o
+        assert np.array_equal(sim.weights(), w2)
+        for rows in _micro_rows(b, p, micro):
+            rc3, _, gref = O.ref_feature_grad(w_before, x[rows], lab[rows], act, p)
+            assert rc3 == 0 and np.array_equal(gref, gfeat[rows])
+
+
 @pytest.mark.ref
 def test_ref_graph_builders():
     rng = np.random.default_rng(1)
