@@ -84,7 +84,9 @@ template <>
 struct Cfg2<kDW> {
   static constexpr uint32_t STAGES = 6, A_BYTES = 2 * 64 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
   static constexpr uint32_t ARES_BYTES = 0;
-  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = 2;  // TMA-store staging
+  // bf16 output: 2 KB per 32x32 chunk, four chunks in flight per warp (the accumulator is
+  // single-buffered, so the drain's store waits sit on the MMA's critical path)
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 2048, NSTG = 4;
 };
 
 template <>
@@ -568,8 +570,8 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_store_2d(&tmOut, stg + sbuf * C::STG, c0, r0);
         tc::tma_store_commit();
       }
-      sbuf ^= 1;
-      if (lane == 0) tc::tma_store_wait_read<1>();  // the buffer written next is free again
+      sbuf = sbuf + 1 == C::NSTG ? 0 : sbuf + 1;
+      if (lane == 0) tc::tma_store_wait_read<(C::NSTG > 1 ? (int)C::NSTG - 1 : 0)>();  // next buffer free
       __syncwarp();
     };
     for (uint32_t u = pair; u < nunits; u += npairs) {
