@@ -109,7 +109,7 @@ __device__ __forceinline__ bool before(float sa, uint32_t ia, float sb, uint32_t
   return ia < ib;
 }
 
-// Pilot seed, one warp per row: after the pilot pass against a strided sample of the own block,
+// Pilot seed, one warp per row: after the pilot pass against a strided sample of all classes,
 // the row's cut starts at the j-th best approximate sample score (the list is emptied; every
 // column is scanned again by the main pass).  A cut is only ever a bound on what was left out,
 // so any starting value is correct; a too-high one shows up as an uncertified row (exact
@@ -583,15 +583,32 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   k_list_init<<<grid_for(n, 256), 256, 0, s>>>(lcnt, lcut, n);
   G_CUDA(cudaGetLastError());
   {
-    // pilot: seed every row's cut from a strided sample of the own block (k_seed_cut)
-    const uint32_t stride = 32, jseed = 18;
-    const uint32_t ns = n / stride;
+    // pilot: seed every row's cut from a 1-in-32 strided sample of ALL classes (k_seed_cut):
+    // every rank samples 1 in 32*P of its block and the samples are all-gathered
+    uint64_t minrows = ~0ull;
+    for (int r = 0; r < world; ++r) {
+      uint64_t rb, re;
+      shard_range_of(n_total, world, r, &rb, &re);
+      minrows = std::min(minrows, re - rb);
+    }
+    const uint32_t jseed = 18, stride = 32u * (uint32_t)world;
+    const uint32_t ns_r = (uint32_t)(minrows / stride), ns = ns_r * (uint32_t)world;
     if (ns >= 4096 && !getenv("XKNN_NO_PILOT")) {
       const uint32_t nspad = (ns + 255) / 256 * 256;
       __half* s16 = nullptr;
       G_CUDA(mem.get(&s16, (uint64_t)nspad * 512));
-      k_sample_rows<<<grid_for((uint64_t)nspad * 64, 256), 256, 0, s>>>(own16, stride, ns, nspad,
-                                                                         s16);
+      if (world == 1) {
+        k_sample_rows<<<grid_for((uint64_t)nspad * 64, 256), 256, 0, s>>>(own16, stride, ns,
+                                                                           nspad, s16);
+      } else {
+        k_sample_rows<<<grid_for((uint64_t)ns_r * 64, 256), 256, 0, s>>>(
+            own16, stride, ns_r, ns_r, s16 + (uint64_t)rank * ns_r * 512);
+        G_CUDA(cudaGetLastError());
+        G_NCCL(ncclAllGather(s16 + (uint64_t)rank * ns_r * 512, s16, (size_t)ns_r * 512,
+                             ncclFloat16, comm, s));
+        if (nspad > ns)
+          G_CUDA(cudaMemsetAsync(s16 + (uint64_t)ns * 512, 0, (size_t)(nspad - ns) * 1024, s));
+      }
       G_CUDA(cudaGetLastError());
       // sample ids lie above every class id: the row itself is not masked (its score only
       // lowers the seed by one rank)
