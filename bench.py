@@ -449,7 +449,23 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
     return res
 
 
+_JSON_OUT = None
+
+
+def emit(obj) -> None:
+    """The one JSON line of this run, on the process's original stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def main():
+    # stdout carries exactly one JSON line: everything else written to fd 1 -- NCCL's version
+    # banner, library logs, prints -- is sent to stderr; emit() writes to the saved stdout
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -473,7 +489,7 @@ def main():
         if rank != 0:
             return
         r = reference_cpu(wl, args.steps, args.warmup)
-        print(json.dumps({
+        emit({
             "impl": "reference",
             "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
                       "B200 vs roofline",
@@ -486,7 +502,7 @@ def main():
             "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": round(r["value"], 3), "unit": "samples/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }), flush=True)
+        })
         return
 
     dist = None
@@ -511,7 +527,7 @@ def main():
                                    "kind": "reference",
                                    "sample": "not run: reference needs >80 GB host RAM and "
                                              "~10 min/step beyond c2 (SURVEY 7.7)"}
-        print(json.dumps(res), flush=True)
+        emit(res)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
