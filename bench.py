@@ -363,6 +363,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             copy_in(j + 1)
             with torch.cuda.stream(stream):
                 layer.prepare(dys[(j + 1) % 2], ready_stream=copy_stream)
+    e2e_enqueue_ms = (time.perf_counter() - t0) * 1e3  # host time to issue every step
     stream.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
@@ -428,6 +429,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                        "l2": "per-step working set > 126 MB L2 (weight shard, P~ bf16)"},
             "e2e": {"value": round(b / (e2e_ms / e2e_steps / 1e3), 1), "unit": "samples/s",
                     "steps": e2e_steps,
+                    "host_issue_ms_per_step": round(e2e_enqueue_ms / e2e_steps, 4),
                     "h2d_bytes_per_step": int(b_local * D * 4 + b_local * 4),
                     "d2h_bytes_per_step": 8,
                     "how": "host wall clock over a pipelined loop: per step H2D of the rank's "
