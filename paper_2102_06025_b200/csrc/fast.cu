@@ -1100,14 +1100,17 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   auto* f = static_cast<FastState*>(fast);
   const uint32_t D = (uint32_t)d;
   if (B > f->bpad) return XKNN_ERR_INVALID_ARGUMENT;
-  // (a) operands: X_hat (bf16) + norms; gathered, normalized active rows of W (bf16) + norms
-  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, nullptr, Xhat16, xnorm, err, stream));
-  ++launches;
+  // (a) operands: gathered, normalized active rows of W (bf16) + norms -- independent of the
+  //     features, so at P > 1 the feature all-gather (side stream) runs under it -- then
+  //     X_hat (bf16) + norms
   XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, nullptr, Wsub16,
                                 wnorm, err, stream));
   ++launches;
   launch_pdl(k_zero_rows_bf16, 64, 256, 0, stream, st, Wsub16, f->mwpad, D);
   XK_LAUNCH();
+  if (world > 1) XK_TRY(wait_features());
+  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, nullptr, Xhat16, xnorm, err, stream));
+  ++launches;
 
   mark(3);
   GemmArgs ga{};

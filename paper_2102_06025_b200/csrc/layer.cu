@@ -253,7 +253,8 @@ xknn_status_t Layer::run_core(uint64_t B) {
   unsigned int* cnt = &st->active_count;
   // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
   // whole shard as parallel.cpp:490-492 does -- row-wise identical)
-  if (world > 1) XK_TRY(wait_features());
+  // (the BF16 core waits for the feature all-gather only after its weight-row gather)
+  if (world > 1 && cfg.precision == XKNN_PREC_FP32_EXACT) XK_TRY(wait_features());
   if (cfg.precision == XKNN_PREC_FP32_EXACT) {
     XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, Xhat, nullptr, xnorm, err, stream));
     ++launches;
