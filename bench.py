@@ -456,6 +456,20 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             "loss": loss_v,
             "active_classes": int(active_total),
         }
+        if world > 1:
+            # N = 1 runs C2 (the largest single-GPU config, BASELINE configs[1]); this line's
+            # workload also runs on one GPU, measured separately -- the base of its strong scaling
+            ref1 = os.path.join(ROOT, "profiles", "r01d", f"bench_{wl_name}_1gpu.json")
+            if os.path.exists(ref1):
+                try:
+                    d1 = json.load(open(ref1))
+                    res["same_workload_1gpu"] = {
+                        "value": d1["value"], "ms_per_step": d1["ms_per_step"],
+                        "strong_scaling_efficiency": round(value / (world * d1["value"]), 4),
+                        "source": f"profiles/r01d/bench_{wl_name}_1gpu.json "
+                                  f"(bench.py --workload {wl_name}, one B200, another box)"}
+                except (OSError, KeyError, ValueError):
+                    pass
     return res
 
 
