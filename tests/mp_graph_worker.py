@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--num-classes", dest="n", type=int, default=3000)
     ap.add_argument("--knn", dest="k", type=int, default=10)
+    ap.add_argument("--ring-only", action="store_true",
+                    help="random unit rows, graph_ring only (large-n runs checked on sampled rows)")
     args = ap.parse_args()
 
     import torch
@@ -42,12 +44,20 @@ def main():
     dist.broadcast_object_list(uid, src=0)
     comm = X.nccl_comm_init(uid[0], world, rank)
     n, k = args.n, args.k
-    w = problem(n, 5)
+    w = (np.random.default_rng(5).standard_normal((n, 512)).astype(np.float32) if args.ring_only
+         else problem(n, 5))
     rc, wn, _, _ = O.l2_normalize(w)
     assert rc == 0
     b, e = O.shard_range(n, world, rank)
     rows, unc, steps = X.graph_ring(torch.from_numpy(np.ascontiguousarray(wn[b:e])).cuda(), n, k,
                                     2 * k, rank, world, comm)
+    if args.ring_only:
+        np.savez(os.path.join(args.out, f"graph{rank}.npz"),
+                 rows=rows.cpu().numpy().view(np.uint32), unc=unc, steps=steps)
+        X.nccl_comm_destroy(comm)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     layer = X.KnnSoftmaxLayer(n, 512, rank=rank, world=world, m_active=n // 10, max_batch=64,
                               rng_seed=42, comm=comm)
     layer.set_weights(torch.from_numpy(np.ascontiguousarray(w[b:e])).cuda())

@@ -68,6 +68,20 @@ def _dup_weights(seed, n_base, n_rand, scale=0.05):
     return (w * scale).astype(np.float32)
 
 
+def test_graph_pilot_chunked_sampled_rows():
+    """n > 131072 on one GPU: the pilot seeds the cuts (1-in-32 sample) and the candidate pass
+    runs chunk-major over three 64K-column chunks; sampled rows bit-exact vs the oracle."""
+    import paper_2102_06025_b200 as X
+
+    n, k = 140_000, 24
+    wn = _normalized(np.random.default_rng(21).standard_normal((n, 512)).astype(np.float32))
+    got, unc = _device_graph(wn, k, 64)
+    for j in np.random.default_rng(4).integers(0, n, 16):
+        assert np.array_equal(got[j], O.graph_row(wn, int(j), k)), j
+    assert unc < n // 1000
+    X.release_graph_cache()  # the cached build scratch goes back to the driver
+
+
 def test_layer_rebuild_graph_single_gpu():
     """xknn_layer_rebuild_graph == compress_graph(build_graph_bruteforce(l2_normalize_rows(W)))
     and the rebuilt graph drives selection exactly like the reference's."""

@@ -102,6 +102,30 @@ def test_multi_gpu_micro_batches(p, micro, tmp_path):
 
 
 @pytest.mark.parametrize("p", [2, 4])
+def test_multi_gpu_graph_ring_large_sampled(p, tmp_path):
+    """The ring at 140K rows per GPU: the all-gathered pilot sample seeds the cuts and the
+    candidate pass runs chunk-major over several 64K-column chunks; sampled rows bit-exact
+    against build_graph_bruteforce's row (oracle), almost every row certified."""
+    if _ngpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    n, k = 140_000 * p, 24
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr=127.0.0.1", f"--master-port={29670 + p}",
+           os.path.join(HERE, "mp_graph_worker.py"), "--out", str(tmp_path), "--num-classes",
+           str(n), "--knn", str(k), "--ring-only"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"graph{i}.npz")) for i in range(p)]
+    rows = np.concatenate([x["rows"] for x in res])
+    assert rows.shape == (n, k)
+    rc, wn, _, _ = O.l2_normalize(np.random.default_rng(5).standard_normal((n, 512)).astype(np.float32))
+    assert rc == 0
+    for j in np.random.default_rng(3).integers(0, n, 16):
+        assert np.array_equal(rows[j], O.graph_row(wn, int(j), k)), j
+    assert sum(int(x["unc"]) for x in res) < n // 1000
+
+
+@pytest.mark.parametrize("p", [2, 4])
 def test_multi_gpu_prepared_selection(p, tmp_path):
     """xknn_prepare over P ranks (selection collectives on the split communicator, on the side
     stream): same ActiveSets, losses and weights as the oracle."""

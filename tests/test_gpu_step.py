@@ -232,3 +232,27 @@ def test_step_micro_batches(precision, micro, b):
     assert rel_err(vg, v_or) <= tol_g
     untouched = np.all(w_or == w, axis=1)
     assert np.array_equal(wg[untouched], w[untouched])
+
+
+def test_step_loss_into_pinned_host_memory():
+    """train_step's loss written straight into pinned host memory (the e2e loop's path) equals
+    the device-memory loss of the same step."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    n, b, k, m = 20_000, 128, 10, 2_000
+    rng = np.random.default_rng(8)
+    w = (rng.standard_normal((n, 512)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 3)
+    x = torch.from_numpy(rng.standard_normal((b, 512)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, n, b).astype(np.int32)).cuda()
+    out = []
+    for dest in ("cuda", "pinned"):
+        layer = make_layer(n, 512, 1, 0, m, b, w, g, precision=X.PREC_BF16, seed=42)
+        buf = (torch.zeros(1, dtype=torch.float64, device="cuda") if dest == "cuda"
+               else torch.zeros(1, dtype=torch.float64).pin_memory())
+        layer.train_step(x, lab, 0.1, loss_out=buf, sync=False)
+        layer.sync()
+        out.append(float(buf.cpu()[0]))
+        layer.close()
+    assert out[0] == out[1] and np.isfinite(out[0]) and out[0] > 0
