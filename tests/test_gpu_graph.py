@@ -70,7 +70,7 @@ def _dup_weights(seed, n_base, n_rand, scale=0.05):
 
 def test_graph_pilot_chunked_sampled_rows():
     """n > 131072 on one GPU: the pilot seeds the cuts (1-in-32 sample) and the candidate pass
-    runs chunk-major over three 64K-column chunks; sampled rows bit-exact vs the oracle."""
+    runs chunk-major over five 32K-column chunks; sampled rows bit-exact vs the oracle."""
     import paper_2102_06025_b200 as X
 
     n, k = 140_000, 24

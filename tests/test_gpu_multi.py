@@ -104,7 +104,7 @@ def test_multi_gpu_micro_batches(p, micro, tmp_path):
 @pytest.mark.parametrize("p", [2, 4])
 def test_multi_gpu_graph_ring_large_sampled(p, tmp_path):
     """The ring at 140K rows per GPU: the all-gathered pilot sample seeds the cuts and the
-    candidate pass runs chunk-major over several 64K-column chunks; sampled rows bit-exact
+    candidate pass runs chunk-major over several 32K-column chunks; sampled rows bit-exact
     against build_graph_bruteforce's row (oracle), almost every row certified."""
     if _ngpus() < p:
         pytest.skip(f"needs {p} GPUs")
