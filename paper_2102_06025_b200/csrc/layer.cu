@@ -186,6 +186,23 @@ __global__ void k_set_f32(float* p, float v) {
   griddep_wait();
   griddep_launch(); *p = v; }
 
+// P = 1 step inputs in one kernel: the caller's features (and labels, unless a prepared
+// selection already holds them) into the layer's buffers, and the learning rate into device
+// memory -- instead of two copy-engine nodes and a kernel between the step graphs
+__global__ void k_stage_inputs(float4* __restrict__ X, const float4* __restrict__ xs,
+                               uint64_t n4, uint32_t* __restrict__ lab,
+                               const uint32_t* __restrict__ ls, uint64_t nl, float* lr_dev,
+                               float lr) {
+  griddep_wait();
+  griddep_launch();
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = t0; i < n4; i += stride) X[i] = xs[i];
+  if (lab)
+    for (uint64_t i = t0; i < nl; i += stride) lab[i] = ls[i];
+  if (t0 == 0) *lr_dev = lr;
+}
+
 // the step's loss to the caller's double (device or pinned host memory, through UVA): a kernel
 // in the stream's launch chain instead of a copy-engine node between two step graphs
 __global__ void k_copy_loss(double* dst, const double* src) {
@@ -475,15 +492,26 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
     XK_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
     XK_NCCL(ncclAllGather(feats_local, X, bl * d, ncclFloat, comm_ag, side));
     XK_CUDA(cudaEventRecord(ev_feat, side));
-  } else {
-    XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
-    if (!core_prepared)
-      XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t),
-                              cudaMemcpyDeviceToDevice, stream));
   }
   // the learning rate travels through device memory so the captured core stays valid
-  launch_pdl(k_set_f32, 1, 1, 0, stream, lr_dev, lr);
-  XK_LAUNCH();
+  if (world == 1 && (reinterpret_cast<uintptr_t>(feats_local) & 15) == 0 && d % 4 == 0) {
+    const uint64_t n4 = B * d / 4;
+    launch_pdl(k_stage_inputs, grid_for(n4, 256, 148u * 8u), 256, 0, stream,
+               reinterpret_cast<float4*>(X), reinterpret_cast<const float4*>(feats_local), n4,
+               core_prepared ? (uint32_t*)nullptr : labels_all, labels_local, (uint64_t)B, lr_dev,
+               lr);
+    XK_LAUNCH();
+  } else {
+    if (world == 1) {
+      XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                              stream));
+      if (!core_prepared)
+        XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, stream));
+    }
+    launch_pdl(k_set_f32, 1, 1, 0, stream, lr_dev, lr);
+    XK_LAUNCH();
+  }
   mark(1);
   if (graph_mode) {
     XK_TRY(ensure_graph(B));
