@@ -835,28 +835,36 @@ __global__ void __launch_bounds__(384, 1)
 __global__ void k_rowreduce(const SelState* st, const float* __restrict__ partial,
                             const float* __restrict__ labelterm, const int32_t* __restrict__ lcol,
                             uint32_t B, uint32_t bpad, double* __restrict__ red) {
+  // 8 rows x 128 tile groups per 1024-thread block (B/8 blocks: enough of them to spread the
+  // partial-sum reads over the SMs); fixed summation order (deterministic)
   griddep_wait();
   griddep_launch();
-  __shared__ double part[32][33];
+  __shared__ double part[128][9];
   const uint32_t nt = 2 * ((st->active_count + 255) / 256);
-  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // row in block, tile group
-  const uint32_t b = blockIdx.x * 32 + tx;
+  const uint32_t tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // row in block, tile group
+  const uint32_t b = blockIdx.x * 8 + tx;
   double s = 0.0;
-  if (b < B) {  // 4 independent loads in flight per thread (fixed order: deterministic)
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  if (b < B) {
+    double s2[2] = {0.0, 0.0};
     uint32_t t = ty;
-    for (; t + 96 < nt; t += 128) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s4[j] += (double)partial[(uint64_t)(t + 32 * j) * bpad + b];
+    for (; t + 128 < nt; t += 256) {
+      s2[0] += (double)partial[(uint64_t)t * bpad + b];
+      s2[1] += (double)partial[(uint64_t)(t + 128) * bpad + b];
     }
-    for (; t < nt; t += 32) s4[0] += (double)partial[(uint64_t)t * bpad + b];
-    s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    for (; t < nt; t += 128) s2[0] += (double)partial[(uint64_t)t * bpad + b];
+    s = s2[0] + s2[1];
   }
   part[ty][tx] = s;
   __syncthreads();
+  double g = 0.0;  // threads ty < 8: row tx, groups ty*16 .. ty*16+15
+  if (ty < 8)
+    for (int i = 0; i < 16; ++i) g += part[ty * 16 + i][tx];
+  __syncthreads();
+  if (ty < 8) part[ty][tx] = g;
+  __syncthreads();
   if (ty == 0 && b < B) {
     double tot = 0.0;
-    for (int g = 0; g < 32; ++g) tot += part[g][tx];
+    for (int g2 = 0; g2 < 8; ++g2) tot += part[g2][tx];
     const int32_t c = lcol[b];
     red[b] = tot;
     red[B + b] = c >= 0 ? (double)labelterm[b] : 0.0;
@@ -1145,7 +1153,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over class shards -> loss
-  launch_pdl(k_rowreduce, (unsigned)((B + 31) / 32), 1024, 0, stream, st, f->partial_f, f->labelterm, label_col,
+  launch_pdl(k_rowreduce, (unsigned)((B + 7) / 8), 1024, 0, stream, st, f->partial_f, f->labelterm, label_col,
                                                      (uint32_t)B, f->bpad, rowred);
   XK_LAUNCH();
   if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
