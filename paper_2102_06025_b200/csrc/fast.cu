@@ -1156,7 +1156,14 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   launch_pdl(k_rowreduce, (unsigned)((B + 7) / 8), 1024, 0, stream, st, f->partial_f, f->labelterm, label_col,
                                                      (uint32_t)B, f->bpad, rowred);
   XK_LAUNCH();
-  if (world > 1) XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
+  if (world > 1) {
+    if (par_ar.ready) {  // one kernel over NVLink peer memory (peer.cu)
+      XK_CUDA(par_ar.launch(rowred, 3 * B, err, stream));
+      ++launches;
+    } else {
+      XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
+    }
+  }
   // (d) label-column fix-up of P~ and the row-scaled X_hat', and the loss (block 0)
   launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, rowred, label_col,
              X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16, loss_dev, st, err);

@@ -159,6 +159,7 @@ void Layer::free_all() {
   if (ev_in) cudaEventDestroy(ev_in);
   if (ev_feat) cudaEventDestroy(ev_feat);
   if (comm_ag) ncclCommDestroy(comm_ag);
+  par_ar.release();
   free_fast();
 }
 
@@ -486,6 +487,15 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   //     right before the first kernel that reads X.
   if (world > 1) {
     if (!comm_ag) XK_NCCL(ncclCommSplit(comm, 0, rank, &comm_ag, nullptr));  // collective
+    if (!par_ar.ready && !par_ar_tried && cfg.precision == XKNN_PREC_BF16 &&
+        !getenv("XKNN_NCCL_ALLREDUCE")) {
+      // collective; without CUDA IPC between the ranks the statistics go through NCCL
+      par_ar_tried = true;
+      if (par_ar.setup(rank, world, 3 * bmax, comm, stream) != XKNN_OK) {
+        par_ar.release();
+        (void)cudaGetLastError();
+      }
+    }
     if (!core_prepared)
       XK_NCCL(ncclAllGather(labels_local, labels_all, bl, ncclUint32, comm, stream));
     XK_CUDA(cudaEventRecord(ev_in, stream));

@@ -52,12 +52,30 @@ struct SelState {
 
 enum Branch : unsigned { kPad = 0, kExact = 1, kOverfull = 2 };
 
+// The softmax statistics all-reduce over NVLink peer memory (peer.cu).
+struct PeerAllreduce {
+  int rank = 0, world = 0;
+  uint64_t cap = 0;
+  double* buf = nullptr;         // [2 slots][world][cap], written by every rank
+  uint64_t* flags = nullptr;     // [world]: the epoch each rank last published here
+  uint64_t* epoch = nullptr;     // this rank's all-reduce count
+  double** peer_bufs = nullptr;  // device table: every rank's buf as mapped here
+  uint64_t** peer_flags = nullptr;
+  std::vector<void*> opened;
+  bool ready = false;
+  xknn_status_t setup(int rank, int world, uint64_t cap, ncclComm_t comm, cudaStream_t s);
+  cudaError_t launch(double* data, uint64_t n, unsigned long long* err, cudaStream_t s) const;
+  void release();
+};
+
 struct Layer {
   // ---- topology / config
   int rank = 0, world = 1, device = 0;
   uint64_t n = 0, d = 0, begin = 0, end = 0, nw = 0;
   xknn_config_t cfg{};
   ncclComm_t comm = nullptr;
+  PeerAllreduce par_ar;               // P > 1: the B x 3 softmax statistics all-reduce
+  bool par_ar_tried = false;
   ncclComm_t comm_ag = nullptr;       // split of comm: the feature all-gather, which overlaps
                                       // the selection's own collectives on comm
   cudaEvent_t ev_in = nullptr, ev_feat = nullptr;
