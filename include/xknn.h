@@ -164,6 +164,15 @@ xknn_status_t xknn_step_micro(xknn_layer_t* h, const float* features_local_dev,
 xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local_dev,
                            uint64_t batch_local, void* ready_stream);
 
+/* Replaces the padding draw's raw 64-bit word stream -- by default std::mt19937_64(rng_seed)
+   re-seeded on every selection as the reference does (knn_softmax.cpp:43) -- with `count`
+   caller-given words (count >= m_active; NULL restores the default).  The words feed
+   std::uniform_int_distribution<size_t>'s Lemire draw (uniform_int_dist.h:257-274) exactly as
+   engine output would, including its rejection loop (a zero word is always rejected unless the
+   range is a power of two), so a crafted stream drives that rare path deterministically: a
+   parity hook for tests, also usable to replay another engine's output.  Synchronizes. */
+xknn_status_t xknn_layer_set_draw_stream(xknn_layer_t* h, const uint64_t* words, uint64_t count);
+
 /* Synchronizes the layer stream, returns the first device-side error of the preceding
    asynchronous calls (label range, ZeroNormRow, MTooSmall, ...) and clears it. */
 xknn_status_t xknn_layer_sync(xknn_layer_t* h);

@@ -1,6 +1,6 @@
 // ref_shim.cpp -- C ABI over the UNMODIFIED reference library (xcls::, /root/reference/proj).
 //
-// TEST / BASELINE INFRASTRUCTURE ONLY.  oracle/build_ref.sh compiles this file together with
+// TEST / BASELINE INFRASTRUCTURE ONLY.  `make -C oracle ref` (oracle/Makefile) compiles this file with
 // the reference's own sources (read in place from /root/reference/proj/src, never copied) into
 // oracle/_ref/libxcls_ref.so.  It is used (1) to pin the C restatement in oracle/xknn_oracle.c,
 // (2) to generate the golden fixtures under tests/golden/, and (3) as bench.py's

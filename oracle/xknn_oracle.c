@@ -8,8 +8,8 @@
  *
  * Parity pin: every function below is checked against the reference itself
  * (oracle/_ref/libxcls_ref.so, compiled from /root/reference/proj/src by
- * oracle/build_ref.sh) on seeded random inputs and against the SPEC.md
- * known-answer examples (tests/test_oracle_golden.py, tests/golden/).
+ * `make -C oracle ref`, oracle/Makefile) on seeded random inputs and against the SPEC.md
+ * known-answer examples and the golden fixtures (tests/test_oracle.py, tests/golden/).
  *
  * Arithmetic is restated operation-for-operation (same loop order, same
  * float/double promotions, no FMA contraction: build with -ffp-contract=off)
@@ -34,9 +34,19 @@
 typedef struct {
   uint64_t mt[MT_N];
   int idx;
+  /* test hook: a caller-given word stream replaces the engine's output (or_*_stream) */
+  const uint64_t* inj;
+  uint64_t inj_len, inj_pos;
 } mt64_t;
 
+/* set by or_select_active_shards_stream for the duration of one selection */
+static const uint64_t* g_inj_words = NULL;
+static uint64_t g_inj_len = 0;
+
 void or_mt64_seed(mt64_t* g, uint64_t seed) {
+  g->inj = g_inj_words;
+  g->inj_len = g_inj_len;
+  g->inj_pos = 0;
   g->mt[0] = seed;
   for (int i = 1; i < MT_N; ++i)
     g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
@@ -61,6 +71,7 @@ static void mt64_twist(mt64_t* g) {
 }
 
 uint64_t or_mt64_next(mt64_t* g) {
+  if (g->inj) return g->inj_pos < g->inj_len ? g->inj[g->inj_pos++] : 0;
   if (g->idx >= MT_N) mt64_twist(g);
   uint64_t z = g->mt[g->idx++];
   z ^= (z >> 29) & 0x5555555555555555ULL;
@@ -296,6 +307,24 @@ int or_select_active_shards(uint64_t n, uint64_t p, const uint32_t* const* k_per
   return rc;
 }
 
+/* select_active_classes(span<CompressedKnnGraph>) with the padding draw's raw mt19937_64 words
+ * replaced by words[0..nwords) (words past the end read as 0): drives the Lemire rejection loop
+ * of uniform_int_distribution (uniform_int_dist.h:268-272) deterministically -- a zero word is
+ * always rejected unless the range is a power of two.  Not thread-safe (test hook). */
+int or_select_active_shards_stream(uint64_t n, uint64_t p, const uint32_t* const* k_per_class,
+                                   const uint64_t* const* offsets, const uint32_t* const* flat,
+                                   const uint32_t* labels, uint64_t b, uint64_t m_active,
+                                   const uint64_t* words, uint64_t nwords, uint32_t* out,
+                                   uint64_t* out_count, int* contains_all) {
+  g_inj_words = words;
+  g_inj_len = nwords;
+  const int rc = or_select_active_shards(n, p, k_per_class, offsets, flat, labels, b, m_active, 0,
+                                         out, out_count, contains_all);
+  g_inj_words = NULL;
+  g_inj_len = 0;
+  return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Core math, matrix.cpp                                                      */
 /* ------------------------------------------------------------------------- */
@@ -335,11 +364,33 @@ void or_l2_normalize_backward(uint64_t rows, uint64_t cols, const float* nrm, co
   }
 }
 
-/* matmul(a, b, transpose_b=true), matrix.cpp:57-68: c = a·bᵀ, ascending k */
+/* The three matmuls below are parallelised over OUTPUT elements with OpenMP (each thread owns
+ * whole output rows / columns and runs the reference's per-element chain unchanged), so their
+ * results are bit-identical to the sequential loops of matrix.cpp at any thread count. */
+
+/* matmul(a, b, transpose_b=true), matrix.cpp:57-68: c = a·bᵀ, ascending k.  Four output columns
+ * are advanced together (independent chains, each in ascending k). */
 void or_matmul_nt(uint64_t m, uint64_t n, uint64_t kd, const float* a, const float* b, float* c) {
+#pragma omp parallel for schedule(dynamic, 1) if (m * n * kd > (1u << 22))
   for (uint64_t i = 0; i < m; ++i) {
     const float* ai = a + i * kd;
-    for (uint64_t j = 0; j < n; ++j) {
+    uint64_t j = 0;
+    for (; j + 4 <= n; j += 4) {
+      const float *b0 = b + j * kd, *b1 = b0 + kd, *b2 = b1 + kd, *b3 = b2 + kd;
+      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+      for (uint64_t k = 0; k < kd; ++k) {
+        const float x = ai[k];
+        a0 += x * b0[k];
+        a1 += x * b1[k];
+        a2 += x * b2[k];
+        a3 += x * b3[k];
+      }
+      c[i * n + j] = a0;
+      c[i * n + j + 1] = a1;
+      c[i * n + j + 2] = a2;
+      c[i * n + j + 3] = a3;
+    }
+    for (; j < n; ++j) {
       const float* bj = b + j * kd;
       float acc = 0.0f;
       for (uint64_t k = 0; k < kd; ++k) acc += ai[k] * bj[k];
@@ -351,6 +402,7 @@ void or_matmul_nt(uint64_t m, uint64_t n, uint64_t kd, const float* a, const flo
 /* matmul(a, b) (ikj), matrix.cpp:69-80: c[m×n] = a[m×kd]·b[kd×n] */
 void or_matmul_nn(uint64_t m, uint64_t n, uint64_t kd, const float* a, const float* b, float* c) {
   memset(c, 0, m * n * sizeof(float));
+#pragma omp parallel for schedule(dynamic, 1) if (m * n * kd > (1u << 22))
   for (uint64_t i = 0; i < m; ++i) {
     const float* ai = a + i * kd;
     float* ci = c + i * n;
@@ -362,16 +414,22 @@ void or_matmul_nn(uint64_t m, uint64_t n, uint64_t kd, const float* a, const flo
   }
 }
 
-/* matmul_at(a, b), matrix.cpp:84-98: c[ac×bc] = aᵀ·b, ascending i */
+/* matmul_at(a, b), matrix.cpp:84-98: c[ac×bc] = aᵀ·b, ascending i (every c[j][l] accumulates
+ * rows i = 0, 1, ... in order; threads own blocks of output rows j) */
 void or_matmul_tn(uint64_t rows, uint64_t ac, uint64_t bc, const float* a, const float* b, float* c) {
   memset(c, 0, ac * bc * sizeof(float));
-  for (uint64_t i = 0; i < rows; ++i) {
-    const float* ai = a + i * ac;
-    const float* bi = b + i * bc;
-    for (uint64_t j = 0; j < ac; ++j) {
-      const float aij = ai[j];
-      float* cj = c + j * bc;
-      for (uint64_t l = 0; l < bc; ++l) cj[l] += aij * bi[l];
+  const uint64_t JB = 64;
+#pragma omp parallel for schedule(dynamic, 1) if (rows * ac * bc > (1u << 22))
+  for (uint64_t j0 = 0; j0 < ac; j0 += JB) {
+    const uint64_t j1 = j0 + JB < ac ? j0 + JB : ac;
+    for (uint64_t i = 0; i < rows; ++i) {
+      const float* ai = a + i * ac;
+      const float* bi = b + i * bc;
+      for (uint64_t j = j0; j < j1; ++j) {
+        const float aij = ai[j];
+        float* cj = c + j * bc;
+        for (uint64_t l = 0; l < bc; ++l) cj[l] += aij * bi[l];
+      }
     }
   }
 }

@@ -31,6 +31,11 @@ int or_select_active_shards(uint64_t n, uint64_t p, const uint32_t* const* k_per
                             const uint64_t* const* offsets, const uint32_t* const* flat,
                             const uint32_t* labels, uint64_t b, uint64_t m_active, uint64_t seed,
                             uint32_t* out, uint64_t* out_count, int* contains_all);
+int or_select_active_shards_stream(uint64_t n, uint64_t p, const uint32_t* const* k_per_class,
+                                   const uint64_t* const* offsets, const uint32_t* const* flat,
+                                   const uint32_t* labels, uint64_t b, uint64_t m_active,
+                                   const uint64_t* words, uint64_t nwords, uint32_t* out,
+                                   uint64_t* out_count, int* contains_all);
 int or_l2_normalize_rows(uint64_t rows, uint64_t cols, const float* in, float eps, float* out,
                          float* norms, uint64_t* bad_row);
 void or_l2_normalize_backward(uint64_t rows, uint64_t cols, const float* nrm, const float* norms,

@@ -105,6 +105,7 @@ for _name, _args in {
     "xknn_step_micro": [VP, VP, VP, U64, C.c_float, C.c_uint32, VP, VP],
     "xknn_prepare": [VP, VP, U64, VP],
     "xknn_layer_sync": [VP],
+    "xknn_layer_set_draw_stream": [VP, VP, U64],
     "xknn_layer_last_active": [VP, C.POINTER(U64), C.POINTER(U64)],
     "xknn_layer_last_logits": [VP, VP, U64],
     "xknn_graph_bruteforce": [VP, U64, U64, C.c_uint32, C.c_uint32, VP, VP, C.POINTER(U64)],
@@ -471,10 +472,19 @@ class KnnSoftmaxLayer:
         train_step must get the same labels).  ready_stream: the torch stream on which
         labels_local becomes valid (None: it already is)."""
         torch = self._torch
-        lab = labels_local if labels_local.dtype == torch.int32 else labels_local.to(torch.int32)
+        cur = torch.cuda.current_stream()
+        ready = ready_stream if ready_stream is not None else cur
+        if labels_local.dtype != torch.int32 or not labels_local.is_contiguous():
+            # the conversion runs on the current stream after the labels are valid; the side
+            # stream then waits for the converted buffer (not only for the caller's labels)
+            if ready != cur:
+                cur.wait_stream(ready)
+            lab = labels_local.to(torch.int32).contiguous()
+            ready = cur
+        else:
+            lab = labels_local
         self._prep_keep = lab  # the buffer must outlive the asynchronous all-gather / copy
-        _check(_lib.xknn_prepare(self.h, lab.data_ptr(), lab.numel(),
-                                 ready_stream.cuda_stream if ready_stream is not None else None))
+        _check(_lib.xknn_prepare(self.h, lab.data_ptr(), lab.numel(), ready.cuda_stream))
 
     def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
                    loss_out=None, sync: bool = True, micro_batches: int = 1):
@@ -500,6 +510,16 @@ class KnnSoftmaxLayer:
             _check(_lib.xknn_layer_sync(self.h))
             return float(loss.item())
         return None
+
+    def set_draw_stream(self, words=None) -> None:
+        """Replace the padding draw's mt19937_64(rng_seed) word stream with `words` (uint64
+        numpy array, >= m_active words), or restore it (None): xknn_layer_set_draw_stream."""
+        if words is None:
+            _check(_lib.xknn_layer_set_draw_stream(self.h, None, 0))
+            return
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        self._enter()
+        _check(_lib.xknn_layer_set_draw_stream(self.h, w.ctypes.data, w.size))
 
     def sync(self) -> None:
         _check(_lib.xknn_layer_sync(self.h))

@@ -7,10 +7,13 @@
 //            epilogue: P~ = exp(s*S - s) -> bf16 (B x M_w), per-tile row sums, label logit.
 //            A fixed stabiliser c = s replaces the row max: |cosine| <= 1 bounds every logit
 //            to [-s, s], so exp(s*S - s) lies in [e^-2s, 1] (fp32-safe for s <= 40).
-// Backward, with r_b = 1 / (B * sum_b) and P~' = P~ minus sum_b at the label column
-// (so G = r * P~' reproduces softmax - onehot over m, parallel.cpp:168-186, exactly):
-//   GEMM-dW  dW  = P~'ᵀ * (diag(s*r) X_hat)    (M = 128 classes, N = 512, K = B) -> fp32
-//   GEMM-dX  dX  = diag(s*r) * (P~' * W_sub)   (M = 128 batch, N = 512, K = M_w split) -> fp32
+// Backward, with r_b = 1 / (B * sum_b), G = r * P~ - onehot / B (= softmax - onehot over m,
+// parallel.cpp:168-186):
+//   GEMM-dW  dW  = P~ᵀ * (diag(s*r) X_hat)     (M = 128 classes, N = 512, K = B) -> bf16 rows
+//   GEMM-dX  dX  = diag(s*r) * (P~ * W_sub)    (M = 128 batch, N = 512, K = M_w split) -> fp32
+// The one-hot term is a sparse fp32 rank-B correction, never rounded to bf16: k_dx_reduce
+// subtracts (s/B) * w_hat[y_b] from feature row b, and the row update subtracts
+// (s/B) * sum{x_hat_b : y_b = class} from the class's dW row (label lists built by k_fixup).
 // Warp roles (384 threads, one CTA per SM, persistent over tiles): warp 0 TMA producer,
 // warp 1 MMA issuer (one thread), warp 2 TMEM allocator, warps 4-11 epilogue (TMEM -> regs).
 #include <cudaTypedefs.h>
@@ -872,13 +875,15 @@ __global__ void k_rowreduce(const SelState* st, const float* __restrict__ partia
   }
 }
 
-// P~' = P~ - sum at the label column; X_hat' = bf16(x_hat * s / (B * sum)); pad rows zeroed
+// X_hat' = bf16(x_hat * s / (B * sum)); pad rows zeroed; the batch rows of every local label
+// column linked into lists (lab_head[col] -> lab_next[b] -> ..., -1 terminated; the row update
+// consumes and clears them)
 template <int DV>
 __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restrict__ lcol,
                         const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
-                        uint32_t bpad, uint32_t d, float scale, __nv_bfloat16* __restrict__ Pt,
-                        uint64_t ldp, __nv_bfloat16* __restrict__ Xs, double* __restrict__ loss,
-                        SelState* st, unsigned long long* err) {
+                        uint32_t bpad, uint32_t d, float scale, int32_t* __restrict__ lab_head,
+                        int32_t* __restrict__ lab_next, __nv_bfloat16* __restrict__ Xs,
+                        double* __restrict__ loss, SelState* st, unsigned long long* err) {
   griddep_wait();
   griddep_launch();
   if (blockIdx.x == 0) {
@@ -911,10 +916,7 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
     }
     const double denom = red[b];
     const int32_t lc = lcol[b];
-    if (lane == 0 && lc >= 0) {
-      __nv_bfloat16* p = Pt + (uint64_t)b * ldp + lc;
-      *p = __float2bfloat16_rn(__bfloat162float(*p) - (float)denom);
-    }
+    if (lane == 0 && lc >= 0) lab_next[b] = atomicExch(&lab_head[lc], (int32_t)b);
     const float inv = 1.0f / xnorm[b];
     const float rs = (float)((double)scale / ((double)B * denom));
     const float4* xp = reinterpret_cast<const float4*>(X + (uint64_t)b * d);
@@ -927,10 +929,15 @@ __global__ void k_fixup(const double* __restrict__ red, const int32_t* __restric
   }
 }
 
-// dX[b][:] = s * r_b * sum_s partial[s][b][:] (fixed split order)
+// dX[b][:] = s * r_b * sum_s partial[s][b][:] (fixed split order) - (s/B) * w_hat[y_b] when the
+// label's class is in this shard (w_hat recomputed in fp32 from W and its cached norm, exactly as
+// the gather normalized it)
 __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __restrict__ red,
                             uint32_t B, uint32_t nbt, uint32_t splits, uint32_t rows_per_unit,
-                            float scale, float* __restrict__ out) {
+                            float scale, const int32_t* __restrict__ lcol,
+                            const uint32_t* __restrict__ active, uint64_t begin,
+                            const float* __restrict__ W, const float* __restrict__ wnorm,
+                            float* __restrict__ out) {
   griddep_wait();
   griddep_launch();
   const uint64_t total = (uint64_t)B * 128;  // float4 units (D = 512)
@@ -948,8 +955,18 @@ __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __r
       acc.w += v.w;
     }
     const float rs = (float)((double)scale / ((double)B * red[b]));
-    reinterpret_cast<float4*>(out + (uint64_t)b * 512)[c4] =
-        make_float4(acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs);
+    float4 o = make_float4(acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs);
+    const int32_t lc = lcol[b];
+    if (lc >= 0) {
+      const float sb = (float)((double)scale / (double)B);
+      const float inv = 1.0f / wnorm[lc];
+      const float4 w = reinterpret_cast<const float4*>(W + ((uint64_t)active[lc] - begin) * 512)[c4];
+      o.x = __fsub_rn(o.x, __fmul_rn(sb, __fmul_rn(w.x, inv)));
+      o.y = __fsub_rn(o.y, __fmul_rn(sb, __fmul_rn(w.y, inv)));
+      o.z = __fsub_rn(o.z, __fmul_rn(sb, __fmul_rn(w.z, inv)));
+      o.w = __fsub_rn(o.w, __fmul_rn(sb, __fmul_rn(w.w, inv)));
+    }
+    reinterpret_cast<float4*>(out + (uint64_t)b * 512)[c4] = o;
   }
 }
 
@@ -1004,6 +1021,8 @@ struct FastState {
   float* labelterm = nullptr;       // [bpad]
   float* partial_dx = nullptr;      // [units][256][512]
   __nv_bfloat16* dW16 = nullptr;    // [mwpad][512] weight gradient, compact active order
+  int32_t* lab_head = nullptr;      // [mwpad] first batch row labelled with each active column
+  int32_t* lab_next = nullptr;      // [bpad]  next batch row with the same label column
   CUtensorMap mF_A, mF2_B, mDX_A, mDX_B, mDW_A, mDW_B;
   CUtensorMap mPt_st, mDXP_st, mDW_st, mF2_B64;
 };
@@ -1066,6 +1085,9 @@ xknn_status_t Layer::init_fast() {
   f->dx_units_cap = 148ull * 256;  // pair-tile units x 256 rows (at most 148 units)
   XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
   XK_CUDA(dalloc(&f->dW16, (uint64_t)f->mwpad * d));
+  XK_CUDA(dalloc(&f->lab_head, f->mwpad));
+  XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));  // all -1
+  XK_CUDA(dalloc(&f->lab_next, f->bpad));
   XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
   bool ok = true;
   ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1100,8 +1122,19 @@ void Layer::free_fast() {
   if (f->labelterm) cudaFree(f->labelterm);
   if (f->partial_dx) cudaFree(f->partial_dx);
   if (f->dW16) cudaFree(f->dW16);
+  if (f->lab_head) cudaFree(f->lab_head);
+  if (f->lab_next) cudaFree(f->lab_next);
   delete f;
   fast = nullptr;
+}
+
+// after a failed step (device error word set): the label lists may hold entries of columns the
+// aborted update never visited
+xknn_status_t Layer::reset_fast_scratch() {
+  auto* f = static_cast<FastState*>(fast);
+  if (!f) return XKNN_OK;
+  XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));
+  return XKNN_OK;
 }
 
 xknn_status_t Layer::run_fast_core(uint64_t B) {
@@ -1166,7 +1199,8 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   }
   // (d) label-column fix-up of P~ and the row-scaled X_hat', and the loss (block 0)
   launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, rowred, label_col,
-             X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, Pt, ldp, Xs16, loss_dev, st, err);
+             X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, f->lab_head, f->lab_next, Xs16,
+             loss_dev, st, err);
   XK_LAUNCH();
   mark(5);
   // (e) GEMM-dW -> bf16 dW rows (compact active order)
@@ -1190,8 +1224,8 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   XK_LAUNCH();
   mark(7);
   launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred, (uint32_t)B,
-                                                           nbp, dx_splits, 256, cfg.scale,
-                                                           world > 1 ? dXpart : dX);
+             nbp, dx_splits, 256u, cfg.scale, (const int32_t*)label_col, (const uint32_t*)active,
+             begin, (const float*)W, (const float*)wnorm, world > 1 ? dXpart : dX);
   XK_LAUNCH();
   const uint64_t bl = B / world;
   if (world > 1) {
@@ -1206,8 +1240,9 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   //     (a separate HBM-streaming kernel: it runs at the copy roofline, while inside the
   //     GEMM-dW kernel the few spare warps per SM could not keep enough bytes in flight)
   mark(8);
+  LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B)};
   XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
-                                  wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream));
+                                  wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream, lf));
   ++launches;
   if (world > 1) XK_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
   return XKNN_OK;

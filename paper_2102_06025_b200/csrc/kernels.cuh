@@ -5,20 +5,32 @@
 namespace xknn {
 
 // rowops.cu
+// The one-hot part of the softmax gradient on the weight side (tensor-core precisions): for
+// active column t, dW[t] -= sb * sum{x_hat_b : b in the list head[t] -> next[b] -> ...}, summed
+// in ascending b; the update clears head[t] (-1) for the next step.  head == nullptr: none.
+struct LabelFix {
+  int32_t* head = nullptr;
+  const int32_t* next = nullptr;
+  const float* X = nullptr;      // gathered raw features (B x D)
+  const float* xnorm = nullptr;  // their norms
+  float sb = 0.f;                // s / B
+};
 cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
-                                  float* norms, unsigned long long* err, cudaStream_t s);
+                                  float* norms, unsigned long long* err, cudaStream_t s,
+                                  bool seq = false);
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
                                const unsigned long long* err, cudaStream_t s,
-                               unsigned max_grid = 148u * 16u);
+                               unsigned max_grid = 148u * 16u, LabelFix lf = {});
 cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
                                     const uint32_t* active, const unsigned int* count,
                                     uint64_t max_rows, uint64_t begin, uint32_t d,
                                     const float* wnorm, const float* lr, float mu, float wd,
-                                    const unsigned long long* err, cudaStream_t s);
+                                    const unsigned long long* err, cudaStream_t s,
+                                    LabelFix lf = {});
 cudaError_t launch_feature_backward(const float* X, const float* xnorm, const float* G,
                                     uint64_t rows, uint32_t d, float* out, cudaStream_t s,
                                     uint32_t micros = 1);

@@ -1,6 +1,7 @@
 // layer.cu -- the xknn C ABI (include/xknn.h) and the per-step orchestration.
 #include <cub/cub.cuh>
 
+#include <cmath>
 #include <cstring>
 #include <random>
 #include <string>
@@ -167,6 +168,7 @@ void Layer::free_all() {
 // select_active_classes call (knn_softmax.cpp:43) -- generated here with the same libstdc++
 // engine, once per (seed, M).
 xknn_status_t Layer::ensure_mt_cache() {
+  if (mt_injected) return XKNN_OK;  // xknn_layer_set_draw_stream
   const uint64_t want = cfg.m_active + 64;
   if (mt_cache && mt_len == want && mt_seed == cfg.rng_seed) return XKNN_OK;
   if (mt_cache) cudaFree(mt_cache);
@@ -377,6 +379,13 @@ void Layer::drop_graphs() {
   }
 }
 
+xknn_status_t Layer::cancel_prepared() {
+  if (!prepared) return XKNN_OK;
+  XK_CUDA(cudaStreamWaitEvent(stream, ev_prep, 0));  // its side-stream work stays ordered
+  prepared = false;
+  return XKNN_OK;
+}
+
 void Layer::use_set(int p) {
   st = ss[p].st;
   active = ss[p].active;
@@ -562,6 +571,18 @@ using xknn::Layer;
 using xknn::fail;
 
 
+// The tensor-core paths replace the row max by the fixed stabilizer c = s (fast.cu): every
+// exp(s*cos - s) lies in [e^-2s, 1], which fp32 (and ex2.approx.ftz) represents for s <= 40.
+// The reference works at any scale; FP32_EXACT (true row max) accepts any finite scale.
+static xknn_status_t check_scale(const xknn_config_t* cfg) {
+  if (!std::isfinite(cfg->scale)) return fail(XKNN_ERR_CONFIG, "scale must be finite");
+  if (cfg->precision != XKNN_PREC_FP32_EXACT && !(cfg->scale > 0.f && cfg->scale <= 40.f))
+    return fail(XKNN_ERR_CONFIG,
+                "tensor-core precisions need 0 < scale <= 40 (fixed softmax stabilizer); use "
+                "XKNN_PREC_FP32_EXACT for other scales");
+  return XKNN_OK;
+}
+
 #define GUARD_H(h) \
   if (!(h)) return fail(XKNN_ERR_INVALID_ARGUMENT, "null layer handle")
 
@@ -644,6 +665,7 @@ xknn_status_t xknn_layer_create(int rank, int world, uint64_t n, uint64_t d,
   if (cfg->m_active > n) return fail(XKNN_ERR_INVALID_ARGUMENT, "M exceeds the class count");
   if (cfg->precision != XKNN_PREC_BF16 && cfg->precision != XKNN_PREC_FP32_EXACT)
     return fail(XKNN_ERR_CONFIG, "unknown precision");
+  if (xknn_status_t s = check_scale(cfg); s != XKNN_OK) return s;
   auto* h = new (std::nothrow) xknn_layer;
   if (!h) return fail(XKNN_ERR_OUT_OF_MEMORY, "host alloc");
   xknn_status_t s = h->L.init(rank, world, n, d, cfg, comm, stream);
@@ -677,6 +699,9 @@ xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg) {
   if (cfg->m_active != L.cfg.m_active || cfg->max_batch != L.cfg.max_batch ||
       cfg->precision != L.cfg.precision)
     return fail(XKNN_ERR_CONFIG, "m_active, max_batch and precision are fixed at creation");
+  XK_TRY_H(check_scale(cfg));
+  // a prepared selection drew from the old rng_seed: the next step selects again
+  XK_TRY_H(L.cancel_prepared());
   L.cfg.scale = cfg->scale;
   L.cfg.momentum = cfg->momentum;
   L.cfg.weight_decay = cfg->weight_decay;
@@ -691,6 +716,27 @@ static cudaMemcpyKind kind_in(int on_device) {
 }
 static cudaMemcpyKind kind_out(int on_device) {
   return on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+}
+
+xknn_status_t xknn_layer_set_draw_stream(xknn_layer_t* h, const uint64_t* words, uint64_t count) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  XK_TRY_H(L.cancel_prepared());
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
+  if (L.side) XK_CUDA_H(cudaStreamSynchronize(L.side));
+  L.drop_graphs();  // the cache pointer is baked into the captured steps
+  if (L.mt_cache) cudaFree(L.mt_cache);
+  L.mt_cache = nullptr;
+  L.mt_len = 0;
+  L.mt_injected = false;
+  if (!words) return XKNN_OK;  // back to mt19937_64(rng_seed)
+  if (count < L.cfg.m_active)
+    return fail(XKNN_ERR_INVALID_ARGUMENT, "draw stream shorter than m_active");
+  XK_CUDA_H(xknn::dalloc(&L.mt_cache, count));
+  XK_CUDA_H(cudaMemcpy(L.mt_cache, words, count * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  L.mt_len = count;
+  L.mt_injected = true;
+  return XKNN_OK;
 }
 
 xknn_status_t xknn_layer_set_weights(xknn_layer_t* h, const float* w, int on_device) {
@@ -756,6 +802,9 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   L.g_flat = nullptr;
   L.has_graph = false;
   L.drop_graphs();  // graph buffers are baked into the graphs
+  // a selection prepared from the old graph is never used after the graph changes (the
+  // reference selects from the current graph at step time)
+  XK_TRY_H(L.cancel_prepared());
   XK_CUDA_H(xknn::dalloc(&L.g_kpc, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_off, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_flat, flat_len));
@@ -862,6 +911,7 @@ xknn_status_t xknn_layer_sync(xknn_layer_t* h) {
   XK_CUDA_H(cudaStreamSynchronize(L.stream));
   if (w) {
     XK_CUDA_H(cudaMemsetAsync(L.err, 0, 8, L.stream));
+    XK_TRY_H(L.reset_fast_scratch());
     XK_CUDA_H(cudaStreamSynchronize(L.stream));
     const xknn_status_t code = (xknn_status_t)(w & 0xff);
     xknn::g_row = w >> 8;

@@ -109,6 +109,7 @@ struct Layer {
   uint32_t* blk_counts = nullptr;     // compaction block counts / offsets
   uint64_t* mt_cache = nullptr;       // u64[m_active + 64]
   uint64_t mt_len = 0, mt_seed = 0;
+  bool mt_injected = false;           // xknn_layer_set_draw_stream replaced the stream
   uint32_t* pick_key = nullptr;       // j_i        [M]
   uint32_t* pick_val = nullptr;       // next-in-group links [M]
   uint32_t* pick_head = nullptr;      // [N] group heads per complement position
@@ -174,6 +175,7 @@ struct Layer {
   cudaGraphExec_t sel_graph[2] = {nullptr, nullptr};
   uint64_t sel_graph_b[2] = {0, 0}, sel_graph_launches[2] = {0, 0};
   void use_set(int p);
+  xknn_status_t cancel_prepared();    // drop a pending xknn_prepare result (graph/seed changed)
   xknn_status_t run_prepare(const uint32_t* labels_local, uint64_t batch_local, cudaStream_t ready);
   xknn_status_t record_external(cudaEvent_t ev, cudaStream_t on);
   xknn_status_t wait_external(cudaEvent_t ev, cudaStream_t on);
@@ -212,6 +214,7 @@ struct Layer {
   xknn_status_t init_fast();
   void free_fast();
   xknn_status_t run_fast_core(uint64_t batch);
+  xknn_status_t reset_fast_scratch();
 };
 
 }  // namespace xknn
@@ -233,6 +236,11 @@ struct xknn_layer {
     if (_r != ncclSuccess) return nccl_ok(_r);         \
   } while (0)
 #define XK_TRY(expr)                                   \
+  do {                                                 \
+    xknn_status_t _s = (expr);                         \
+    if (_s != XKNN_OK) return _s;                      \
+  } while (0)
+#define XK_TRY_H(expr)                                 \
   do {                                                 \
     xknn_status_t _s = (expr);                         \
     if (_s != XKNN_OK) return _s;                      \

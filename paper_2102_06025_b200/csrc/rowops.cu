@@ -32,7 +32,10 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst, float a, float 
 }
 
 // D is a multiple of 128 (checked at create); each lane owns D/128 float4 chunks.
-template <int DV>  // DV = D/128 float4 per lane
+// SEQ: the fp64 sum of squares in ascending column order, as matrix.cpp:18-21 (FP32_EXACT, whose
+// logits are bit-identical to the reference's); otherwise lane-strided partials + a butterfly
+// (the norm may differ from the reference's in the last bit for ~2^-28 of rows).
+template <int DV, bool SEQ = false>  // DV = D/128 float4 per lane
 __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, uint32_t d,
                                  const uint32_t* __restrict__ row_ids, const unsigned int* count,
                                  uint64_t id_base, float* __restrict__ out32,
@@ -50,12 +53,30 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
 #pragma unroll
     for (int c = 0; c < DV; ++c) {
       v[c] = src[lane + 32 * c];
-      sq += (double)v[c].x * v[c].x;
-      sq += (double)v[c].y * v[c].y;
-      sq += (double)v[c].z * v[c].z;
-      sq += (double)v[c].w * v[c].w;
+      if (!SEQ) {
+        sq += (double)v[c].x * v[c].x;
+        sq += (double)v[c].y * v[c].y;
+        sq += (double)v[c].z * v[c].z;
+        sq += (double)v[c].w * v[c].w;
+      }
     }
-    sq = warp_allsum(sq);
+    if (SEQ) {  // every lane runs the same column-order chain on broadcast values
+#pragma unroll
+      for (int c = 0; c < DV; ++c)
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const float a = __shfl_sync(XKNN_FULL_MASK, v[c].x, j);
+          const float b = __shfl_sync(XKNN_FULL_MASK, v[c].y, j);
+          const float e = __shfl_sync(XKNN_FULL_MASK, v[c].z, j);
+          const float f = __shfl_sync(XKNN_FULL_MASK, v[c].w, j);
+          sq += (double)a * a;
+          sq += (double)b * b;
+          sq += (double)e * e;
+          sq += (double)f * f;
+        }
+    } else {
+      sq = warp_allsum(sq);
+    }
     const float norm = (float)sqrt(sq);
     if (norm < 1e-12f) {
       if (lane == 0) raise_error(err, XKNN_ERR_ZERO_NORM_ROW, r);
@@ -78,8 +99,9 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
 }
 
 // Normalize-backward of each active row through its cached norm, then SgdMomentum::step_rows
-// on (W, V).  g rows are compact (row t <-> active[t]).  Skipped entirely if any error was
-// raised earlier in the step (the reference throws before touching parameters).
+// on (W, V).  g rows are compact (row t <-> active[t]), minus the one-hot correction of
+// LabelFix.  Parameters are not touched if any error was raised earlier in the step (the
+// reference throws before touching parameters); the label lists are cleared either way.
 __device__ __forceinline__ float4 load_g4(const float* __restrict__ G, uint64_t i) {
   return reinterpret_cast<const float4*>(G)[i];
 }
@@ -94,14 +116,23 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
                               const GT* __restrict__ G, const uint32_t* __restrict__ active,
                               const unsigned int* count, uint64_t begin, uint32_t d,
                               const float* __restrict__ wnorm, const float* __restrict__ lr_dev,
-                              float mu, float wd, const unsigned long long* err) {
+                              float mu, float wd, const unsigned long long* err, LabelFix lf) {
   griddep_wait();
-  if (*err) return;
+  const bool dead = *err != 0;
+  if (dead && !lf.head) return;
   const float lr = *lr_dev;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = *count;
   for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < nrows;
        t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    // the batch rows labelled with this class, ascending (lists are almost always 1 long)
+    int32_t lh = -1;
+    if (lf.head) {
+      lh = lf.head[t];
+      __syncwarp();
+      if (lane == 0 && lh >= 0) lf.head[t] = -1;
+    }
+    if (dead) continue;
     const uint64_t row = (uint64_t)active[t] - begin;
     float4* wp = reinterpret_cast<float4*>(W + row * d);
     float4* vp = reinterpret_cast<float4*>(V + row * d);
@@ -116,6 +147,36 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
       w[c] = wp[lane + 32 * c];
       g[c] = load_g4(G, g0 + lane + 32 * c);
       vel[c] = vp[lane + 32 * c];
+    }
+    if (lh >= 0) {
+      float4 xs[DV];
+#pragma unroll
+      for (int c = 0; c < DV; ++c) xs[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      int32_t cur = -1;
+      for (;;) {  // next larger batch row of the list (every lane walks it: broadcast loads)
+        int32_t best = INT32_MAX;
+        for (int32_t b = lh; b >= 0; b = lf.next[b])
+          if (b > cur && b < best) best = b;
+        if (best == INT32_MAX) break;
+        cur = best;
+        const float xi = 1.0f / lf.xnorm[cur];
+        const float4* xp = reinterpret_cast<const float4*>(lf.X + (uint64_t)cur * d);
+#pragma unroll
+        for (int c = 0; c < DV; ++c) {
+          const float4 x = xp[lane + 32 * c];
+          xs[c].x = __fadd_rn(xs[c].x, __fmul_rn(x.x, xi));
+          xs[c].y = __fadd_rn(xs[c].y, __fmul_rn(x.y, xi));
+          xs[c].z = __fadd_rn(xs[c].z, __fmul_rn(x.z, xi));
+          xs[c].w = __fadd_rn(xs[c].w, __fmul_rn(x.w, xi));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < DV; ++c) {
+        g[c].x = __fsub_rn(g[c].x, __fmul_rn(lf.sb, xs[c].x));
+        g[c].y = __fsub_rn(g[c].y, __fmul_rn(lf.sb, xs[c].y));
+        g[c].z = __fsub_rn(g[c].z, __fmul_rn(lf.sb, xs[c].z));
+        g[c].w = __fsub_rn(g[c].w, __fmul_rn(lf.sb, xs[c].w));
+      }
     }
 #pragma unroll
     for (int c = 0; c < DV; ++c) {
@@ -220,8 +281,15 @@ __global__ void k_feature_backward(const float* __restrict__ X, const float* __r
 cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
-                                  float* norms, unsigned long long* err, cudaStream_t s) {
+                                  float* norms, unsigned long long* err, cudaStream_t s,
+                                  bool seq) {
   const unsigned grid = grid_for(rows * 32, 256);
+  if (seq) {
+    if (d != 512) return cudaErrorInvalidValue;
+    launch_pdl(k_normalize_rows<4, true>, grid, 256, 0, s, in, rows, d, row_ids, count, id_base,
+               out32, out16, norms, err);
+    return cudaGetLastError();
+  }
   XKNN_DISPATCH_D(d, k_normalize_rows, grid, 256, s, in, rows, d, row_ids, count, id_base, out32,
                   out16, norms, err);
   return cudaGetLastError();
@@ -230,10 +298,11 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
-                               const unsigned long long* err, cudaStream_t s, unsigned max_grid) {
+                               const unsigned long long* err, cudaStream_t s, unsigned max_grid,
+                               LabelFix lf) {
   const unsigned grid = grid_for(max_rows * 32, 256, max_grid);
   XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,
-                  wd, err);
+                  wd, err, lf);
   return cudaGetLastError();
 }
 
@@ -241,11 +310,12 @@ cudaError_t launch_update_rows_bf16(float* W, float* V, const __nv_bfloat16* G,
                                     const uint32_t* active, const unsigned int* count,
                                     uint64_t max_rows, uint64_t begin, uint32_t d,
                                     const float* wnorm, const float* lr, float mu, float wd,
-                                    const unsigned long long* err, cudaStream_t s) {
+                                    const unsigned long long* err, cudaStream_t s,
+                                    LabelFix lf) {
   if (d != 512) return cudaErrorInvalidValue;
   const unsigned grid = grid_for(max_rows * 32, 256, 148u * 16u);
   launch_pdl(k_update_rows<4, __nv_bfloat16>, grid, 256, 0, s, W, V, G, active, count, begin, d, wnorm,
-                                                       lr, mu, wd, err);
+                                                       lr, mu, wd, err, lf);
   return cudaGetLastError();
 }
 

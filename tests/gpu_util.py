@@ -33,3 +33,46 @@ def rel_err(a, b):
     b = np.asarray(b, np.float64)
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+def device_graph(n, k, seed, chunk=1 << 20):
+    """A seeded self-first random k-graph generated on the device (N x k int32, row-major, as
+    bench.py's build_shard_graph at P = 1): (flat, k_per_class, offsets) CUDA tensors of the
+    one-shard CompressedKnnGraph.  Used where the host cannot hold the graph (C3/C4 geometry)."""
+    torch = torch_cuda()
+    flat = torch.empty(n * k, dtype=torch.int32, device="cuda")
+    g = torch.Generator(device="cuda")
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        g.manual_seed(seed * 1_000_003 + c0)
+        nb = torch.randint(0, n, (c1 - c0, k), device="cuda", dtype=torch.int32, generator=g)
+        nb[:, 0] = torch.arange(c0, c1, device="cuda", dtype=torch.int32)
+        flat[c0 * k:c1 * k] = nb.reshape(-1)
+    kpc = torch.full((n,), k, dtype=torch.int32, device="cuda")
+    off = torch.arange(n, device="cuda", dtype=torch.int64) * k
+    return flat, kpc, off
+
+
+def host_label_csr(flat_dev, n, k, labels):
+    """The one-shard CSR restricted to the batch's labels (every other class gets k = 0): the
+    selection reads only the labels' slices, so the oracle's result equals the full graph's."""
+    torch = torch_cuda()
+    u = np.unique(labels.astype(np.int64))
+    rows = flat_dev.view(n, k)[torch.from_numpy(u).cuda()].cpu().numpy().view(np.uint32)
+    kpc = np.zeros(n, np.uint32)
+    kpc[u] = k
+    off = np.zeros(n, np.uint64)
+    off[1:] = np.cumsum(kpc[:-1].astype(np.uint64))
+    return kpc, off, np.ascontiguousarray(rows.reshape(-1))
+
+
+def parity_record(name, **vals):
+    """Appends measured errors to $XKNN_PARITY_OUT (JSON lines) when set."""
+    import json
+    import os
+
+    path = os.environ.get("XKNN_PARITY_OUT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": name, **vals}) + "\n")
+    print(name, vals)

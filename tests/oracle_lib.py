@@ -130,6 +130,26 @@ def select_shards(lib_kind: str, n: int, shards, labels: np.ndarray, m: int, see
     return rc, out[: cnt.value].copy(), bool(ca.value)
 
 
+def select_shards_stream(n: int, shards, labels: np.ndarray, m: int, words: np.ndarray):
+    """select_active_classes(span<CompressedKnnGraph>) with the padding draw's mt19937_64 words
+    replaced by `words` (or_select_active_shards_stream: drives the Lemire rejection loop)."""
+    p = len(shards)
+    flats = [s[2] if s[2].size else np.zeros(1, np.uint32) for s in shards]
+    out = np.zeros(max(m, 1), np.uint32)
+    cnt = U64(0)
+    ca = C.c_int(0)
+    labels = np.ascontiguousarray(labels, dtype=np.uint32)
+    words = np.ascontiguousarray(words, dtype=np.uint64)
+    fn = oracle().or_select_active_shards_stream
+    fn.restype = C.c_int
+    fn.argtypes = [U64, U64, C.c_void_p, C.c_void_p, C.c_void_p, u32p, U64, U64, u64p, U64, u32p,
+                   C.POINTER(U64), C.POINTER(C.c_int)]
+    rc = fn(n, p, _ptr_array([s[0] for s in shards], None), _ptr_array([s[1] for s in shards], None),
+            _ptr_array(flats, None), labels, labels.size, m, words, words.size, out, C.byref(cnt),
+            C.byref(ca))
+    return rc, out[: cnt.value].copy(), bool(ca.value)
+
+
 def select_full(lib_kind: str, g: np.ndarray, labels: np.ndarray, m: int, seed: int):
     n, k = g.shape
     out = np.zeros(max(m, 1), np.uint32)

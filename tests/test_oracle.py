@@ -228,3 +228,42 @@ def test_ref_selection_not_self_first():
         a = O.select_shards("oracle", n, shards, lab, m, trial)
         r = O.select_shards("ref", n, shards, lab, m, trial)
         assert a[0] == r[0] and np.array_equal(a[1], r[1]) and a[2] == r[2]
+
+
+def _py_select_pad_stream(n, pool, m, words):
+    """Pure-Python finish_selection padding branch (knn_softmax.cpp:33-51) over an injected word
+    stream with libstdc++'s Lemire draw (uniform_int_dist.h:257-274) -- small cases only."""
+    comp = [c for c in range(n) if c not in pool]
+    sel = sorted(pool)
+    it = iter(int(w) for w in words)
+    for i in range(m - len(pool)):
+        rng_ = len(comp) - i
+        prod = next(it, 0) * rng_
+        low = prod & (2**64 - 1)
+        if low < rng_:
+            thr = (2**64 - rng_) % rng_
+            while low < thr:
+                prod = next(it, 0) * rng_
+                low = prod & (2**64 - 1)
+        j = i + (prod >> 64)
+        comp[i], comp[j] = comp[j], comp[i]
+        sel.append(comp[i])
+    return np.array(sorted(sel), np.uint32)
+
+
+def test_oracle_injected_stream():
+    """or_select_active_shards_stream: the true mt19937_64 words reproduce the seeded selection,
+    and zero words take the Lemire rejection loop exactly as a Python restatement does."""
+    n, k, b, m = 3_000, 6, 40, 600
+    g = O.random_graph(n, k, 2)
+    shards = [O.compress(g, 1, 0)]
+    lab = np.random.default_rng(1).integers(0, n, b).astype(np.uint32)
+    words = O.mt64_stream(5, m + 64)
+    rc, a, _ = O.select_shards("oracle", n, shards, lab, m, 5)
+    rc2, b_, _ = O.select_shards_stream(n, shards, lab, m, words)
+    assert rc == rc2 == 0 and np.array_equal(a, b_)
+    pool = set(int(c) for c in np.unique(g[lab].ravel()))
+    words[[2, 7, 8]] = 0
+    rc, c_, _ = O.select_shards_stream(n, shards, lab, m, words)
+    assert rc == 0 and not np.array_equal(a, c_)
+    assert np.array_equal(c_, _py_select_pad_stream(n, pool, m, words))
