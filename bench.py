@@ -239,7 +239,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             uid.copy_(torch.frombuffer(bytearray(X.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         comm = X.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
-    prec = X.PREC_BF16 if args.precision == "bf16" else X.PREC_FP32_EXACT
+    prec = {"bf16": X.PREC_BF16, "fp32": X.PREC_FP32, "fp32_exact": X.PREC_FP32_EXACT}[
+        args.precision]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         layer = X.KnnSoftmaxLayer(n, D, rank=rank, world=world, m_active=m, max_batch=b,
@@ -498,7 +499,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "fp32_exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)

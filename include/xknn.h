@@ -47,13 +47,18 @@ typedef enum {
   XKNN_ERR_UNSUPPORTED = 23
 } xknn_status_t;
 
-/* Arithmetic of the three fc GEMMs.  Selection, indices and the update are identical in both. */
+/* Arithmetic of the three fc GEMMs.  Selection, indices and the update are identical in all. */
 typedef enum {
-  /* tcgen05/TMEM tensor cores, bf16 operands, fp32 accumulation (the performance path) */
+  /* tcgen05/TMEM tensor cores, bf16 operands, fp32 accumulation (the performance path; stated
+     bf16 bound).  Needs 0 < scale <= 40 (fixed softmax stabilizer). */
   XKNN_PREC_BF16 = 0,
   /* CUDA-core fp32 with the reference's summation order (matrix.cpp:57-98), logits
-     materialized; the parity path, 1e-5 relative to the reference */
-  XKNN_PREC_FP32_EXACT = 1
+     materialized and bit-identical; any scale */
+  XKNN_PREC_FP32_EXACT = 1,
+  /* tcgen05/TMEM tensor cores at fp32 accuracy: 3xTF32 split operands (hi*hi + hi*lo + lo*hi,
+     kind::tf32), fp32 accumulation; within 1e-5 relative of the fp32 reference.  Needs
+     0 < scale <= 40 (fixed softmax stabilizer). */
+  XKNN_PREC_FP32 = 2
 } xknn_precision_t;
 
 typedef struct {

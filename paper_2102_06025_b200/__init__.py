@@ -30,6 +30,7 @@ VP = C.c_void_p
 
 PREC_BF16 = 0
 PREC_FP32_EXACT = 1
+PREC_FP32 = 2  # 3xTF32 tensor cores, fp32 accuracy
 FLAG_NO_GRAPH = 1
 
 
@@ -472,19 +473,23 @@ class KnnSoftmaxLayer:
         train_step must get the same labels).  ready_stream: the torch stream on which
         labels_local becomes valid (None: it already is)."""
         torch = self._torch
-        cur = torch.cuda.current_stream()
-        ready = ready_stream if ready_stream is not None else cur
+        ready = ready_stream
         if labels_local.dtype != torch.int32 or not labels_local.is_contiguous():
-            # the conversion runs on the current stream after the labels are valid; the side
-            # stream then waits for the converted buffer (not only for the caller's labels)
-            if ready != cur:
-                cur.wait_stream(ready)
-            lab = labels_local.to(torch.int32).contiguous()
-            ready = cur
+            # converted on a stream of its own (not the current one, which may be the layer
+            # stream with the step in flight: the selection must not wait for that), after the
+            # labels are valid; the layer's side stream then waits for the converted buffer
+            if getattr(self, "_conv_stream", None) is None:
+                self._conv_stream = torch.cuda.Stream()
+            conv = self._conv_stream
+            conv.wait_stream(ready if ready is not None else torch.cuda.current_stream())
+            with torch.cuda.stream(conv):
+                lab = labels_local.to(torch.int32).contiguous()
+            ready = conv
         else:
             lab = labels_local
         self._prep_keep = lab  # the buffer must outlive the asynchronous all-gather / copy
-        _check(_lib.xknn_prepare(self.h, lab.data_ptr(), lab.numel(), ready.cuda_stream))
+        _check(_lib.xknn_prepare(self.h, lab.data_ptr(), lab.numel(),
+                                 ready.cuda_stream if ready is not None else None))
 
     def train_step(self, features_local, labels_local, lr: float, grad_features_local=None,
                    loss_out=None, sync: bool = True, micro_batches: int = 1):

@@ -1030,7 +1030,7 @@ struct FastState {
 // splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
 // whole waves: the fewest splits with >= 95% wave efficiency (else the most efficient), at most
 // max_units units
-static uint32_t pair_splits(uint32_t nbp, uint32_t max_units, uint32_t streams = 74) {
+uint32_t gemm_pair_splits(uint32_t nbp, uint32_t max_units, uint32_t streams) {
   uint32_t best = 1;
   double best_eff = -1;
   for (uint32_t s = 1; s <= streams && (uint64_t)nbp * s <= max_units; ++s) {
@@ -1064,6 +1064,23 @@ static unsigned cluster_grid(K kernel, unsigned cluster, size_t smem) {
     return kNumSMs / cluster * cluster;
   }
   return std::min<unsigned>((unsigned)n * cluster, kNumSMs / cluster * cluster);
+}
+
+cudaError_t launch_rowreduce(const SelState* st, const float* partial, const float* labelterm,
+                             const int32_t* lcol, uint32_t B, uint32_t bpad, double* red,
+                             cudaStream_t s) {
+  launch_pdl(k_rowreduce, (unsigned)((B + 7) / 8), 1024, 0, s, st, partial, labelterm, lcol, B,
+             bpad, red);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dx_reduce(const float* partial, const double* red, uint32_t B, uint32_t nbt,
+                             uint32_t splits, float scale, const int32_t* lcol,
+                             const uint32_t* active, uint64_t begin, const float* W,
+                             const float* wnorm, float* out, cudaStream_t s) {
+  launch_pdl(k_dx_reduce, grid_for((uint64_t)B * 128, 256), 256, 0, s, partial, red, B, nbt,
+             splits, 256u, scale, lcol, active, begin, W, wnorm, out);
+  return cudaGetLastError();
 }
 
 xknn_status_t Layer::init_fast() {
@@ -1175,11 +1192,11 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   static const unsigned grid_f4 = cluster_grid(k_gemm2<kF, 2>, 4, smem_bytes2<kF>());
   static const unsigned grid_dx4 = cluster_grid(k_gemm2<kDX, 2>, 4, smem_bytes2<kDX>());
   if (mc) {
-    ga.splits = pair_splits(nbp / 2, 1u << 30, grid_f4 / 4);
+    ga.splits = gemm_pair_splits(nbp / 2, 1u << 30, grid_f4 / 4);
     launch_pdl_cluster(k_gemm2<kF, 2>, grid_f4, 384, smem_bytes2<kF>(), stream, 4u, f->mF_A,
                        f->mF2_B64, f->mPt_st, ga);
   } else {
-    ga.splits = pair_splits(nbp, 1u << 30);
+    ga.splits = gemm_pair_splits(nbp, 1u << 30);
     launch_pdl_cluster(k_gemm2<kF>, kNumSMs, 384, smem_bytes2<kF>(), stream, 2u, f->mF_A,
                        f->mF2_B, f->mPt_st, ga);
   }
@@ -1212,7 +1229,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
   ga.partial = f->partial_dx;
   const uint32_t dx_splits =
-      mc ? pair_splits(nbp / 2, 74, grid_dx4 / 4) : pair_splits(nbp, 148);
+      mc ? gemm_pair_splits(nbp / 2, 74, grid_dx4 / 4) : gemm_pair_splits(nbp, 148);
   ga.nbt = nbp;
   ga.splits = dx_splits;
   if (mc)

@@ -1,0 +1,734 @@
+// fast32.cu -- XKNN_PREC_FP32: the three fc GEMMs at fp32 accuracy on 5th-gen tensor cores, by
+// 3xTF32 operand splitting (tcgen05.mma kind::tf32, accumulators in TMEM, operands staged by TMA).
+//
+// Every fp32 operand a is stored as a_hi = tf32(a) (round to nearest) and a_lo = a - a_hi (exact
+// in fp32; the tensor core keeps its top 11 significant bits), and each product is
+//   a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi        (|error| <~ 2^-21 |a*b|, fp32 accumulation)
+// -- three kind::tf32 MMAs into the same TMEM accumulator.  This meets the north star's 1e-5
+// relative tolerance of the fp32 reference (matrix.cpp:57-98), which a single TF32 (2^-11) or
+// bf16 pass does not.
+//
+// The step has the BF16 path's structure (fast.cu), with fp32 hi/lo operands in place of bf16:
+//   GEMM-F   S = X_hat * W_subᵀ   (M = 256 batch rows / CTA pair, N = 256 classes, K = 512)
+//            epilogue: P~ = exp(s*S - s) (fixed stabilizer, |cos| <= 1), split hi/lo -> HBM,
+//            per-tile row sums and the label logit (as fast.cu)
+//   GEMM-dW  dW  = P~ᵀ * (diag(s*r) X_hat)     (M = 256 classes, N = 512, K = B) -> fp32 rows
+//   GEMM-dX  dX  = diag(s*r) * (P~ * W_sub)    (M = 256 batch, N = 512, K = M_w split) -> fp32
+// with r_b = 1 / (B * sum_b); the one-hot part of G is applied exactly in fp32 by k_dx_reduce and
+// the row update (LabelFix), as on the BF16 path.
+//
+// Shared-memory tiles (per CTA of a cta_group::2 pair; 128B swizzle unless noted):
+//   F : A = X_hat rows   K-major, 128 rows x 32 fp32 (128 B), hi + lo;  B = W_sub rows, same
+//   dX: A = P~ rows      K-major, 128 rows x 16 fp32 (64 B, 64B swizzle), hi + lo
+//       B = W_sub        MN-major (d contiguous): 2 N-halves x 4 atoms of 32 d x 16 K rows
+//   dW: A = P~ᵀ          MN-major (classes contiguous): 4 atoms of 32 classes x 16 K rows
+//       B = X_hat'       MN-major, as dX's B
+// MN-major tf32 operands exist only in the 128B swizzle with 32-byte granules (UMMA layout type
+// SWIZZLE_128B_BASE32B: 128 B along MN x 4 K rows per atom, granules XORed with row % 4), loaded
+// by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; LBO = stride between MN atoms, SBO = stride
+// between 4-row K groups.
+// Warp roles as fast.cu: warp 0 TMA producer, warp 1 MMA issuer (leader CTA), warp 2 TMEM
+// allocator, warps 4-11 epilogue.
+#include <cudaTypedefs.h>
+
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace xknn {
+
+namespace {
+
+enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2 };
+
+// Instruction descriptor, kind::tf32: TF32 A/B (format 2), fp32 D.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t m, uint32_t n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+
+constexpr uint32_t kSwizzle128Base32 = 1;  // UMMA descriptor layout type
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct Gemm3Args {
+  const SelState* st;
+  uint32_t B, bpad, nbt, splits;
+  float scale;
+  const int32_t* label_col;
+  float* p_hi;  // P~ [bpad][ldp] fp32 hi / lo (GEMM-F output)
+  float* p_lo;
+  uint64_t ldp;
+  float* partial;    // F: [2 * class tiles][bpad] row sums; dX: split-K partial rows
+  float* labelterm;  // F: [bpad]
+};
+
+template <int KIND>
+struct Cfg3;
+template <>
+struct Cfg3<kF3> {
+  static constexpr uint32_t STAGES = 3, A_BYTES = 2 * 128 * 128, B_BYTES = 2 * 128 * 128;
+  static constexpr uint32_t NBUF = 2, ACC = 256, KB = 32;  // KB: K elements per stage
+};
+template <>
+struct Cfg3<kDX3> {
+  static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 128 * 64, B_BYTES = 2 * 8 * 2048;
+  static constexpr uint32_t NBUF = 1, ACC = 512, KB = 16;
+};
+template <>
+struct Cfg3<kDW3> {
+  static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 4 * 2048, B_BYTES = 2 * 8 * 2048;
+  static constexpr uint32_t NBUF = 1, ACC = 512, KB = 16;
+};
+constexpr uint32_t kStg3 = 4096;  // per epilogue warp: one 32 x 32 fp32 staging block
+
+template <int KIND>
+constexpr uint32_t smem_bytes3() {
+  using C = Cfg3<KIND>;
+  return C::STAGES * (C::A_BYTES + C::B_BYTES) + 8 * kStg3 + 1024 + 256;
+}
+
+struct Unit3 {
+  uint32_t row0;    // F/dX: first batch row of the pair; dW: first class of the pair
+  uint32_t t0, t1;  // F: class-tile range; dX: 16-class K-chunk range; dW: unused
+  uint32_t id;
+  bool valid;
+};
+
+template <int KIND>
+__device__ __forceinline__ uint32_t num_units3(const Gemm3Args& a, uint32_t mw) {
+  if (KIND == kDW3) return (mw + 255) / 256;
+  return a.nbt * a.splits;
+}
+
+template <int KIND>
+__device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint32_t u) {
+  Unit3 x{};
+  x.id = u;
+  if (KIND == kDW3) {
+    x.row0 = u * 256;
+    x.valid = true;
+    return x;
+  }
+  const uint32_t bp = u % a.nbt, r = u / a.nbt;
+  const uint32_t nt = KIND == kF3 ? (mw + 255) / 256 : (mw + 15) / 16;
+  x.row0 = bp * 256;
+  x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
+  x.t1 = (uint32_t)((uint64_t)(r + 1) * nt / a.splits);
+  x.valid = KIND == kDX3 || x.t1 > x.t0;  // dX units always write their (maybe zero) partial
+  return x;
+}
+
+// one thread's 32 fp32 of a row into a 128B-swizzled 32 x 32 staging block (TMA-store layout)
+__device__ __forceinline__ void stage_f32(uint8_t* buf, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {
+    float4* d = reinterpret_cast<float4*>(buf + r * 128 + ((c ^ (r & 7)) * 16));
+    *d = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+// the same for the tf32 split of the values: LO = false: tf32(v), LO = true: v - tf32(v)
+template <bool LO>
+__device__ __forceinline__ void stage_split(uint8_t* buf, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {
+    float t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float x = v[4 * c + i], hi = tf32_rna(x);
+      t[i] = LO ? x - hi : hi;
+    }
+    float4* d = reinterpret_cast<float4*>(buf + r * 128 + ((c ^ (r & 7)) * 16));
+    *d = make_float4(t[0], t[1], t[2], t[3]);
+  }
+}
+// ... and the block to global rows `ld` floats apart: lane l writes row 4i + l/8, 16-B unit l%8
+// (four full 128-B row segments per instruction)
+__device__ __forceinline__ void store_f32_block(const uint8_t* buf, float* dst, uint64_t ld,
+                                                uint32_t lane) {
+  const uint32_t c = lane & 7;
+#pragma unroll
+  for (uint32_t i = 0; i < 8; ++i) {
+    const uint32_t r = 4 * i + (lane >> 3);
+    const float4 v = *reinterpret_cast<const float4*>(buf + r * 128 + ((c ^ (r & 7)) * 16));
+    *reinterpret_cast<float4*>(dst + (uint64_t)r * ld + c * 4) = v;
+  }
+  __syncwarp();
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(384, 1)
+    k_gemm3(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
+            const __grid_constant__ CUtensorMap tmBhi, const __grid_constant__ CUtensorMap tmBlo,
+            const __grid_constant__ CUtensorMap tmOut, Gemm3Args a) {
+  using C = Cfg3<KIND>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;                                // [stage][hi | lo]
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;         // [stage][hi | lo]
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;       // epilogue staging, 8 warps x 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * kStg3);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = tc::cluster_ctarank() & 1;
+  const bool leader = cta == 0;
+  const uint32_t pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    for (uint32_t s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (uint32_t s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 16);  // 8 epilogue warps in each CTA of the pair
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmAhi);
+    tc::tma_prefetch(&tmAlo);
+    tc::tma_prefetch(&tmBhi);
+    tc::tma_prefetch(&tmBlo);
+    if (KIND != kF3) tc::tma_prefetch(&tmOut);
+  }
+  if (warp == 2) tc::tmem_alloc_2sm<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+  griddep_wait();
+
+  const uint32_t mw = a.st->active_count;
+  const uint32_t nunits = num_units3<KIND>(a, mw);
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs load their half) =================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t u = pair; u < nunits; u += npairs) {
+        const Unit3 x = unit3_of<KIND>(a, mw, u);
+        if (!x.valid) continue;
+        const int32_t myrow = (int32_t)(x.row0 + cta * 128);
+        const uint32_t nk = KIND == kF3 ? (x.t1 - x.t0) * (512 / C::KB)
+                                        : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
+        for (uint32_t k = 0; k < nk; ++k) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          uint8_t* dA = sA + stage * C::A_BYTES;
+          uint8_t* dB = sB + stage * C::B_BYTES;
+          if (KIND == kF3) {
+            const int32_t kc = (int32_t)((k % 16) * 32);
+            const int32_t crow = (int32_t)((x.t0 + k / 16) * 256 + cta * 128);
+            tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
+            tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
+            tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
+            tc::tma_load_2d_2sm(dB + C::B_BYTES / 2, &tmBlo, &full[stage], kc, crow);
+          } else {
+            const int32_t kk = (int32_t)((KIND == kDX3 ? x.t0 + k : k) * 16);
+            if (KIND == kDX3) {  // P~ [b][class]: this CTA's 128 batch rows, 16 classes
+              tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kk, myrow);
+              tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kk, myrow);
+            } else {  // P~ᵀ: this CTA's 128 classes (4 atoms of 32) at batch rows kk..kk+15
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                tc::tma_load_2d_2sm(dA + t * 2048, &tmAhi, &full[stage], myrow + 32 * t, kk);
+                tc::tma_load_2d_2sm(dA + C::A_BYTES / 2 + t * 2048, &tmAlo, &full[stage],
+                                    myrow + 32 * t, kk);
+              }
+            }
+            // B [K rows][512 d]: this CTA's 128 d of each 256-wide N instruction j, 4 atoms
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int32_t dc = (int32_t)(256 * j + 128 * cta + 32 * t);
+                tc::tma_load_2d_2sm(dB + (j * 4 + t) * 2048, &tmBhi, &full[stage], dc, kk);
+                tc::tma_load_2d_2sm(dB + C::B_BYTES / 2 + (j * 4 + t) * 2048, &tmBlo,
+                                    &full[stage], dc, kk);
+              }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA, one thread) =================
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, buf = 0, tphase = 0;
+      for (uint32_t u = pair; u < nunits; u += npairs) {
+        const Unit3 x = unit3_of<KIND>(a, mw, u);
+        if (!x.valid) continue;
+        const uint32_t ntile = KIND == kF3 ? x.t1 - x.t0 : 1;
+        for (uint32_t t = 0; t < ntile; ++t) {
+          tc::mbar_wait(&tempty[buf], tphase ^ 1);
+          tc::fence_after_sync();
+          const uint32_t dcol = tbase + buf * C::ACC;
+          const uint32_t nk =
+              KIND == kF3 ? 16 : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
+          for (uint32_t k = 0; k < nk; ++k) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::fence_after_sync();
+            const uint32_t ah = tc::smem_u32(sA + stage * C::A_BYTES), al = ah + C::A_BYTES / 2;
+            const uint32_t bh = tc::smem_u32(sB + stage * C::B_BYTES), bl = bh + C::B_BYTES / 2;
+            if (KIND == kF3) {
+              constexpr uint32_t id = idesc_tf32(256, 256, false, false);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 8 fp32 = 32 B per instruction
+                const uint64_t dah = tc::smem_desc(ah + kk * 32, 16, 1024, tc::kSwizzle128);
+                const uint64_t dal = tc::smem_desc(al + kk * 32, 16, 1024, tc::kSwizzle128);
+                const uint64_t dbh = tc::smem_desc(bh + kk * 32, 16, 1024, tc::kSwizzle128);
+                const uint64_t dbl = tc::smem_desc(bl + kk * 32, 16, 1024, tc::kSwizzle128);
+                mma_tf32_2sm(dcol, dal, dbh, id, (k | kk) != 0);  // small terms first
+                mma_tf32_2sm(dcol, dah, dbl, id, 1u);
+                mma_tf32_2sm(dcol, dah, dbh, id, 1u);
+              }
+            } else {
+              constexpr uint32_t id = idesc_tf32(256, 256, KIND == kDW3, true);
+#pragma unroll
+              for (uint32_t ks = 0; ks < 2; ++ks) {  // K = 8 rows per instruction
+                const uint64_t dah =
+                    KIND == kDX3 ? tc::smem_desc(ah + ks * 32, 16, 512, tc::kSwizzle64)
+                                 : tc::smem_desc(ah + ks * 1024, 2048, 512, kSwizzle128Base32);
+                const uint64_t dal =
+                    KIND == kDX3 ? tc::smem_desc(al + ks * 32, 16, 512, tc::kSwizzle64)
+                                 : tc::smem_desc(al + ks * 1024, 2048, 512, kSwizzle128Base32);
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                  const uint64_t dbh =
+                      tc::smem_desc(bh + j * 8192 + ks * 1024, 2048, 512, kSwizzle128Base32);
+                  const uint64_t dbl =
+                      tc::smem_desc(bl + j * 8192 + ks * 1024, 2048, 512, kSwizzle128Base32);
+                  mma_tf32_2sm(dcol + j * 256, dal, dbh, id, (k | ks) != 0);
+                  mma_tf32_2sm(dcol + j * 256, dah, dbl, id, 1u);
+                  mma_tf32_2sm(dcol + j * 256, dah, dbh, id, 1u);
+                }
+              }
+            }
+            tc::mma_commit_2sm(&empty[stage]);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (nk) {
+            tc::mma_commit_2sm(&tfull[buf]);
+          } else {  // an empty split-K range: the epilogue writes zeros
+            tc::mbar_arrive_remote(&tfull[buf], 0);
+            tc::mbar_arrive_remote(&tfull[buf], 1);
+          }
+          if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs: their own 128 rows) =================
+    const uint32_t q = warp & 3, h = (warp - 4) >> 2, ew = warp - 4;
+    const uint32_t row = q * 32 + lane;
+    const uint32_t lane_addr = (q * 32) << 16;
+    uint8_t* stg = sStg + ew * kStg3;
+    uint32_t buf = 0, tphase = 0;
+    for (uint32_t u = pair; u < nunits; u += npairs) {
+      const Unit3 x = unit3_of<KIND>(a, mw, u);
+      if (!x.valid) continue;
+      const uint32_t ntile = KIND == kF3 ? x.t1 - x.t0 : 1;
+      for (uint32_t t = 0; t < ntile; ++t) {
+        tc::mbar_wait(&tfull[buf], tphase);
+        tc::fence_after_sync();
+        const uint32_t tb = tbase + buf * C::ACC + lane_addr;
+        const int32_t grow0 = (int32_t)(x.row0 + cta * 128 + q * 32);  // this warp's 32 rows
+        if (KIND == kF3) {
+          const uint32_t ct = x.t0 + t;
+          const uint32_t b = x.row0 + cta * 128 + row;
+          const bool vrow = b < a.B;
+          const int32_t lc = vrow ? a.label_col[b] : -1;
+          const float k2 = a.scale * 1.4426950408889634f;
+          float sum = 0.f, lab = 0.f;
+          bool has = false;
+          auto process = [&](const uint32_t (&r)[32], uint32_t ch) {
+            const uint32_t c0 = ct * 256 + h * 128 + ch * 32;
+            float e[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const bool ok = vrow && c0 + j < mw;
+              e[j] = ok ? ex2_approx(fmaf(__uint_as_float(r[j]), k2, -k2)) : 0.f;
+              sum += e[j];
+            }
+            if (lc >= (int32_t)c0 && lc < (int32_t)c0 + 32) {  // at most once per row
+              const int32_t idx = lc - (int32_t)c0;
+              float sel = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) sel = (j == idx) ? __uint_as_float(r[j]) : sel;
+              lab = sel * a.scale;
+              has = true;
+            }
+            const uint64_t off = (uint64_t)grow0 * a.ldp + c0;
+            stage_split<false>(stg, lane, e);
+            __syncwarp();
+            store_f32_block(stg, a.p_hi + off, a.ldp, lane);
+            stage_split<true>(stg, lane, e);
+            __syncwarp();
+            store_f32_block(stg, a.p_lo + off, a.ldp, lane);
+          };
+          uint32_t ra[32], rb[32];
+          tc::tmem_ld32_issue(tb + h * 128, ra);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 32, rb);
+          process(ra, 0);
+          tc::tmem_ld_wait(rb);
+          tc::tmem_ld32_issue(tb + h * 128 + 64, ra);
+          process(rb, 1);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld32_issue(tb + h * 128 + 96, rb);
+          process(ra, 2);
+          tc::tmem_ld_wait(rb);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
+          process(rb, 3);
+          a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
+          if (has) a.labelterm[b] = lab - a.scale;
+        } else {
+          // dX: split-K partial rows of unit x.id; dW: fp32 dW rows (compact active order)
+          const int32_t orow = KIND == kDX3 ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
+          const bool zero = KIND == kDX3 && x.t1 == x.t0;
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < 8; ++ch) {
+            const uint32_t col = h * 256 + ch * 32;
+            float v[32];
+            if (!zero) {
+              tc::tmem_ld32(tb + col, v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            stage_f32(stg, lane, v);
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tc::tma_store_2d(&tmOut, stg, (int32_t)col, orow);
+              tc::tma_store_commit();
+              tc::tma_store_wait_read<0>();
+            }
+            __syncwarp();
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote_relaxed(&tempty[buf], 0);
+        }
+        if (++buf == C::NBUF) { buf = 0; tphase ^= 1; }
+      }
+    }
+    if (lane == 0) tc::tma_store_wait_all();
+    __syncwarp();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();
+  if (warp == 2) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_2sm<512>(tbase);
+  }
+}
+
+// X_hat' = x_hat * s / (B * sum) split hi/lo (pad rows zero); the batch rows of every local label
+// column linked into lists for the row update; the step's loss (block 0, k_loss's arithmetic)
+__global__ void k_fixup32(const double* __restrict__ red, const int32_t* __restrict__ lcol,
+                          const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
+                          uint32_t bpad, float scale, int32_t* __restrict__ lab_head,
+                          int32_t* __restrict__ lab_next, float* __restrict__ xs_hi,
+                          float* __restrict__ xs_lo, double* __restrict__ loss, SelState* st,
+                          unsigned long long* err) {
+  griddep_wait();
+  griddep_launch();
+  if (blockIdx.x == 0) {
+    __shared__ double part[256];
+    double s = 0.0;
+    const uint32_t chunk = (B + blockDim.x - 1) / blockDim.x;
+    for (uint32_t i = threadIdx.x * chunk; i < min(B, (threadIdx.x + 1) * chunk); ++i) {
+      if (red[2 * B + i] != 1.0) raise_error(err, XKNN_ERR_LABEL_OUT_OF_RANGE, i);
+      s += log(red[i]) - red[B + i];
+    }
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (uint32_t k = 0; k < blockDim.x; ++k) t += part[k];
+      const double l = t / (double)B;
+      *loss = l;
+      st->loss = l;
+    }
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < bpad;
+       b += (gridDim.x * blockDim.x) >> 5) {
+    float4* dh = reinterpret_cast<float4*>(xs_hi + (uint64_t)b * 512);
+    float4* dl = reinterpret_cast<float4*>(xs_lo + (uint64_t)b * 512);
+    if (b >= B) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        dh[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dl[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    const int32_t lc = lcol[b];
+    if (lane == 0 && lc >= 0) lab_next[b] = atomicExch(&lab_head[lc], (int32_t)b);
+    const float inv = 1.0f / xnorm[b];
+    const float rs = (float)((double)scale / ((double)B * red[b]));
+    const float4* xp = reinterpret_cast<const float4*>(X + (uint64_t)b * 512);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float4 x = xp[lane + 32 * c];
+      const float4 v = make_float4(__fmul_rn(__fmul_rn(x.x, inv), rs), __fmul_rn(__fmul_rn(x.y, inv), rs),
+                                   __fmul_rn(__fmul_rn(x.z, inv), rs), __fmul_rn(__fmul_rn(x.w, inv), rs));
+      const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+      dh[lane + 32 * c] = hi;
+      dl[lane + 32 * c] = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+    }
+  }
+}
+
+// rows [count, round_up(count, 256)) of W_sub hi/lo must be zero for GEMM-dX's K loop
+__global__ void k_zero_rows32(const SelState* st, float* whi, float* wlo, uint32_t cap_rows) {
+  griddep_wait();
+  griddep_launch();
+  const uint32_t c = st->active_count;
+  const uint32_t e = min(cap_rows, (c + 255) / 256 * 256);
+  const uint64_t n = (uint64_t)(e - c) * 512 / 4;
+  float4* ph = reinterpret_cast<float4*>(whi + (uint64_t)c * 512);
+  float4* pl = reinterpret_cast<float4*>(wlo + (uint64_t)c * 512);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    ph[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    pl[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn3() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// fp32 row-major [outer][inner] tensor, box_inner x box_outer
+bool make_map32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  auto fn = encode_fn3();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct Fast32State {
+  uint32_t bpad = 0, mwpad = 0;
+  uint64_t dx_units_cap = 0;
+  float *xh_hi = nullptr, *xh_lo = nullptr;  // X_hat hi/lo [bpad][512]
+  float *xs_hi = nullptr, *xs_lo = nullptr;  // X_hat' hi/lo [bpad][512]
+  float *w_hi = nullptr, *w_lo = nullptr;    // W_sub hi/lo [mwpad][512]
+  float *p_hi = nullptr, *p_lo = nullptr;    // P~ hi/lo [bpad][mwpad]
+  float* partial_f = nullptr;                // [2 * mwpad/256][bpad]
+  float* labelterm = nullptr;                // [bpad]
+  float* partial_dx = nullptr;               // [units][256][512]
+  float* dW32 = nullptr;                     // [mwpad][512]
+  int32_t* lab_head = nullptr;               // [mwpad]
+  int32_t* lab_next = nullptr;               // [bpad]
+  CUtensorMap mF_Ah, mF_Al, mF_Bh, mF_Bl;    // X_hat, W_sub (K-major, 32 x 128 boxes)
+  CUtensorMap mDX_Ah, mDX_Al, mDX_Bh, mDX_Bl, mDX_st;  // P~ (16 x 128, SW64), W_sub (32 x 16)
+  CUtensorMap mDW_Ah, mDW_Al, mDW_Bh, mDW_Bl, mDW_st;  // P~ (32 x 16), X_hat' (32 x 16)
+};
+
+xknn_status_t Layer::init_fast32() {
+  auto* f = new Fast32State;
+  fast32 = f;
+  if (d != 512) return fail_msg(XKNN_ERR_UNSUPPORTED, "FP32 tensor-core path is specialised for D = 512");
+  f->bpad = (uint32_t)((bmax + 255) / 256 * 256);
+  f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
+  ldp = f->mwpad;
+  const uint64_t xb = (uint64_t)f->bpad * 512, wb = (uint64_t)f->mwpad * 512,
+                 pb = (uint64_t)f->bpad * f->mwpad;
+  for (float** p : {&f->xh_hi, &f->xh_lo, &f->xs_hi, &f->xs_lo}) {
+    XK_CUDA(dalloc(p, xb));
+    XK_CUDA(cudaMemsetAsync(*p, 0, xb * 4, stream));
+  }
+  for (float** p : {&f->w_hi, &f->w_lo}) {
+    XK_CUDA(dalloc(p, wb));
+    XK_CUDA(cudaMemsetAsync(*p, 0, wb * 4, stream));
+  }
+  for (float** p : {&f->p_hi, &f->p_lo}) {
+    XK_CUDA(dalloc(p, pb));
+    XK_CUDA(cudaMemsetAsync(*p, 0, pb * 4, stream));
+  }
+  XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
+  XK_CUDA(dalloc(&f->labelterm, f->bpad));
+  f->dx_units_cap = 148ull * 256;
+  XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
+  XK_CUDA(dalloc(&f->dW32, wb));
+  XK_CUDA(dalloc(&f->lab_head, f->mwpad));
+  XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));
+  XK_CUDA(dalloc(&f->lab_next, f->bpad));
+  XK_CUDA(dalloc(&dXpart, (uint64_t)f->bpad * d));
+  const auto S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  const auto S32G = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;  // MN-major tf32 operands
+  bool ok = true;
+  ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, 32, 128, S128);
+  ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, 32, 128, S128);
+  ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, 32, 128, S128);
+  ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, 32, 128, S128);
+  ok &= make_map32(&f->mDX_Ah, f->p_hi, f->mwpad, f->bpad, 16, 128, S64);
+  ok &= make_map32(&f->mDX_Al, f->p_lo, f->mwpad, f->bpad, 16, 128, S64);
+  ok &= make_map32(&f->mDX_Bh, f->w_hi, 512, f->mwpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDX_Bl, f->w_lo, 512, f->mwpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDX_st, f->partial_dx, 512, f->dx_units_cap, 32, 32, S128);
+  ok &= make_map32(&f->mDW_Ah, f->p_hi, f->mwpad, f->bpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDW_Al, f->p_lo, f->mwpad, f->bpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDW_Bh, f->xs_hi, 512, f->bpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDW_Bl, f->xs_lo, 512, f->bpad, 32, 16, S32G);
+  ok &= make_map32(&f->mDW_st, f->dW32, 512, f->mwpad, 32, 32, S128);
+  if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kF3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kF3>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDX3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kDX3>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDW3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kDW3>()));
+  return XKNN_OK;
+}
+
+void Layer::free_fast32() {
+  auto* f = static_cast<Fast32State*>(fast32);
+  if (!f) return;
+  for (void* p : {(void*)f->xh_hi, (void*)f->xh_lo, (void*)f->xs_hi, (void*)f->xs_lo,
+                  (void*)f->w_hi, (void*)f->w_lo, (void*)f->p_hi, (void*)f->p_lo,
+                  (void*)f->partial_f, (void*)f->labelterm, (void*)f->partial_dx, (void*)f->dW32,
+                  (void*)f->lab_head, (void*)f->lab_next})
+    if (p) cudaFree(p);
+  delete f;
+  fast32 = nullptr;
+}
+
+xknn_status_t Layer::reset_fast32_scratch() {
+  auto* f = static_cast<Fast32State*>(fast32);
+  if (!f) return XKNN_OK;
+  XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));
+  return XKNN_OK;
+}
+
+xknn_status_t Layer::run_fast32_core(uint64_t B) {
+  auto* f = static_cast<Fast32State*>(fast32);
+  const uint32_t D = (uint32_t)d;
+  if (B > f->bpad) return XKNN_ERR_INVALID_ARGUMENT;
+  // (a) operands: the active weight rows gathered + normalized, split hi/lo (feature all-gather
+  //     runs under it at P > 1), then X_hat hi/lo
+  XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, f->w_hi, nullptr,
+                                wnorm, err, stream, false, f->w_lo));
+  ++launches;
+  launch_pdl(k_zero_rows32, 64, 256, 0, stream, (const SelState*)st, f->w_hi, f->w_lo, f->mwpad);
+  XK_LAUNCH();
+  if (world > 1) XK_TRY(wait_features());
+  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, f->xh_hi, nullptr, xnorm, err,
+                                stream, false, f->xh_lo));
+  ++launches;
+  mark(3);
+  Gemm3Args ga{};
+  ga.st = st;
+  ga.B = (uint32_t)B;
+  ga.bpad = f->bpad;
+  ga.scale = cfg.scale;
+  ga.label_col = label_col;
+  ga.p_hi = f->p_hi;
+  ga.p_lo = f->p_lo;
+  ga.ldp = ldp;
+  ga.labelterm = f->labelterm;
+  const uint32_t nbp = (uint32_t)((B + 255) / 256);
+  // (b) GEMM-F with the fused exp / row-sum / label-logit epilogue
+  ga.partial = f->partial_f;
+  ga.nbt = nbp;
+  ga.splits = gemm_pair_splits(nbp, 1u << 30);
+  launch_pdl_cluster(k_gemm3<kF3>, kNumSMs, 384, smem_bytes3<kF3>(), stream, 2u, f->mF_Ah,
+                     f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, ga);
+  XK_LAUNCH();
+  mark(4);
+  // (c) row statistics -> all-reduce over the class shards -> (d) loss, X_hat', label lists
+  XK_CUDA(launch_rowreduce(st, f->partial_f, f->labelterm, label_col, (uint32_t)B, f->bpad, rowred,
+                           stream));
+  ++launches;
+  if (world > 1) {
+    if (par_ar.ready) {
+      XK_CUDA(par_ar.launch(rowred, 3 * B, err, stream));
+      ++launches;
+    } else {
+      XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
+    }
+  }
+  launch_pdl(k_fixup32, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, (const double*)rowred,
+             (const int32_t*)label_col, (const float*)X, (const float*)xnorm, (uint32_t)B, f->bpad,
+             cfg.scale, f->lab_head, f->lab_next, f->xs_hi, f->xs_lo, loss_dev, st, err);
+  XK_LAUNCH();
+  mark(5);
+  // (e) GEMM-dW -> fp32 dW rows (compact active order)
+  launch_pdl_cluster(k_gemm3<kDW3>, kNumSMs, 384, smem_bytes3<kDW3>(), stream, 2u, f->mDW_Ah,
+                     f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, ga);
+  XK_LAUNCH();
+  mark(6);
+  // (f) GEMM-dX split-K partials -> reduce (+ one-hot correction) -> reduce-scatter
+  ga.partial = f->partial_dx;
+  const uint32_t dx_splits = gemm_pair_splits(nbp, 148);
+  ga.nbt = nbp;
+  ga.splits = dx_splits;
+  launch_pdl_cluster(k_gemm3<kDX3>, kNumSMs, 384, smem_bytes3<kDX3>(), stream, 2u, f->mDX_Ah,
+                     f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, ga);
+  XK_LAUNCH();
+  mark(7);
+  XK_CUDA(launch_dx_reduce(f->partial_dx, rowred, (uint32_t)B, nbp, dx_splits, cfg.scale,
+                           label_col, active, begin, W, wnorm, world > 1 ? dXpart : dX, stream));
+  ++launches;
+  const uint64_t bl = B / world;
+  if (world > 1) {
+    XK_CUDA(cudaEventRecord(ev_fork, stream));
+    XK_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, side));
+    XK_CUDA(cudaEventRecord(ev_join, side));
+  }
+  // (g) normalize-backward + momentum SGD on the active rows, with the one-hot correction
+  mark(8);
+  LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B)};
+  XK_CUDA(launch_update_rows(W, V, f->dW32, active, &st->active_count, mw_cap, begin, D, wnorm,
+                             lr_dev, cfg.momentum, cfg.weight_decay, err, stream, 148u * 16u, lf));
+  ++launches;
+  if (world > 1) XK_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+  return XKNN_OK;
+}
+
+}  // namespace xknn
+static_assert(xknn::smem_bytes3<xknn::kF3>() <= 232448, "GEMM-F tf32 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kDX3>() <= 232448, "GEMM-dX tf32 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kDW3>() <= 232448, "GEMM-dW tf32 pair smem");

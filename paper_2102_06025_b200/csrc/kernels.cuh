@@ -19,7 +19,7 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
                                   float* norms, unsigned long long* err, cudaStream_t s,
-                                  bool seq = false);
+                                  bool seq = false, float* out_lo = nullptr);
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,
@@ -56,4 +56,16 @@ cudaError_t launch_softmax_grad(float* L, uint64_t rows, const unsigned int* col
                                 uint64_t max_cols, const float* rowmax, const double* red,
                                 const int32_t* label_col, cudaStream_t s);
 
+}  // namespace xknn
+
+namespace xknn {
+// fast.cu: pieces shared by the BF16 and FP32 (3xTF32) tensor-core paths
+cudaError_t launch_rowreduce(const SelState* st, const float* partial, const float* labelterm,
+                             const int32_t* lcol, uint32_t B, uint32_t bpad, double* red,
+                             cudaStream_t s);
+cudaError_t launch_dx_reduce(const float* partial, const double* red, uint32_t B, uint32_t nbt,
+                             uint32_t splits, float scale, const int32_t* lcol,
+                             const uint32_t* active, uint64_t begin, const float* W,
+                             const float* wnorm, float* out, cudaStream_t s);
+uint32_t gemm_pair_splits(uint32_t nbp, uint32_t max_units, uint32_t streams = 74);
 }  // namespace xknn

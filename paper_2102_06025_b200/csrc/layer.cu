@@ -127,6 +127,8 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
     XK_CUDA(dalloc(&Wsub, mw_cap * d));
     XK_CUDA(dalloc(&logits, bmax * mw_cap * 2));  // logits, then G
     XK_CUDA(dalloc(&dXpart, bmax * d));
+  } else if (cfg.precision == XKNN_PREC_FP32) {
+    XK_TRY(init_fast32());
   } else {
     XK_TRY(init_fast());
   }
@@ -162,6 +164,7 @@ void Layer::free_all() {
   if (comm_ag) ncclCommDestroy(comm_ag);
   par_ar.release();
   free_fast();
+  free_fast32();
 }
 
 // The padding draw's raw stream: std::mt19937_64(rng_seed), re-seeded by the reference on every
@@ -312,6 +315,8 @@ xknn_status_t Layer::run_core(uint64_t B) {
       XK_NCCL(ncclReduceScatter(dXpart, dX, bl * d, ncclFloat, ncclSum, comm, stream));
     else
       XK_CUDA(cudaMemcpyAsync(dX, dXpart, B * d * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+  } else if (cfg.precision == XKNN_PREC_FP32) {
+    XK_TRY(run_fast32_core(B));
   } else {
     XK_TRY(run_fast_core(B));
   }
@@ -496,7 +501,7 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   //     right before the first kernel that reads X.
   if (world > 1) {
     if (!comm_ag) XK_NCCL(ncclCommSplit(comm, 0, rank, &comm_ag, nullptr));  // collective
-    if (!par_ar.ready && !par_ar_tried && cfg.precision == XKNN_PREC_BF16 &&
+    if (!par_ar.ready && !par_ar_tried && cfg.precision != XKNN_PREC_FP32_EXACT &&
         !getenv("XKNN_NCCL_ALLREDUCE")) {
       // collective; without CUDA IPC between the ranks the statistics go through NCCL
       par_ar_tried = true;
@@ -663,7 +668,8 @@ xknn_status_t xknn_layer_create(int rank, int world, uint64_t n, uint64_t d,
   if (cfg->max_batch == 0 || cfg->max_batch % world)
     return fail(XKNN_ERR_INVALID_ARGUMENT, "max_batch must be a positive multiple of world");
   if (cfg->m_active > n) return fail(XKNN_ERR_INVALID_ARGUMENT, "M exceeds the class count");
-  if (cfg->precision != XKNN_PREC_BF16 && cfg->precision != XKNN_PREC_FP32_EXACT)
+  if (cfg->precision != XKNN_PREC_BF16 && cfg->precision != XKNN_PREC_FP32_EXACT &&
+      cfg->precision != XKNN_PREC_FP32)
     return fail(XKNN_ERR_CONFIG, "unknown precision");
   if (xknn_status_t s = check_scale(cfg); s != XKNN_OK) return s;
   auto* h = new (std::nothrow) xknn_layer;
@@ -912,6 +918,7 @@ xknn_status_t xknn_layer_sync(xknn_layer_t* h) {
   if (w) {
     XK_CUDA_H(cudaMemsetAsync(L.err, 0, 8, L.stream));
     XK_TRY_H(L.reset_fast_scratch());
+    XK_TRY_H(L.reset_fast32_scratch());
     XK_CUDA_H(cudaStreamSynchronize(L.stream));
     const xknn_status_t code = (xknn_status_t)(w & 0xff);
     xknn::g_row = w >> 8;
@@ -937,7 +944,7 @@ xknn_status_t xknn_layer_last_logits(xknn_layer_t* h, float* out, uint64_t capac
   GUARD_H(h);
   Layer& L = h->L;
   if (L.cfg.precision != XKNN_PREC_FP32_EXACT)
-    return fail(XKNN_ERR_UNSUPPORTED, "logits are never materialized in BF16 precision");
+    return fail(XKNN_ERR_UNSUPPORTED, "logits are only materialized in FP32_EXACT precision");
   xknn::SelState hs;
   XK_CUDA_H(cudaMemcpyAsync(&hs, L.st, sizeof(hs), cudaMemcpyDeviceToHost, L.stream));
   XK_CUDA_H(cudaStreamSynchronize(L.stream));

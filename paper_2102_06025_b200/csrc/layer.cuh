@@ -215,6 +215,13 @@ struct Layer {
   void free_fast();
   xknn_status_t run_fast_core(uint64_t batch);
   xknn_status_t reset_fast_scratch();
+
+  // FP32 (3xTF32) tensor-core path (fast32.cu)
+  void* fast32 = nullptr;
+  xknn_status_t init_fast32();
+  void free_fast32();
+  xknn_status_t run_fast32_core(uint64_t batch);
+  xknn_status_t reset_fast32_scratch();
 };
 
 }  // namespace xknn

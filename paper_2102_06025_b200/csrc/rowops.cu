@@ -40,7 +40,7 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
                                  const uint32_t* __restrict__ row_ids, const unsigned int* count,
                                  uint64_t id_base, float* __restrict__ out32,
                                  __nv_bfloat16* __restrict__ out16, float* __restrict__ norms,
-                                 unsigned long long* err) {
+                                 unsigned long long* err, float* __restrict__ out_lo) {
   griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = count ? *count : rows;
@@ -92,7 +92,14 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
       o.z = __fmul_rn(v[c].z, inv);
       o.w = __fmul_rn(v[c].w, inv);
       const uint64_t col = (uint64_t)(lane + 32 * c) * 4;
-      if (out32) *reinterpret_cast<float4*>(out32 + r * d + col) = o;
+      if (out_lo) {  // 3xTF32 operand split: out32 = tf32(o) (round to nearest), out_lo = o - it
+        const float4 hi = make_float4(tf32_rna(o.x), tf32_rna(o.y), tf32_rna(o.z), tf32_rna(o.w));
+        *reinterpret_cast<float4*>(out32 + r * d + col) = hi;
+        *reinterpret_cast<float4*>(out_lo + r * d + col) =
+            make_float4(o.x - hi.x, o.y - hi.y, o.z - hi.z, o.w - hi.w);
+      } else if (out32) {
+        *reinterpret_cast<float4*>(out32 + r * d + col) = o;
+      }
       if (out16) store_bf16x4(out16 + r * d + col, o.x, o.y, o.z, o.w);
     }
   }
@@ -125,14 +132,14 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
   const uint64_t nrows = *count;
   for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < nrows;
        t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-    // the batch rows labelled with this class, ascending (lists are almost always 1 long)
-    int32_t lh = -1;
-    if (lf.head) {
-      lh = lf.head[t];
+    // the batch rows labelled with this class (lists are almost always empty or 1 long); the
+    // list head is cleared after the row's last access (no load waits behind that store)
+    const int32_t lh = lf.head ? lf.head[t] : -1;
+    if (dead) {
       __syncwarp();
       if (lane == 0 && lh >= 0) lf.head[t] = -1;
+      continue;
     }
-    if (dead) continue;
     const uint64_t row = (uint64_t)active[t] - begin;
     float4* wp = reinterpret_cast<float4*>(W + row * d);
     float4* vp = reinterpret_cast<float4*>(V + row * d);
@@ -205,6 +212,10 @@ __global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
 #undef XKNN_UPD
       vp[lane + 32 * c] = v;
       wp[lane + 32 * c] = w[c];
+    }
+    if (lh >= 0) {
+      __syncwarp();
+      if (lane == 0) lf.head[t] = -1;
     }
   }
 }
@@ -282,16 +293,23 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
                                   float* norms, unsigned long long* err, cudaStream_t s,
-                                  bool seq) {
+                                  bool seq, float* out_lo) {
   const unsigned grid = grid_for(rows * 32, 256);
   if (seq) {
-    if (d != 512) return cudaErrorInvalidValue;
-    launch_pdl(k_normalize_rows<4, true>, grid, 256, 0, s, in, rows, d, row_ids, count, id_base,
-               out32, out16, norms, err);
+#define XKNN_SEQ_CASE(DV)                                                                      \
+  case DV:                                                                                     \
+    launch_pdl(k_normalize_rows<DV, true>, grid, 256, 0, s, in, rows, d, row_ids, count, id_base, \
+               out32, out16, norms, err, out_lo);                                              \
+    break;
+    switch (d / 128) {
+      XKNN_SEQ_CASE(1) XKNN_SEQ_CASE(2) XKNN_SEQ_CASE(4) XKNN_SEQ_CASE(8)
+      default: return cudaErrorInvalidValue;
+    }
+#undef XKNN_SEQ_CASE
     return cudaGetLastError();
   }
   XKNN_DISPATCH_D(d, k_normalize_rows, grid, 256, s, in, rows, d, row_ids, count, id_base, out32,
-                  out16, norms, err);
+                  out16, norms, err, out_lo);
   return cudaGetLastError();
 }
 

@@ -54,7 +54,7 @@ def main():
 
     n, d, b, k, m = args.n, 512, args.b, args.k, args.m
     w, g = problem(n, d, k, 7)
-    prec = X.PREC_BF16 if args.precision == "bf16" else X.PREC_FP32_EXACT
+    prec = {"bf16": X.PREC_BF16, "fp32": X.PREC_FP32_EXACT, "fp32tc": X.PREC_FP32}[args.precision]
     layer = make_layer(n, d, world, rank, m, b, w, g, precision=prec, seed=42, comm=comm)
     rng = np.random.default_rng(99)
     bl = b // world

@@ -16,8 +16,8 @@ import numpy as np
 import pytest
 
 import oracle_lib as O
-from gpu_util import (device_graph, host_label_csr, make_layer, parity_record, rel_err,
-                      torch_cuda)
+from gpu_util import (BF16_GRAD, BF16_LOSS, device_graph, host_label_csr, make_layer,
+                      parity_record, rel_err, torch_cuda)
 
 pytestmark = pytest.mark.gpu
 
@@ -135,9 +135,9 @@ def test_step_c2_bf16():
     r = _c2_step(X.PREC_BF16, 2)
     parity_record("c2_bf16", **r)
     for e in r["steps"]:
-        assert e["loss_rel"] <= 2e-4
-        assert e["gf_relF"] <= 1e-2
-    assert r["update_relF"] <= 1e-2
+        assert e["loss_rel"] <= BF16_LOSS
+        assert e["gf_relF"] <= BF16_GRAD
+    assert r["update_relF"] <= BF16_GRAD
 
 
 def test_step_c2_fp32_exact():
@@ -145,6 +145,18 @@ def test_step_c2_fp32_exact():
 
     r = _c2_step(X.PREC_FP32_EXACT, 1)
     parity_record("c2_fp32_exact", **r)
+    for e in r["steps"]:
+        assert e["loss_rel"] <= 1e-5
+        assert e["gf_relF"] <= 1e-5
+    assert r["update_relF"] <= 1e-5
+    assert r["velocity_relF"] <= 1e-5
+
+
+def test_step_c2_fp32_tensor_cores():
+    import paper_2102_06025_b200 as X
+
+    r = _c2_step(X.PREC_FP32, 2)
+    parity_record("c2_fp32tc", **r)
     for e in r["steps"]:
         assert e["loss_rel"] <= 1e-5
         assert e["gf_relF"] <= 1e-5
