@@ -45,12 +45,64 @@ PHASES = ["allgather", "select", "gather_normalize", "gemm_logits_softmax", "sof
 
 
 def peaks():
+    """Roofline denominators.  HBM GB/s and bf16 TF/s (burst: best of 10; sustained: back to
+    back for 4 s) from the driver-written MEASURED_PEAKS.json; TF32 (cuBLAS TF32 8192^3 via
+    torch, same method, tools/measure_tf32.py) from profiles/r02/tf32_peak.json.  Fallbacks:
+    B200_PROFILING.md's figures."""
+    out = {"hbm": 6650.0, "bf16_burst": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+        out.update(hbm=p["hbm_gbs"], bf16_burst=p["bf16_tflops"],
+                   bf16_sus=p["bf16_tflops_sustained"], src="MEASURED_PEAKS.json")
     except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        pass
+    out.update(tf32_burst=out["bf16_burst"] / 2, tf32_sus=out["bf16_sus"] / 2,
+               tf32_src="half the bf16 peak (nominal ratio)")
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "tf32_peak.json")) as f:
+            t = json.load(f)
+        out.update(tf32_burst=t["tf32_tflops"], tf32_sus=t["tf32_tflops_sustained"],
+                   tf32_src="profiles/r02/tf32_peak.json (cuBLAS TF32, measured)")
+    except Exception:
+        pass
+    return out
+
+
+def kernel_rooflines(phase_ms, precision, b, mw, splits, pk, burst):
+    """Per-phase roofline of one step (SURVEY 8(d) units, stated per launch).  GEMMs: 2*B*M_w*D
+    algorithmic flops each; HBM kernels: their algorithmic bytes (the update: 16*M_w*D = W and
+    velocity read + written in fp32 -- the dW row it also reads is not credited; the gather: the
+    M_w fp32 rows read + their tensor-core operand copy written).  Peak: burst when the clocks
+    sat at max with no throttle reason, else sustained."""
+    f32 = precision != "bf16"
+    opb = 8 if f32 else 2  # bytes per element of a tensor-core operand copy (hi+lo | bf16)
+    tflops = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if f32 else (
+        pk["bf16_burst"] if burst else pk["bf16_sus"])
+    gemm = 2.0 * b * mw * D
+    work = {
+        "gemm_logits_softmax": ("tensor", gemm),
+        "gemm_dW": ("tensor", gemm),
+        "gemm_dX": ("tensor", gemm),
+        "update": ("hbm", 16.0 * mw * D),
+        "gather_normalize": ("hbm", (4.0 + opb) * mw * D + (4.0 + opb) * b * D),
+        "softmax_stats": ("hbm", 2.0 * math.ceil(mw / 256) * b * 4 + (4.0 + opb) * b * D),
+        "dX_reduce_scatter": ("hbm", (splits + 1) * 4.0 * b * D),
+        "feature_backward": ("hbm", 3 * 4.0 * b * D),
+    }
+    rows, floor_ms = {}, 0.0
+    for name, (bound, w) in work.items():
+        ms = phase_ms.get(name)
+        if not ms:
+            continue
+        if bound == "tensor":
+            ach, peak, unit = w / (ms / 1e3) / 1e12, tflops, "TFLOP/s"
+        else:
+            ach, peak, unit = w / (ms / 1e3) / 1e9, pk["hbm"], "GB/s"
+        floor_ms += (w / (peak * (1e12 if bound == "tensor" else 1e9))) * 1e3
+        rows[name] = {"bound": bound, "ms": round(ms, 4), "work": w, "achieved": round(ach, 2),
+                      "peak": round(peak, 1), "unit": unit, "frac": round(ach / peak, 4)}
+    return rows, floor_ms
 
 
 # ----------------------------------------------------------------------------------------------
@@ -148,42 +200,55 @@ def make_batches(torch, n, b_local, rank, count=4):
 # ----------------------------------------------------------------------------------------------
 # the reference (CPU) arm
 # ----------------------------------------------------------------------------------------------
-def reference_cpu(wl, steps, warmup, budget_s=150.0, log=print):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_cpu(wl, steps, warmup, budget_s=150.0, workers=None, max_n=1_000_000):
     """The reference's stock HybridSim::train_step (kKnn) from oracle/_ref (compiled from the
-    unmodified reference sources), P = nproc worker threads (SimOptions::worker_threads, the
-    reference's only multi-core mechanism).  Falls back to the oracle port (1 thread)."""
+    unmodified reference sources) at the workload's FULL global batch, with `workers` simulated
+    workers (SimOptions::worker_threads: one thread each, the reference's only multi-core
+    mechanism; default nproc; 1 = one core).  Falls back to the oracle port (1 thread).
+    Bounded sample: the warm-up step (which also allocates the velocity) is timed first, and only
+    as many of the requested steps are timed as fit budget_s (at least one)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
 
-    n_full, b_full, k = wl["n"], wl["b"], wl["k"]
-    # bounded sample: beyond 1M classes the reference's step is O(N*D) host work per step
-    # (whole-shard normalization, a dense N/P x D gradient block) and tens of GB of host RAM,
-    # minutes per step at 10M -- it is timed at 1M classes with the workload's batch and k.
-    # Its cost per sample grows with N, so this overstates the reference's rate at N > 1M.
-    n = min(n_full, 1_000_000)
+    n_full, b, k = wl["n"], wl["b"], wl["k"]
+    # beyond 1M classes the reference's step is O(N*D) host work per step (whole-shard
+    # normalization, a dense N/P x D gradient block) and tens of GB of host RAM, minutes per step
+    # at 10M: it is timed at max_n classes with the workload's batch and k (its per-sample cost
+    # grows with N, so this overstates its rate there)
+    n = min(n_full, max_n)
     m = max(1, int(math.ceil(0.1 * n)))
     cores = os.cpu_count() or 1
     rng = np.random.default_rng(SEED)
     w = (rng.standard_normal((n, D), dtype=np.float32) * np.float32(0.05)).astype(np.float32)
     g = O.random_graph(n, k, 7)
     kind = "reference" if O.ref_available() else "port"
-    p = cores if kind == "reference" else 1
-    while b_full % p:
+    p = (workers or cores) if kind == "reference" else 1
+    while b % p:
         p -= 1
-    shards = [O.compress(g, p, s) for s in range(p)]
+    shards = [O.compress(g, p, s_) for s_ in range(p)]
     del g
 
-    def batch(bs, i):
+    def batch(i):
         r = np.random.default_rng(100 + i)
-        return (r.standard_normal((bs, D), dtype=np.float32),
-                r.integers(0, n, bs).astype(np.uint32))
+        return (r.standard_normal((b, D), dtype=np.float32),
+                r.integers(0, n, b).astype(np.uint32))
 
     if kind == "reference":
-        sim = O.RefSim(w, p, threads=True, scale=SCALE, momentum=MOMENTUM)
+        sim = O.RefSim(w, p, threads=p > 1, scale=SCALE, momentum=MOMENTUM)
         sim.set_graphs(shards)
 
-        def one(bs, i):
-            x, y = batch(bs, i)
+        def one(i):
+            x, y = batch(i)
             t = time.perf_counter()
             rc, loss, _ = sim.step(x, y, m, SEED, LR, reset_fe=False)
             assert rc == 0, rc
@@ -191,33 +256,33 @@ def reference_cpu(wl, steps, warmup, budget_s=150.0, log=print):
     else:
         vel = np.zeros_like(w)
 
-        def one(bs, i):
-            x, y = batch(bs, i)
+        def one(i):
+            x, y = batch(i)
             t = time.perf_counter()
             rc, *_ = O.fc_train_step(w, vel, x, y, shards, m, SEED, SCALE, LR, MOMENTUM, 0.0)
             assert rc == 0, rc
             return time.perf_counter() - t
 
-    # bounded sample: the full global batch if the run fits the budget, else a sub-batch
-    bs = b_full
-    t0 = one(bs, 0)  # also the velocity-allocating first step
-    total = steps + max(warmup - 1, 0)
-    while t0 * total > budget_s and bs // 2 >= 16 and (bs // 2) % p == 0:
-        bs //= 2
-        t0 = one(bs, 1)
-    for i in range(max(warmup - 1, 0)):
-        one(bs, 2 + i)
-    times = [one(bs, 100 + i) for i in range(steps)]
+    t0 = one(0)  # warm-up 1 (allocates the velocity); always run
+    t_start = time.perf_counter()
+    done_warm = 1
+    while done_warm < warmup and (time.perf_counter() - t_start) + t0 < budget_s / 3:
+        t0 = one(done_warm)
+        done_warm += 1
+    n_timed = max(1, min(steps, int(budget_s / max(t0, 1e-3))))
+    times = [one(100 + i) for i in range(n_timed)]
     med = float(np.median(times))
-    return dict(value=bs / med, unit="samples/s", cores=p if kind == "reference" else 1,
-                kind=kind,
+    return dict(value=b / med, unit="samples/s", cores=p if kind == "reference" else 1,
+                kind=kind, steps_timed=n_timed, warmup_steps=done_warm, cpu_model=cpu_model(),
+                nproc=cores,
                 sample=(f"{'HybridSim::train_step(kKnn)' if kind == 'reference' else 'oracle port'}"
                         f" at N={n}" + (f" (bounded sample of the N={n_full} workload: the "
                                         f"reference's per-sample cost grows with N, so this "
                                         f"overstates its rate there)" if n < n_full else "") +
-                        f", k={k}, M={m}, D={D}, batch {bs} of {b_full}, P={p} worker "
-                        f"threads, median of {steps} steps on {cores} host cores"),
-                ms_per_step=med * 1e3)
+                        f", k={k}, M={m}, D={D}, full batch {b}, P={p} worker thread(s), median of "
+                        f"{n_timed} step(s) after {done_warm} warm-up, {cores} host cores ("
+                        f"{cpu_model()})"),
+                ms_per_step=med * 1e3, config_n=n)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -394,29 +459,37 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
     if rank == 0:
         ms_step = ms / args.steps
         value = b / (ms_step / 1e3)
-        hbm, tf_burst, tf_sus, pk_src = peaks()
-        gemms = {k_: phase_ms[k_] for k_ in ("gemm_logits_softmax", "gemm_dW", "gemm_dX")}
-        dom = max(gemms, key=gemms.get)
-        if args.precision == "bf16":
-            flops = 2.0 * (((b + 127) // 128) * 128) * active_local * D  # per launch, algorithmic
-            achieved = flops / (gemms[dom] / 1e3) / 1e12
-            traffic = None
-            tp = os.path.join(ROOT, "profiles", f"traffic_{wl_name}.json")
-            if os.path.exists(tp):
-                try:
-                    traffic = json.load(open(tp)).get(dom)
-                except Exception:
-                    traffic = None
-            roof = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 2),
-                    "peak": tf_sus, "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4),
-                    "traffic": traffic, "peak_source": f"{pk_src} bf16 sustained",
-                    "flops_per_launch": flops, "launch_ms": round(gemms[dom], 4)}
-        else:
-            roof = {"bound": "tensor", "kernel": dom, "achieved": None, "peak": tf_sus,
-                    "unit": "TFLOP/s", "frac": None, "traffic": None}
-        # whole-step roofline: max(6 B M_w D / Pi, 16 M_w D / beta)
-        t_roof = max(6.0 * b * mw_max * D / (tf_sus * 1e12), 16.0 * mw_max * D / (hbm * 1e9))
+        pk = peaks()
         clocks = clk.summary()
+        # burst peaks when the SMs ran at their max clock with no throttle reason in the timed
+        # region (a short run that never reached the power limit), else the sustained ones
+        burst = (clocks.get("sm_mhz") is not None and clocks.get("sm_max_mhz") is not None and
+                 clocks["sm_mhz"] >= 0.98 * clocks["sm_max_mhz"] and not clocks["reasons"])
+        splits = max(1, -(-148 // max(1, -(-b // 256))))  # dX split-K ranges (upper bound)
+        kern, floor_ms = kernel_rooflines(phase_ms, args.precision, b, active_local, splits, pk,
+                                          burst)
+        dom = max(kern, key=lambda k_: kern[k_]["ms"])
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r02", f"traffic_{wl_name}_{args.precision}.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(dom)
+            except Exception:
+                traffic = None
+        kd = kern[dom]
+        roof = {"bound": kd["bound"], "kernel": dom, "achieved": kd["achieved"],
+                "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
+                "work_per_launch": kd["work"], "launch_ms": kd["ms"],
+                "peak_source": (("tf32 " + pk["tf32_src"] + " / 3 (3xTF32)")
+                                if args.precision != "bf16" and kd["bound"] == "tensor" else
+                                pk["src"]) + (" burst" if burst else " sustained"),
+                "how": "work per launch / the kernel's CUDA-event time on the layer stream "
+                       "(phase_ms, second pass); dominant = the longest phase"}
+        # whole-step floors: every kernel at its own roofline, serialized (the step's kernels
+        # run back to back), and the SURVEY 8(d) overlap bound max(flops/peak, bytes/peak)
+        tpk = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if args.precision != "bf16" \
+            else (pk["bf16_burst"] if burst else pk["bf16_sus"])
+        t_roof = max(6.0 * b * mw_max * D / (tpk * 1e12), 16.0 * mw_max * D / (pk["hbm"] * 1e9))
         res = {
             "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
                       "B200 vs roofline",
@@ -430,6 +503,10 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None,
             "dtype": "bf16" if args.precision == "bf16" else "f32",
+            "precision": {"bf16": "bf16 operands, fp32 accumulation (stated bound, DESIGN.md 2)",
+                          "fp32": "3xTF32 tensor cores, fp32 accuracy (1e-5 of the reference)",
+                          "fp32_exact": "CUDA-core fp32 in the reference's summation order"}[
+                              args.precision],
             "data": "synthetic (W~N(0,0.05^2), X~N(0,1), uniform labels, seeded random "
                     "self-first k-NN graph)",
             "config": {"workload": wl_name, "num_classes": n, "dim": D, "global_batch": b,
@@ -447,8 +524,13 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                            "loss"},
             "gpu_launches": int(launches),
             "roofline": roof,
-            "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4),
-                              "frac": round(t_roof * 1e3 / ms_step, 4)},
+            "kernels": kern,
+            "step_roofline": {"t_floor_serial_ms": round(floor_ms, 4),
+                              "frac_serial": round(floor_ms / ms_step, 4),
+                              "t_roof_overlap_ms": round(t_roof * 1e3, 4),
+                              "frac_overlap": round(t_roof * 1e3 / ms_step, 4),
+                              "how": "serial: sum over the step's kernels of work/peak; overlap: "
+                                     "max(6*B*M_w*D/tensor peak, 16*M_w*D/HBM peak)"},
             "phase_ms": {k_: round(v, 4) for k_, v in phase_ms.items()},
             "phase_profile": {"ms_per_step": round(ms_prof / args.steps, 4), "steps": args.steps,
                               "how": "second pass of the same steps with CUDA events at the "
@@ -514,17 +596,21 @@ def main():
         if rank != 0:
             return
         r = reference_cpu(wl, args.steps, args.warmup)
+        same = r["config_n"] == wl["n"]
         emit({
             "impl": "reference",
             "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
                       "B200 vs roofline",
             "value": round(r["value"], 3), "unit": "samples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_step"], 2),
+            "steps": r["steps_timed"], "steps_requested": args.steps,
+            "warmup": r["warmup_steps"], "ms_per_step": round(r["ms_per_step"], 2),
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl_name, "num_classes": wl["n"], "dim": D,
                        "global_batch": wl["b"], "k": wl["k"]},
-            "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")},
+            "same_config": same,
+            "cpu_baseline": {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample",
+                                                  "cpu_model", "nproc")},
             "e2e": {"value": round(r["value"], 3), "unit": "samples/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         })
@@ -540,11 +626,17 @@ def main():
     res = run_ours(args, wl_name, wl, rank, world, local_rank, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and wl_name in ("c1", "c2"):
+            # the reference on all host cores (P = nproc worker threads) and on one
+            # core (P = 1), full batch, median after a warm-up step
             try:
-                r = reference_cpu(wl, 1, 1, budget_s=40.0)
+                r = reference_cpu(wl, 3, 1, budget_s=40.0)
                 res["cpu_baseline"] = {k_: r[k_] for k_ in ("value", "unit", "cores", "kind",
-                                                            "sample")}
+                                                            "sample", "cpu_model", "nproc")}
                 res["cpu_baseline"]["value"] = round(res["cpu_baseline"]["value"], 3)
+                r1 = reference_cpu(WORKLOADS["c1"], 3, 1, budget_s=30.0, workers=1)
+                res["cpu_baseline"]["single_core_c1"] = {
+                    "value": round(r1["value"], 3), "unit": "samples/s", "cores": 1,
+                    "sample": r1["sample"]}
             except Exception as e:  # the baseline is reported, never required
                 res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
         else:

@@ -621,6 +621,58 @@ int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k,
   return OR_OK;
 }
 
+/* Sampled rows of build_graph_bruteforce over a class matrix streamed in chunks (for checks at
+   sizes where the matrix does not fit host memory): nq query rows (global ids qid[], vectors q)
+   keep their exact top-k lists (sc/ix/sz, nq x k) under `better` while chunks of rows
+   [base, base + rows) pass by, in any order -- `better` is a strict total order, so the final
+   lists equal or_graph_row's.  Same per-pair arithmetic as or_graph_row (ascending-d fp32 dot).
+   Parallel over row blocks of the chunk (private lists, merged under the same order). */
+static void cand_insert(float* sc, uint32_t* ix, uint64_t* sz, uint64_t k, float dot, uint32_t i,
+                        uint32_t self) {
+  if (*sz == k && !better(dot, i, sc[*sz - 1], ix[*sz - 1], self)) return;
+  uint64_t pos = 0;
+  while (pos < *sz && better(sc[pos], ix[pos], dot, i, self)) ++pos;
+  uint64_t last = *sz < k ? *sz : k - 1;
+  for (uint64_t q = last; q > pos; --q) { sc[q] = sc[q - 1]; ix[q] = ix[q - 1]; }
+  sc[pos] = dot;
+  ix[pos] = i;
+  if (*sz < k) ++*sz;
+}
+
+void or_graph_rows_update(uint64_t nq, uint64_t d, const float* q, const uint64_t* qid, uint64_t k,
+                          const float* chunk, uint64_t rows, uint64_t base, float* sc, uint32_t* ix,
+                          uint64_t* sz) {
+  const uint64_t RB = 4096, nb = (rows + RB - 1) / RB;
+  float* psc = (float*)malloc(nb * nq * k * sizeof(float));
+  uint32_t* pix = (uint32_t*)malloc(nb * nq * k * sizeof(uint32_t));
+  uint64_t* psz = (uint64_t*)calloc(nb * nq, sizeof(uint64_t));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (uint64_t blk = 0; blk < nb; ++blk) {
+    const uint64_t r1 = (blk + 1) * RB < rows ? (blk + 1) * RB : rows;
+    for (uint64_t r = blk * RB; r < r1; ++r) {
+      const float* wi = chunk + r * d;
+      for (uint64_t a = 0; a < nq; ++a) {
+        const float* wj = q + a * d;
+        float dot = 0.0f;
+        for (uint64_t t = 0; t < d; ++t) dot += wj[t] * wi[t];
+        const uint64_t o = blk * nq + a;
+        cand_insert(psc + o * k, pix + o * k, psz + o, k, dot, (uint32_t)(base + r),
+                    (uint32_t)qid[a]);
+      }
+    }
+  }
+  for (uint64_t blk = 0; blk < nb; ++blk)
+    for (uint64_t a = 0; a < nq; ++a) {
+      const uint64_t o = blk * nq + a;
+      for (uint64_t e = 0; e < psz[o]; ++e)
+        cand_insert(sc + a * k, ix + a * k, sz + a, k, psc[o * k + e], pix[o * k + e],
+                    (uint32_t)qid[a]);
+    }
+  free(psc);
+  free(pix);
+  free(psz);
+}
+
 /* classify_retrieval (the reference tree has no implementation, this
    restates the spec): the nearest class of each query among the L2-normalized class weights,
    i.e. the argmax of the cosine logits matmul(q_hat, w_hat, T) (matrix.cpp:57-68 order; the

@@ -58,6 +58,9 @@ int or_topk(uint64_t len, const float* t, uint64_t k, uint64_t* out_idx, float* 
 uint64_t or_selected_count(double ratio, uint64_t len);
 int or_dgc_step(uint64_t len, const float* g, float* vel, float* res, double ratio, float mom,
                 uint64_t* out_idx, float* out_val, uint64_t* count);
+void or_graph_rows_update(uint64_t nq, uint64_t d, const float* q, const uint64_t* qid, uint64_t k,
+                          const float* chunk, uint64_t rows, uint64_t base, float* sc, uint32_t* ix,
+                          uint64_t* sz);
 int or_graph_row(uint64_t n, uint64_t d, const float* w, uint64_t j, uint64_t k, uint32_t* out);
 int or_fc_train_step(uint64_t n, uint64_t d, uint64_t p, float* w, float* velocity,
                      const float* x, const uint32_t* labels, uint64_t b,

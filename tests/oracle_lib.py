@@ -255,6 +255,33 @@ def graph_row(w_norm: np.ndarray, j: int, k: int) -> np.ndarray:
     return out
 
 
+class GraphRowChecker:
+    """Exact build_graph_bruteforce rows of a few query classes over a class matrix streamed in
+    chunks (or_graph_rows_update): feed every chunk once, in any order; rows() then equals
+    graph_row() on the whole matrix."""
+
+    def __init__(self, qid, q: np.ndarray, k: int):
+        self.qid = np.ascontiguousarray(qid, np.uint64)
+        self.q = np.ascontiguousarray(q, np.float32)
+        self.k = k
+        nq = self.qid.size
+        self.sc = np.zeros((nq, k), np.float32)
+        self.ix = np.zeros((nq, k), np.uint32)
+        self.sz = np.zeros(nq, np.uint64)
+        fn = oracle().or_graph_rows_update
+        fn.restype = None
+        fn.argtypes = [U64, U64, f32p, u64p, U64, f32p, U64, U64, f32p, u32p, u64p]
+
+    def update(self, chunk: np.ndarray, base: int) -> None:
+        chunk = np.ascontiguousarray(chunk, np.float32)
+        oracle().or_graph_rows_update(self.qid.size, self.q.shape[1], self.q, self.qid, self.k,
+                                      chunk, chunk.shape[0], base, self.sc, self.ix, self.sz)
+
+    def rows(self) -> np.ndarray:
+        assert (self.sz == self.k).all()
+        return self.ix.copy()
+
+
 def l2_normalize(x: np.ndarray):
     x = np.ascontiguousarray(x, np.float32)
     r, c = x.shape

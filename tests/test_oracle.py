@@ -267,3 +267,18 @@ def test_oracle_injected_stream():
     rc, c_, _ = O.select_shards_stream(n, shards, lab, m, words)
     assert rc == 0 and not np.array_equal(a, c_)
     assert np.array_equal(c_, _py_select_pad_stream(n, pool, m, words))
+
+
+def test_graph_row_checker_streamed():
+    """GraphRowChecker (chunks streamed in any order) == graph_row on the whole matrix."""
+    rng = np.random.default_rng(4)
+    n, d, k = 3_000, 64, 12
+    rc, wn, _, _ = O.l2_normalize(rng.standard_normal((n, d)).astype(np.float32))
+    wn[17] = wn[900]  # an exact duplicate: a score tie resolved by index
+    qid = np.array([0, 17, 900, 2999, 1234])
+    chk = O.GraphRowChecker(qid, wn[qid], k)
+    for c0 in (2000, 0, 1000):  # out of order
+        chk.update(wn[c0:c0 + 1000], c0)
+    got = chk.rows()
+    for a, j in enumerate(qid):
+        assert np.array_equal(got[a], O.graph_row(wn, int(j), k))

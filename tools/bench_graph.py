@@ -5,8 +5,13 @@ P GPUs (one process per GPU; torchrun for P > 1) on N synthetic class weights, D
     torchrun --nproc-per-node 2 tools/bench_graph.py --n 4000000 --k 100
 
 Prints one JSON line: pairs/s (N^2 / time, max over ranks), the candidate GEMM's tensor-core
-work as a fraction of the measured bf16/fp16 peak, uncertified rows.  Weights are random
-N(0, 1) rows normalized on device (random-init class weights, as the bench's fc layer)."""
+work as a fraction of the measured bf16/fp16 peak (burst when the clocks sampled during the
+timed build sat at max with no throttle reason, else sustained), the clocks, uncertified rows,
+and a bit-exact check of --verify sampled rows (spread over the ranks) against
+build_graph_bruteforce's rows computed by the oracle (oracle/liboracle.so, the test
+infrastructure) over the whole class matrix, which every rank regenerates chunk by chunk from
+the seeds and streams through host memory.  Weights are random N(0, 1) rows normalized on device
+(random-init class weights, as the bench's fc layer)."""
 import argparse
 import json
 import os
@@ -24,6 +29,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--classes", type=int, default=1_000_000)
 ap.add_argument("--k", type=int, default=100)
 ap.add_argument("--kprime", type=int, default=200)
+ap.add_argument("--verify", type=int, default=16, help="sampled rows checked against the oracle")
 a = ap.parse_args()
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
@@ -36,13 +42,23 @@ if world > 1:
     uid = [X.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = X.nccl_comm_init(uid[0], world, rank)
+CH = 1 << 20
+
+
+def block_chunks(s):
+    """Rank s's normalized class rows, chunk by chunk (deterministic in the seed)."""
+    bs, es = X.ShardLayout(a.classes, world).class_range(s)
+    gs = torch.Generator(device="cuda")
+    gs.manual_seed(1000 + s)
+    for r0 in range(0, es - bs, CH):
+        blk = torch.randn(min(CH, es - bs - r0), 512, device="cuda", generator=gs)
+        yield bs + r0, blk / blk.norm(dim=1, keepdim=True)
+
+
 b, e = X.ShardLayout(a.classes, world).class_range(rank)
-g = torch.Generator(device="cuda")
-g.manual_seed(1000 + rank)
 w = torch.empty(e - b, 512, device="cuda")
-for r0 in range(0, e - b, 1 << 20):
-    blk = torch.randn(min(1 << 20, e - b - r0), 512, device="cuda", generator=g)
-    w[r0:r0 + blk.shape[0]] = blk / blk.norm(dim=1, keepdim=True)
+for c0, blk in block_chunks(rank):
+    w[c0 - b:c0 - b + blk.shape[0]] = blk
     del blk
 # warm-up (module load, kernel attributes, NCCL channels) on a small problem
 ws = w[: max(64, min(4096, e - b))].contiguous()
@@ -52,33 +68,76 @@ torch.cuda.synchronize()
 if world > 1:
     dist.barrier()
 # two full-size builds; the second is timed (the first pays the allocator's first touches)
+from bench import ClockSampler  # noqa: E402
+
 for rep in range(2):
     if world > 1:
         dist.barrier()
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    if rep == 1:
+        clk.__enter__()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     out, unc, steps = X.graph_ring(w, a.classes, a.k, a.kprime, rank, world, comm)
     ev1.record()
     ev1.synchronize()
     sec = ev0.elapsed_time(ev1) / 1e3
-    del out
+    if rep == 1:
+        clk.__exit__(None, None, None)
+    else:
+        del out
+clocks = clk.summary()
+
+# sampled rows vs the oracle's build_graph_bruteforce rows over the whole (regenerated) matrix
+import numpy as np  # noqa: E402
+
+nq = -(-a.verify // world) if a.verify > 0 else 0
+ok, checked = 1, 0
+if nq:
+    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tests"))
+    import oracle_lib as O  # noqa: E402
+
+    t_v = time.perf_counter()
+    loc = np.random.default_rng(77 + rank).choice(e - b, size=min(nq, e - b), replace=False)
+    chk = O.GraphRowChecker(loc + b, w[torch.from_numpy(loc).cuda()].cpu().numpy(), a.k)
+    for s_ in range(world):
+        for c0, blk in block_chunks(s_):
+            chk.update(blk.cpu().numpy(), c0)
+            del blk
+    want = chk.rows()
+    got = out[torch.from_numpy(loc).cuda()].cpu().numpy().view(np.uint32)
+    ok = int(np.array_equal(got, want))
+    checked = len(loc)
+    verify_s = time.perf_counter() - t_v
+del out
 if world > 1:
     t = torch.tensor([sec, float(unc)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     sec = float(t[0])
-    ut = torch.tensor([float(unc)], dtype=torch.float64)
+    ut = torch.tensor([float(unc), float(checked)], dtype=torch.float64)
     dist.all_reduce(ut)
-    unc = int(ut.item())
+    unc, checked = int(ut[0].item()), int(ut[1].item())
+    okt = torch.tensor([ok], dtype=torch.int64)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    ok = int(okt.item())
 if rank == 0:
     peaks = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))
     pairs = float(a.classes) * a.classes
     tf = 2.0 * pairs * 512 / sec / 1e12
+    burst = (clocks.get("sm_mhz") is not None and clocks.get("sm_max_mhz") is not None and
+             clocks["sm_mhz"] >= 0.98 * clocks["sm_max_mhz"] and not clocks["reasons"])
+    pk = peaks["bf16_tflops"] if burst else peaks["bf16_tflops_sustained"]
     print(json.dumps({"metric": "exact KNN graph rebuild pairs/s", "n": a.classes, "k": a.k,
                       "kprime": a.kprime, "n_gpus": world, "seconds": round(sec, 3),
                       "pairs_per_s": pairs / sec, "tflops_equiv": round(tf, 1),
-                      "frac_of_tensor_peak": round(tf / (world * peaks["bf16_tflops_sustained"]), 4),
-                      "peak_source": "MEASURED_PEAKS bf16 sustained (fp16 same rate)",
-                      "uncertified_rows": unc, "transfer_steps": int(steps)}))
+                      "frac_of_tensor_peak": round(tf / (world * pk), 4),
+                      "peak_source": "MEASURED_PEAKS bf16 " + ("burst" if burst else "sustained")
+                                     + " (fp16 same rate)",
+                      "clocks": clocks, "uncertified_rows": unc, "transfer_steps": int(steps),
+                      "verified_rows": checked, "verified_bit_exact": bool(ok),
+                      "verify_s_rank0": round(verify_s, 1) if nq else None}))
 if world > 1:
     X.nccl_comm_destroy(comm)
     dist.destroy_process_group()
