@@ -75,6 +75,9 @@ typedef struct {
 /* The step's device work (selection .. update) is captured once per batch size into a CUDA
    graph and replayed; this flag launches it kernel by kernel instead. */
 #define XKNN_FLAG_NO_GRAPH 1
+/* A selection-only layer: graph + Algorithm-1 selection state, no weight/velocity shard and no
+   step scratch (xknn_select only; parameter and step calls return XKNN_ERR_UNSUPPORTED). */
+#define XKNN_FLAG_SELECT_ONLY 2
 
 typedef struct xknn_layer xknn_layer_t;
 
@@ -119,6 +122,15 @@ xknn_status_t xknn_layer_weights_ptr(xknn_layer_t* h, float** w_dev);
 xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* k_per_class,
                                        const uint64_t* offsets, const uint32_t* flat,
                                        uint64_t flat_len, int on_device);
+
+/* xknn_layer_set_graph_csr with a per-entry rank (rank[flat_len], NULL = the position within
+   the class's list): lets one layer hold several shards' slices of a label concatenated into one
+   list, each entry ranked within its own slice -- select_active_classes(span<CompressedKnnGraph>)
+   (knn_softmax.cpp:117-134) over P shards on one device. */
+xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* k_per_class,
+                                              const uint64_t* offsets, const uint32_t* flat,
+                                              const uint32_t* rank, uint64_t flat_len,
+                                              int on_device);
 
 /* select_active_classes(span<CompressedKnnGraph>, ...) (knn_softmax.cpp:117-134 +
    finish_selection :17-81) for the global batch `labels_dev` (B u32, identical on every
@@ -168,6 +180,37 @@ xknn_status_t xknn_step_micro(xknn_layer_t* h, const float* features_local_dev,
    Collective when world > 1 (uses a communicator split from the layer's). */
 xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local_dev,
                            uint64_t batch_local, void* ready_stream);
+
+/* select_active_classes(const KnnGraph&, labels, cfg, n_total) (knn_softmax.cpp:100-115 +
+   finish_selection :17-81) on one device: graph_dev is the uncompressed KnnGraph (num_classes x
+   k u32, row-major, device), candidate ranks are positions in the full lists (equal to the shard
+   overload only when P = 1, knn_softmax.hpp:40-43).  out_active_dev (capacity m_active) receives
+   ActiveSet::class_indices (sorted), *count_host its size, *contains_all_host
+   ActiveSet::contains_all_labels.  Errors as the reference: LabelOutOfRange, MTooSmall,
+   InvalidArgument (M > N), ShapeMismatch (an id >= num_classes in the graph).  Synchronizes
+   `stream`. */
+xknn_status_t xknn_select_full_graph(const uint32_t* graph_dev, uint64_t num_classes, uint32_t k,
+                                     const uint32_t* labels_dev, uint64_t batch,
+                                     uint64_t m_active, uint64_t seed, uint32_t* out_active_dev,
+                                     uint64_t* count_host, int* contains_all_host, void* stream);
+
+/* knn_softmax_forward_backward(x_norm, w_norm, labels, active, scale) (knn_softmax.cpp:136-186),
+   the single-shard free function, on device in fp32 with the reference's summation order
+   (logits bit-identical; loss and gradients within 1e-5):
+     x_norm_dev  batch x dim fp32 (already normalized), w_norm_dev num_classes x dim fp32,
+     labels_dev  batch u32, active_dev m_act u32 (ActiveSet::class_indices, sorted, unique).
+   Outputs: *loss_host (LossAndGrad::loss); grad_logits_dev (batch x m_act, may be NULL);
+   grad_features_dev (batch x dim, d loss / d x_norm, times scale); grad_w_active_dev (m_act x
+   dim: the active rows of LossAndGrad::grad_weights, which is zero elsewhere).  Errors:
+   InvalidArgument (empty active set), LabelOutOfRange (active class >= num_classes),
+   LabelNotActive (xknn_last_error_row = the batch row), ShapeMismatch.  Synchronizes. */
+xknn_status_t xknn_knn_softmax_fwd_bwd(const float* x_norm_dev, uint64_t batch,
+                                       const float* w_norm_dev, uint64_t num_classes,
+                                       uint64_t dim, const uint32_t* labels_dev,
+                                       const uint32_t* active_dev, uint64_t m_act, float scale,
+                                       double* loss_host, float* grad_logits_dev,
+                                       float* grad_features_dev, float* grad_w_active_dev,
+                                       void* stream);
 
 /* Replaces the padding draw's raw 64-bit word stream -- by default std::mt19937_64(rng_seed)
    re-seeded on every selection as the reference does (knn_softmax.cpp:43) -- with `count`

@@ -463,6 +463,46 @@ int or_softmax_xent(uint64_t m, uint64_t c, const float* logits, const uint32_t*
   return OR_OK;
 }
 
+/* knn_softmax_forward_backward, knn_softmax.cpp:136-186: gather of the active rows of w_norm
+ * (LabelOutOfRange for an id >= n), labels remapped by position_of (LabelNotActive), logits =
+ * matmul(x, w_active, T) then *= scale, softmax_xent, grad_features = matmul(G, w_active) *
+ * scale, grad_weights[active[i]] = matmul_at(G, x)[i] * scale (returned compact: m_act x d). */
+int or_knn_softmax_forward_backward(uint64_t b, uint64_t n, uint64_t d, const float* x,
+                                    const float* w, const uint32_t* labels, const uint32_t* active,
+                                    uint64_t m_act, float scale, double* loss, float* grad_logits,
+                                    float* grad_features, float* grad_w_active) {
+  if (m_act == 0) return OR_ERR_INVALID_ARGUMENT;
+  float* wa = (float*)malloc(m_act * d * sizeof(float));
+  uint32_t* rl = (uint32_t*)malloc((b ? b : 1) * sizeof(uint32_t));
+  int rc = OR_OK;
+  for (uint64_t i = 0; i < m_act && rc == OR_OK; ++i) {
+    if (active[i] >= n) rc = OR_ERR_LABEL_OUT_OF_RANGE;
+    else memcpy(wa + i * d, w + (uint64_t)active[i] * d, d * sizeof(float));
+  }
+  for (uint64_t i = 0; i < b && rc == OR_OK; ++i) {
+    uint64_t lo = 0, hi = m_act; /* ActiveSet::position_of, lower_bound */
+    while (lo < hi) { uint64_t mid = (lo + hi) / 2; if (active[mid] < labels[i]) lo = mid + 1; else hi = mid; }
+    if (lo == m_act || active[lo] != labels[i]) rc = OR_ERR_LABEL_NOT_ACTIVE;
+    else rl[i] = (uint32_t)lo;
+  }
+  if (rc == OR_OK) {
+    float* lg = (float*)malloc(b * m_act * sizeof(float));
+    or_matmul_nt(b, m_act, d, x, wa, lg);
+    for (uint64_t t = 0; t < b * m_act; ++t) lg[t] *= scale;
+    rc = or_softmax_xent(b, m_act, lg, rl, loss, grad_logits);
+    free(lg);
+  }
+  if (rc == OR_OK) {
+    or_matmul_nn(b, d, m_act, grad_logits, wa, grad_features);
+    for (uint64_t t = 0; t < b * d; ++t) grad_features[t] *= scale;
+    or_matmul_tn(b, m_act, d, grad_logits, x, grad_w_active);
+    for (uint64_t t = 0; t < m_act * d; ++t) grad_w_active[t] = grad_w_active[t] * scale;
+  }
+  free(wa);
+  free(rl);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------- */
 /* distributed_softmax_xent_cols, parallel.cpp:106-188 (rank-ordered          */
 /* scalar_reduce :66-88).  logits[s] is m × ncols[s]; cols[s] sorted ids.     */

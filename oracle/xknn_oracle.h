@@ -46,6 +46,10 @@ void or_matmul_tn(uint64_t rows, uint64_t ac, uint64_t bc, const float* a, const
                   float* c);
 int or_softmax_xent(uint64_t m, uint64_t c, const float* logits, const uint32_t* labels,
                     double* loss, float* grad);
+int or_knn_softmax_forward_backward(uint64_t b, uint64_t n, uint64_t d, const float* x,
+                                    const float* w, const uint32_t* labels, const uint32_t* active,
+                                    uint64_t m_act, float scale, double* loss, float* grad_logits,
+                                    float* grad_features, float* grad_w_active);
 int or_distributed_softmax_xent_cols(uint64_t p, uint64_t m, const float* const* logits,
                                      const uint32_t* const* cols, const uint64_t* ncols,
                                      const uint32_t* labels, double* loss, float* const* grads);

@@ -32,6 +32,7 @@ PREC_BF16 = 0
 PREC_FP32_EXACT = 1
 PREC_FP32 = 2  # 3xTF32 tensor cores, fp32 accuracy
 FLAG_NO_GRAPH = 1
+FLAG_SELECT_ONLY = 2
 
 
 class XknnConfig(C.Structure):
@@ -101,6 +102,11 @@ for _name, _args in {
     "xknn_layer_get_velocity": [VP, VP, C.c_int],
     "xknn_layer_weights_ptr": [VP, C.POINTER(VP)],
     "xknn_layer_set_graph_csr": [VP, VP, VP, VP, U64, C.c_int],
+    "xknn_layer_set_graph_csr_ranked": [VP, VP, VP, VP, VP, U64, C.c_int],
+    "xknn_select_full_graph": [VP, U64, C.c_uint32, VP, U64, U64, U64, VP, C.POINTER(U64),
+                               C.POINTER(C.c_int), VP],
+    "xknn_knn_softmax_fwd_bwd": [VP, U64, VP, U64, U64, VP, VP, U64, C.c_float,
+                                 C.POINTER(C.c_double), VP, VP, VP, VP],
     "xknn_select": [VP, VP, U64, VP, C.POINTER(U64), C.POINTER(C.c_int)],
     "xknn_step": [VP, VP, VP, U64, C.c_float, VP, VP],
     "xknn_step_micro": [VP, VP, VP, U64, C.c_float, C.c_uint32, VP, VP],
@@ -202,6 +208,48 @@ def graph_ring(w_norm_local, num_classes: int, k: int, kprime: int, rank: int, w
                                 torch.cuda.current_stream().cuda_stream, out.data_ptr(),
                                 C.byref(unc), C.byref(steps)))
     return out, unc.value, steps.value
+
+
+def select_active_classes_full(graph, labels, m_active: int, seed: int):
+    """select_active_classes(const KnnGraph&, labels, {m_active, seed}, N)
+    (knn_softmax.cpp:100-115): graph is the uncompressed (N, k) int32/uint32 CUDA tensor; ranks
+    are positions in the full lists.  Returns (sorted active classes int32 tensor,
+    contains_all_labels)."""
+    import torch
+
+    g = graph.contiguous()
+    n, k = g.shape
+    lab = labels.to(torch.int32).contiguous()
+    out = torch.empty(max(m_active, 1), dtype=torch.int32, device=g.device)
+    cnt, ca = U64(), C.c_int()
+    _check(_lib.xknn_select_full_graph(g.data_ptr(), n, k, lab.data_ptr(), lab.numel(), m_active,
+                                       seed, out.data_ptr(), C.byref(cnt), C.byref(ca),
+                                       torch.cuda.current_stream().cuda_stream))
+    return out[: cnt.value], bool(ca.value)
+
+
+def knn_softmax_forward_backward(x_norm, w_norm, labels, active, scale: float):
+    """knn_softmax_forward_backward(x_norm, w_norm, labels, active, scale)
+    (knn_softmax.cpp:136-186) on device (fp32, the reference's summation order).  Returns
+    (loss, grad_logits (B, M), grad_features (B, D), grad_w_active (M, D) -- the active rows of
+    the reference's dense grad_weights, zero elsewhere)."""
+    import torch
+
+    x = x_norm.contiguous()
+    w = w_norm.contiguous()
+    lab = labels.to(torch.int32).contiguous()
+    act = active.to(torch.int32).contiguous()
+    b, d = x.shape
+    m = act.numel()
+    gl = torch.empty(b, max(m, 1), device=x.device)
+    gf = torch.empty(b, d, device=x.device)
+    gw = torch.empty(max(m, 1), d, device=x.device)
+    loss = C.c_double()
+    _check(_lib.xknn_knn_softmax_fwd_bwd(x.data_ptr(), b, w.data_ptr(), w.shape[0], d,
+                                         lab.data_ptr(), act.data_ptr(), m, float(scale),
+                                         C.byref(loss), gl.data_ptr(), gf.data_ptr(),
+                                         gw.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return loss.value, gl[:, :m], gf, gw[:m]
 
 
 def release_graph_cache() -> None:
@@ -325,13 +373,14 @@ class KnnSoftmaxLayer:
     def __init__(self, num_classes: int, dim: int, *, rank: int = 0, world: int = 1,
                  m_active: int, max_batch: int, scale: float = 30.0, momentum: float = 0.9,
                  weight_decay: float = 0.0, rng_seed: int = 0, precision: int = PREC_BF16,
-                 comm=None, stream=None, use_graph: bool = True):
+                 comm=None, stream=None, use_graph: bool = True, select_only: bool = False):
         import torch  # plumbing only: device memory and streams
 
         self._torch = torch
         self.num_classes, self.dim, self.rank, self.world = num_classes, dim, rank, world
         self.cfg = XknnConfig(scale, momentum, weight_decay, m_active, rng_seed, max_batch,
-                              precision, (0 if use_graph else FLAG_NO_GRAPH))
+                              precision, (0 if use_graph else FLAG_NO_GRAPH) |
+                              (FLAG_SELECT_ONLY if select_only else 0))
         # the layer works on its own stream (capturable into a CUDA graph); every call is
         # ordered after the caller's current stream and the caller's stream after it
         self.stream = stream if stream is not None else torch.cuda.Stream()
@@ -397,6 +446,17 @@ class KnnSoftmaxLayer:
         self._enter()
         _check(_lib.xknn_layer_set_graph_csr(self.h, kpc.data_ptr(), off.data_ptr(),
                                              fl.data_ptr() if fl.numel() else 0, fl.numel(), dev))
+
+    def set_shard_graph_ranked(self, k_per_class, offsets, flat, rank) -> None:
+        """set_shard_graph with a per-entry rank (several shards' slices of a label merged into
+        one list, each entry ranked within its own slice): xknn_layer_set_graph_csr_ranked."""
+        dev = int(k_per_class.is_cuda)
+        kpc, off, fl, rk = (t.contiguous() for t in (k_per_class, offsets, flat, rank))
+        self._enter()
+        _check(_lib.xknn_layer_set_graph_csr_ranked(self.h, kpc.data_ptr(), off.data_ptr(),
+                                                    fl.data_ptr() if fl.numel() else 0,
+                                                    rk.data_ptr() if rk.numel() else 0,
+                                                    fl.numel(), dev))
 
     def set_graph_rows(self, rows, k: int) -> None:
         """compress_graph + set_shard_graphs from this rank's rows [begin, end) x k of the full

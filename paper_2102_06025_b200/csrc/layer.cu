@@ -62,9 +62,12 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   bmax = cfg.max_batch;
   mw_cap = std::min<uint64_t>(nw, cfg.m_active);
 
-  XK_CUDA(dalloc(&W, nw * d));
-  XK_CUDA(dalloc(&V, nw * d));
-  XK_CUDA(cudaMemsetAsync(V, 0, nw * d * sizeof(float), stream));
+  select_only = (cfg.flags & XKNN_FLAG_SELECT_ONLY) != 0;
+  if (!select_only) {
+    XK_CUDA(dalloc(&W, nw * d));
+    XK_CUDA(dalloc(&V, nw * d));
+    XK_CUDA(cudaMemsetAsync(V, 0, nw * d * sizeof(float), stream));
+  }
   XK_CUDA(dalloc(&sel_best, nw));
   XK_CUDA(dalloc(&sel_occ, nw));
   XK_CUDA(cudaMemsetAsync(sel_best, 0xff, nw * sizeof(uint32_t), stream));
@@ -115,6 +118,10 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   XK_CUDA(cudaMalloc(&cub_tmp, cub_tmp_bytes));
 
   // step scratch
+  if (select_only) {
+    XK_CUDA(cudaStreamSynchronize(stream));
+    return XKNN_OK;
+  }
   XK_CUDA(dalloc(&X, bmax * d));
   XK_CUDA(dalloc(&xnorm, bmax));
   XK_CUDA(dalloc(&wnorm, mw_cap));
@@ -137,7 +144,7 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
 }
 
 void Layer::free_all() {
-  void* ptrs[] = {W, V, g_kpc, g_off, g_flat, sel_best, sel_occ, pool_bits, pos_of,
+  void* ptrs[] = {W, V, g_kpc, g_off, g_flat, g_rank, sel_best, sel_occ, pool_bits, pos_of,
                   pool_list, pool_samp, blk_counts, mt_cache, pick_key, pick_val, pick_head,
                   pred, lw, labels_all, pool_counts, tie_counts, hist, cub_tmp, err, X, Xhat, Xhat16,
                   Xs16, xnorm, Wsub, Wsub16, wnorm, logits, Pt, rowstat, rowred, rowmax, dW, dX,
@@ -748,6 +755,7 @@ xknn_status_t xknn_layer_set_draw_stream(xknn_layer_t* h, const uint64_t* words,
 xknn_status_t xknn_layer_set_weights(xknn_layer_t* h, const float* w, int on_device) {
   GUARD_H(h);
   Layer& L = h->L;
+  if (L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer has no parameters");
   cudaError_t e = cudaMemcpyAsync(L.W, w, L.nw * L.d * sizeof(float), kind_in(on_device), L.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
   L.has_weights = true;
@@ -757,6 +765,7 @@ xknn_status_t xknn_layer_set_weights(xknn_layer_t* h, const float* w, int on_dev
 xknn_status_t xknn_layer_get_weights(xknn_layer_t* h, float* w, int on_device) {
   GUARD_H(h);
   Layer& L = h->L;
+  if (L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer has no parameters");
   cudaError_t e = cudaMemcpyAsync(w, L.W, L.nw * L.d * sizeof(float), kind_out(on_device), L.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
   return L.cuda_ok(e);
@@ -765,6 +774,7 @@ xknn_status_t xknn_layer_get_weights(xknn_layer_t* h, float* w, int on_device) {
 xknn_status_t xknn_layer_get_velocity(xknn_layer_t* h, float* v, int on_device) {
   GUARD_H(h);
   Layer& L = h->L;
+  if (L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer has no parameters");
   cudaError_t e = cudaMemcpyAsync(v, L.V, L.nw * L.d * sizeof(float), kind_out(on_device), L.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L.stream);
   return L.cuda_ok(e);
@@ -772,6 +782,7 @@ xknn_status_t xknn_layer_get_velocity(xknn_layer_t* h, float* v, int on_device) 
 
 xknn_status_t xknn_layer_weights_ptr(xknn_layer_t* h, float** w_dev) {
   GUARD_H(h);
+  if (h->L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer has no parameters");
   *w_dev = h->L.W;
   h->L.has_weights = true;
   return XKNN_OK;
@@ -796,16 +807,20 @@ __global__ void k_graph_check(const uint32_t* kpc, const uint64_t* off, const ui
 }
 }  // namespace
 
-xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, const uint64_t* off,
-                                       const uint32_t* flat, uint64_t flat_len, int on_device) {
+xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* kpc,
+                                              const uint64_t* off, const uint32_t* flat,
+                                              const uint32_t* rank, uint64_t flat_len,
+                                              int on_device) {
   GUARD_H(h);
   Layer& L = h->L;
   if (L.g_kpc) cudaFree(L.g_kpc);
   if (L.g_off) cudaFree(L.g_off);
   if (L.g_flat) cudaFree(L.g_flat);
+  if (L.g_rank) cudaFree(L.g_rank);
   L.g_kpc = nullptr;
   L.g_off = nullptr;
   L.g_flat = nullptr;
+  L.g_rank = nullptr;
   L.has_graph = false;
   L.drop_graphs();  // graph buffers are baked into the graphs
   // a selection prepared from the old graph is never used after the graph changes (the
@@ -818,6 +833,11 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   XK_CUDA_H(cudaMemcpyAsync(L.g_off, off, L.n * 8, kind_in(on_device), L.stream));
   if (flat_len)
     XK_CUDA_H(cudaMemcpyAsync(L.g_flat, flat, flat_len * 4, kind_in(on_device), L.stream));
+  if (rank) {
+    XK_CUDA_H(xknn::dalloc(&L.g_rank, flat_len));
+    if (flat_len)
+      XK_CUDA_H(cudaMemcpyAsync(L.g_rank, rank, flat_len * 4, kind_in(on_device), L.stream));
+  }
   L.g_flat_len = flat_len;
   unsigned int* dk;
   unsigned long long* db;
@@ -856,6 +876,11 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, con
   return XKNN_OK;
 }
 
+xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, const uint64_t* off,
+                                       const uint32_t* flat, uint64_t flat_len, int on_device) {
+  return xknn_layer_set_graph_csr_ranked(h, kpc, off, flat, nullptr, flat_len, on_device);
+}
+
 xknn_status_t xknn_select(xknn_layer_t* h, const uint32_t* labels_dev, uint64_t batch,
                           uint32_t* out_active_dev, uint64_t* count_host, int* contains_all) {
   GUARD_H(h);
@@ -887,6 +912,7 @@ xknn_status_t xknn_prepare(xknn_layer_t* h, const uint32_t* labels_local, uint64
                            void* ready_stream) {
   GUARD_H(h);
   Layer& L = h->L;
+  if (L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer: no train step");
   if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "prepare: knn mode without shard graphs");
   if (bl == 0 || bl * L.world > L.bmax)
     return fail(XKNN_ERR_INVALID_ARGUMENT, "prepare: batch size must be a positive multiple of P (<= max_batch)");
@@ -898,6 +924,7 @@ xknn_status_t xknn_step_micro(xknn_layer_t* h, const float* feats, const uint32_
                               float* gfeat) {
   GUARD_H(h);
   Layer& L = h->L;
+  if (L.select_only) return fail(XKNN_ERR_UNSUPPORTED, "select-only layer: no train step");
   if (!L.has_graph) return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: knn mode without shard graphs");
   if (bl == 0 || bl * L.world > L.bmax)
     return fail(XKNN_ERR_INVALID_ARGUMENT, "train_step: batch size must be a positive multiple of P (<= max_batch)");

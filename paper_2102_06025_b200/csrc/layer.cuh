@@ -90,6 +90,8 @@ struct Layer {
   uint32_t* g_kpc = nullptr;
   uint64_t* g_off = nullptr;
   uint32_t* g_flat = nullptr;
+  uint32_t* g_rank = nullptr;         // optional per-entry rank (merged multi-shard slices)
+  bool select_only = false;           // XKNN_FLAG_SELECT_ONLY: no parameters, no step scratch
   uint64_t g_flat_len = 0;
   uint32_t g_kmax = 0;
   bool has_graph = false, has_weights = false;

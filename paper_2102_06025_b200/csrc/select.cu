@@ -31,12 +31,16 @@ namespace {
 constexpr int kCompactBlock = 256;
 
 // ---- pool marking: one warp per batch label, lanes stride the label's slice; lane 0 also
-// marks the label (distinct labels of this shard counted as newly set bits)
+// marks the label (distinct labels of this shard counted as newly set bits).  A label's list is
+// its slice of this shard's CompressedKnnGraph; with per-entry ranks it may be the concatenation
+// of several shards' slices (the span<CompressedKnnGraph> overload on one device), each entry
+// ranked within its own slice (knn_softmax.cpp:125-130).
 __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch, uint64_t n,
                             uint64_t begin, uint64_t nw, const uint32_t* __restrict__ kpc,
                             const uint64_t* __restrict__ off, const uint32_t* __restrict__ flat,
-                            uint32_t* pool_bits, uint32_t* lab_bits, uint32_t* best, uint32_t* occ,
-                            SelState* st, unsigned long long* err, int track) {
+                            const uint32_t* __restrict__ rankv, uint32_t* pool_bits,
+                            uint32_t* lab_bits, uint32_t* best, uint32_t* occ, SelState* st,
+                            unsigned long long* err, int track) {
   griddep_wait();
   griddep_launch();
   const uint32_t lane = threadIdx.x & 31;
@@ -61,7 +65,9 @@ __global__ void k_mark_pool(const uint32_t* __restrict__ labels, uint32_t batch,
       if (lc >= nw) continue;  // validated at set_graph time
       atomicOr(&pool_bits[lc >> 5], 1u << (lc & 31));
       if (track) {  // candidate rank / occurrences: only the over-full branch ranks by them
-        atomicMin(&best[lc], r);
+        // rank = position within the slice, or the caller's per-entry rank (several shards'
+        // slices merged into one list: xknn_layer_set_graph_csr_ranked)
+        atomicMin(&best[lc], rankv ? rankv[o + r] : r);
         atomicAdd(&occ[lc], 1u);
       }
     }
@@ -520,7 +526,7 @@ xknn_status_t Layer::run_selection(uint64_t batch) {
   // when the pool can exceed M; the default M = 10% N never lets it
   const bool overfull_possible = (uint64_t)B * g_kmax > m;
   launch_pdl(k_mark_pool, grid_for((uint64_t)B * 32, 256), 256, 0, stream, 
-      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, pool_bits, lab_bits, sel_best, sel_occ,
+      labels_all, B, n, begin, nw, g_kpc, g_off, g_flat, (const uint32_t*)g_rank, pool_bits, lab_bits, sel_best, sel_occ,
       st, err, overfull_possible ? 1 : 0);
   XK_LAUNCH();
   // (2) sorted local pool; [pool size, distinct labels] exchanged between shards

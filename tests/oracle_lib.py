@@ -255,6 +255,34 @@ def graph_row(w_norm: np.ndarray, j: int, k: int) -> np.ndarray:
     return out
 
 
+def knn_softmax_fwd_bwd(lib_kind: str, x_norm, w_norm, labels, active, scale=30.0):
+    """knn_softmax_forward_backward (knn_softmax.cpp:136-186) via the oracle ('oracle'; grad
+    weights compact, m_act x d) or the compiled reference ('ref'; dense n x d, the active rows
+    gathered here).  Returns (rc, loss, grad_logits, grad_features, grad_w_active)."""
+    x = np.ascontiguousarray(x_norm, np.float32)
+    w = np.ascontiguousarray(w_norm, np.float32)
+    lab = np.ascontiguousarray(labels, np.uint32)
+    act = np.ascontiguousarray(active, np.uint32)
+    b, d = x.shape
+    n, m = w.shape[0], act.size
+    loss = C.c_double(0)
+    gl = np.zeros((b, max(m, 1)), np.float32)
+    gf = np.zeros((b, d), np.float32)
+    if lib_kind == "oracle":
+        gw = np.zeros((max(m, 1), d), np.float32)
+        fn = oracle().or_knn_softmax_forward_backward
+    else:
+        gw = np.zeros((n, d), np.float32)
+        fn = ref().ref_knn_softmax_forward_backward
+    fn.restype = C.c_int
+    fn.argtypes = [U64, U64, U64, f32p, f32p, u32p, u32p, U64, C.c_float, C.POINTER(C.c_double),
+                   f32p, f32p, f32p]
+    rc = fn(b, n, d, x, w, lab, act, m, scale, C.byref(loss), gl, gf, gw)
+    if lib_kind != "oracle" and rc == 0:
+        gw = gw[act.astype(np.int64)]
+    return rc, loss.value, gl[:, :m], gf, gw[:m]
+
+
 class GraphRowChecker:
     """Exact build_graph_bruteforce rows of a few query classes over a class matrix streamed in
     chunks (or_graph_rows_update): feed every chunk once, in any order; rows() then equals

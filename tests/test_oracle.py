@@ -282,3 +282,24 @@ def test_graph_row_checker_streamed():
     got = chk.rows()
     for a, j in enumerate(qid):
         assert np.array_equal(got[a], O.graph_row(wn, int(j), k))
+
+
+@pytest.mark.ref
+def test_oracle_knn_softmax_fwd_bwd_vs_reference():
+    """or_knn_softmax_forward_backward is bit-identical with the compiled reference's
+    knn_softmax_forward_backward (knn_softmax.cpp:136-186), including its errors."""
+    rng = np.random.default_rng(6)
+    n, d, b, m = 700, 128, 33, 90
+    _, x, _, _ = O.l2_normalize(rng.standard_normal((b, d)).astype(np.float32))
+    _, w, _, _ = O.l2_normalize(rng.standard_normal((n, d)).astype(np.float32))
+    act = np.sort(rng.choice(n, m, replace=False)).astype(np.uint32)
+    lab = act[rng.integers(0, m, b)]
+    a = O.knn_softmax_fwd_bwd("oracle", x, w, lab, act)
+    r = O.knn_softmax_fwd_bwd("ref", x, w, lab, act)
+    assert a[0] == r[0] == 0 and a[1] == r[1]
+    for i in (2, 3, 4):
+        assert np.array_equal(a[i], r[i])
+    bad = lab.copy()
+    bad[5] = np.setdiff1d(np.arange(n), act)[0]
+    assert O.knn_softmax_fwd_bwd("oracle", x, w, bad, act)[0] == 7  # LabelNotActive
+    assert O.knn_softmax_fwd_bwd("ref", x, w, bad, act)[0] == 7
