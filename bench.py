@@ -13,7 +13,8 @@ Workloads (BASELINE.json configs, D = 512, M = 10% N, s = 30, lr = 0.1, mu = 0.9
     c1  N=100K  B=256   k=10    (the reference's CPU-runnable case; parity config)
     c2  N=1M    B=1024  k=50    single B200 -- the default at N=1 (configs[1])
     c3  N=10M   B=4096  k=100   class-sharded over 2/4/8 GPUs -- the default at N>1 (strong)
-    c4  N=100M  B=8192  k=100   8 GPUs (paper headline scale)
+    c4  N=100M  B=8192  k=100   8 GPUs (paper headline scale); 25M classes/GPU on 4 GPUs
+    c4r N=12.5M B=8192  k=100   one GPU: the per-rank work of C4 on 8 GPUs
 Synthetic data: W ~ N(0, 0.05^2), features ~ N(0,1), labels uniform, a seeded self-first random
 graph of k neighbours per class (random-init W makes the true KNN graph statistically random).
 The per-step working set (weight shard, P~ of B x M_w bf16) exceeds the 126 MB L2.
@@ -37,6 +38,10 @@ WORKLOADS = {
     "c2": dict(n=1_000_000, b=1024, k=50),
     "c3": dict(n=10_000_000, b=4096, k=100),
     "c4": dict(n=100_000_000, b=8192, k=100),
+    # one rank of C4 on 8 GPUs, run on one GPU: its 12.5M-class shard, the global batch 8192,
+    # k = 100, M_w = 1.25M active rows -- the GEMM/update work of a C4 rank (its selection differs:
+    # the pool is drawn from 12.5M classes instead of 100M)
+    "c4r": dict(n=12_500_000, b=8192, k=100),
 }
 D = 512
 SCALE, LR, MOMENTUM, SEED = 30.0, 0.1, 0.9, 42
@@ -158,28 +163,40 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------------
 # synthetic inputs
 # ----------------------------------------------------------------------------------------------
-def build_shard_graph(torch, n, k, p, rank, seed=7, chunk=1 << 20):
+def install_shard_graph(torch, layer, n, k, p, rank, seed=7, chunk=1 << 20):
     """This shard's CompressedKnnGraph (compress_graph, knn_graph.cpp:235-266) of a seeded
-    self-first random graph, generated chunk-wise on device identically on every rank."""
+    self-first random k-graph, generated chunk-wise on device identically on every rank and
+    written straight into the layer's own graph arrays (xknn_layer_graph_buffers): a counting
+    pass sizes the shard's entries, a second pass regenerates the chunks and fills them -- no
+    staging copy (C4: ~10 GB of entries per GPU next to a 100 GB weight+velocity shard)."""
     import paper_2102_06025_b200 as X
 
     lo, hi = X.ShardLayout(n, p).class_range(rank)
-    kpc = torch.empty(n, dtype=torch.int32, device="cuda")
-    flats = []
     g = torch.Generator(device="cuda")
-    for c0 in range(0, n, chunk):
-        c1 = min(n, c0 + chunk)
-        g.manual_seed(seed * 1_000_003 + c0)
-        nb = torch.randint(0, n, (c1 - c0, k), device="cuda", dtype=torch.int32, generator=g)
-        nb[:, 0] = torch.arange(c0, c1, device="cuda", dtype=torch.int32)
-        mask = (nb >= lo) & (nb < hi)
+
+    def chunks():
+        for c0 in range(0, n, chunk):
+            c1 = min(n, c0 + chunk)
+            g.manual_seed(seed * 1_000_003 + c0)
+            nb = torch.randint(0, n, (c1 - c0, k), device="cuda", dtype=torch.int32, generator=g)
+            nb[:, 0] = torch.arange(c0, c1, device="cuda", dtype=torch.int32)
+            yield c0, c1, nb, (nb >= lo) & (nb < hi)
+
+    kpc = torch.empty(n, dtype=torch.int32, device="cuda")
+    for c0, c1, nb, mask in chunks():
         kpc[c0:c1] = mask.sum(1, dtype=torch.int32)
-        flats.append(nb[mask])
-        del nb, mask
-    flat = torch.cat(flats)
-    del flats
-    off = torch.cumsum(kpc.to(torch.int64), 0) - kpc.to(torch.int64)
-    return kpc, off, flat
+    flat_len = int(kpc.sum(dtype=torch.int64).item())
+    kb, ob, fb = layer.graph_buffers(flat_len)
+    kb.copy_(kpc)
+    del kpc
+    ob.copy_(torch.cumsum(kb, 0, dtype=torch.int64))
+    ob.sub_(kb.to(torch.int64))
+    for c0, c1, nb, mask in chunks():
+        vals = nb[mask]
+        start = int(ob[c0].item())
+        fb[start:start + vals.numel()] = vals
+    torch.cuda.synchronize()
+    layer.commit_graph()
 
 
 def make_batches(torch, n, b_local, rank, count=4):
@@ -312,9 +329,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
         wv = layer.weights_view().tensor
         for r0 in range(0, wv.shape[0], 1 << 20):
             wv[r0:r0 + (1 << 20)].normal_(0.0, 0.05, generator=gw)
-        kpc, off, flat = build_shard_graph(torch, n, k, world, rank)
-        layer.set_shard_graph(kpc, off, flat)
-        del kpc, off, flat
+        install_shard_graph(torch, layer, n, k, world, rank)
         batches = make_batches(torch, n, b_local, rank)
         gfeat = torch.empty(b_local, D, device="cuda")
         loss = torch.zeros(1, dtype=torch.float64, device="cuda")

@@ -123,6 +123,15 @@ xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* k_per_cl
                                        const uint64_t* offsets, const uint32_t* flat,
                                        uint64_t flat_len, int on_device);
 
+/* In-place graph install for shards too large to stage twice (C4: ~10 GB of entries per GPU):
+   xknn_layer_graph_buffers drops the installed graph and returns the layer-owned device arrays
+   k_per_class[num_classes], offsets[num_classes], flat[flat_len] for the caller to fill (on any
+   stream; synchronize before committing); xknn_layer_graph_commit validates them as
+   xknn_layer_set_graph_csr does and installs them (collective when world > 1). */
+xknn_status_t xknn_layer_graph_buffers(xknn_layer_t* h, uint64_t flat_len, uint32_t** k_per_class_dev,
+                                       uint64_t** offsets_dev, uint32_t** flat_dev);
+xknn_status_t xknn_layer_graph_commit(xknn_layer_t* h);
+
 /* xknn_layer_set_graph_csr with a per-entry rank (rank[flat_len], NULL = the position within
    the class's list): lets one layer hold several shards' slices of a label concatenated into one
    list, each entry ranked within its own slice -- select_active_classes(span<CompressedKnnGraph>)

@@ -103,6 +103,8 @@ for _name, _args in {
     "xknn_layer_weights_ptr": [VP, C.POINTER(VP)],
     "xknn_layer_set_graph_csr": [VP, VP, VP, VP, U64, C.c_int],
     "xknn_layer_set_graph_csr_ranked": [VP, VP, VP, VP, VP, U64, C.c_int],
+    "xknn_layer_graph_buffers": [VP, U64, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)],
+    "xknn_layer_graph_commit": [VP],
     "xknn_select_full_graph": [VP, U64, C.c_uint32, VP, U64, U64, U64, VP, C.POINTER(U64),
                                C.POINTER(C.c_int), VP],
     "xknn_knn_softmax_fwd_bwd": [VP, U64, VP, U64, U64, VP, VP, U64, C.c_float,
@@ -446,6 +448,30 @@ class KnnSoftmaxLayer:
         self._enter()
         _check(_lib.xknn_layer_set_graph_csr(self.h, kpc.data_ptr(), off.data_ptr(),
                                              fl.data_ptr() if fl.numel() else 0, fl.numel(), dev))
+
+    def graph_buffers(self, flat_len: int):
+        """In-place graph install: the layer-owned (k_per_class int32[N], offsets int64[N],
+        flat int32[flat_len]) device arrays as torch tensors; fill them, synchronize, then
+        commit_graph()."""
+        torch = self._torch
+        k, o, f = VP(), VP(), VP()
+        self._enter()
+        _check(_lib.xknn_layer_graph_buffers(self.h, flat_len, C.byref(k), C.byref(o), C.byref(f)))
+
+        def view(ptr, n, typestr, dtype):
+            class _V:
+                __cuda_array_interface__ = {"data": (ptr, False), "shape": (n,),
+                                            "typestr": typestr, "version": 2}
+            return torch.as_tensor(_V(), device="cuda").view(dtype)
+
+        return (view(k.value, self.num_classes, "<i4", torch.int32),
+                view(o.value, self.num_classes, "<i8", torch.int64),
+                view(f.value, max(flat_len, 1), "<i4", torch.int32)[:flat_len])
+
+    def commit_graph(self) -> None:
+        """Validate and install the arrays filled through graph_buffers (collective)."""
+        self._enter()
+        _check(_lib.xknn_layer_graph_commit(self.h))
 
     def set_shard_graph_ranked(self, k_per_class, offsets, flat, rank) -> None:
         """set_shard_graph with a per-entry rank (several shards' slices of a label merged into

@@ -807,10 +807,8 @@ __global__ void k_graph_check(const uint32_t* kpc, const uint64_t* off, const ui
 }
 }  // namespace
 
-xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* kpc,
-                                              const uint64_t* off, const uint32_t* flat,
-                                              const uint32_t* rank, uint64_t flat_len,
-                                              int on_device) {
+xknn_status_t xknn_layer_graph_buffers(xknn_layer_t* h, uint64_t flat_len, uint32_t** kpc_dev,
+                                       uint64_t** off_dev, uint32_t** flat_dev) {
   GUARD_H(h);
   Layer& L = h->L;
   if (L.g_kpc) cudaFree(L.g_kpc);
@@ -821,24 +819,28 @@ xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* k
   L.g_off = nullptr;
   L.g_flat = nullptr;
   L.g_rank = nullptr;
+  L.g_flat_len = 0;
   L.has_graph = false;
   L.drop_graphs();  // graph buffers are baked into the graphs
   // a selection prepared from the old graph is never used after the graph changes (the
   // reference selects from the current graph at step time)
   XK_TRY_H(L.cancel_prepared());
+  XK_CUDA_H(cudaStreamSynchronize(L.stream));
   XK_CUDA_H(xknn::dalloc(&L.g_kpc, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_off, L.n));
   XK_CUDA_H(xknn::dalloc(&L.g_flat, flat_len));
-  XK_CUDA_H(cudaMemcpyAsync(L.g_kpc, kpc, L.n * 4, kind_in(on_device), L.stream));
-  XK_CUDA_H(cudaMemcpyAsync(L.g_off, off, L.n * 8, kind_in(on_device), L.stream));
-  if (flat_len)
-    XK_CUDA_H(cudaMemcpyAsync(L.g_flat, flat, flat_len * 4, kind_in(on_device), L.stream));
-  if (rank) {
-    XK_CUDA_H(xknn::dalloc(&L.g_rank, flat_len));
-    if (flat_len)
-      XK_CUDA_H(cudaMemcpyAsync(L.g_rank, rank, flat_len * 4, kind_in(on_device), L.stream));
-  }
   L.g_flat_len = flat_len;
+  if (kpc_dev) *kpc_dev = L.g_kpc;
+  if (off_dev) *off_dev = L.g_off;
+  if (flat_dev) *flat_dev = L.g_flat;
+  return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_graph_commit(xknn_layer_t* h) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  if (!L.g_kpc) return fail(XKNN_ERR_INVALID_ARGUMENT, "graph_commit: no graph buffers");
+  const uint64_t flat_len = L.g_flat_len;
   unsigned int* dk;
   unsigned long long* db;
   XK_CUDA_H(cudaMalloc(&dk, 16));
@@ -874,6 +876,25 @@ xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* k
   }
   L.has_graph = true;
   return XKNN_OK;
+}
+
+xknn_status_t xknn_layer_set_graph_csr_ranked(xknn_layer_t* h, const uint32_t* kpc,
+                                              const uint64_t* off, const uint32_t* flat,
+                                              const uint32_t* rank, uint64_t flat_len,
+                                              int on_device) {
+  GUARD_H(h);
+  Layer& L = h->L;
+  XK_TRY_H(xknn_layer_graph_buffers(h, flat_len, nullptr, nullptr, nullptr));
+  XK_CUDA_H(cudaMemcpyAsync(L.g_kpc, kpc, L.n * 4, kind_in(on_device), L.stream));
+  XK_CUDA_H(cudaMemcpyAsync(L.g_off, off, L.n * 8, kind_in(on_device), L.stream));
+  if (flat_len)
+    XK_CUDA_H(cudaMemcpyAsync(L.g_flat, flat, flat_len * 4, kind_in(on_device), L.stream));
+  if (rank) {
+    XK_CUDA_H(xknn::dalloc(&L.g_rank, flat_len));
+    if (flat_len)
+      XK_CUDA_H(cudaMemcpyAsync(L.g_rank, rank, flat_len * 4, kind_in(on_device), L.stream));
+  }
+  return xknn_layer_graph_commit(h);
 }
 
 xknn_status_t xknn_layer_set_graph_csr(xknn_layer_t* h, const uint32_t* kpc, const uint64_t* off,

@@ -47,7 +47,7 @@ def rel_err(a, b):
 
 def device_graph(n, k, seed, chunk=1 << 20):
     """A seeded self-first random k-graph generated on the device (N x k int32, row-major, as
-    bench.py's build_shard_graph at P = 1): (flat, k_per_class, offsets) CUDA tensors of the
+    bench.py's install_shard_graph at P = 1): (flat, k_per_class, offsets) CUDA tensors of the
     one-shard CompressedKnnGraph.  Used where the host cannot hold the graph (C3/C4 geometry)."""
     torch = torch_cuda()
     flat = torch.empty(n * k, dtype=torch.int32, device="cuda")

@@ -101,3 +101,27 @@ def test_knn_softmax_forward_backward(n, b, m, d):
     if m < n:
         with pytest.raises(X.LabelNotActive):
             X.knn_softmax_forward_backward(t(x), t(w), t(bad.view(np.int32)), t(act.view(np.int32)), 30.0)
+
+
+def test_in_place_graph_install_matches_copy():
+    """xknn_layer_graph_buffers + xknn_layer_graph_commit (bench.py's in-place install) installs
+    the same CompressedKnnGraph as xknn_layer_set_graph_csr, and selection agrees."""
+    import paper_2102_06025_b200 as X
+    import bench
+
+    torch = torch_cuda()
+    n, k, b, m = 50_000, 8, 128, 5_000
+    a = X.KnnSoftmaxLayer(n, 128, m_active=m, max_batch=b, rng_seed=3,
+                          precision=X.PREC_FP32_EXACT, select_only=True)
+    bench.install_shard_graph(torch, a, n, k, 1, 0, seed=5, chunk=7_000)
+    kpc, off, flat = a.graph()
+    g = np.zeros((n, k), np.uint32)
+    for c in range(n):
+        g[c] = flat[int(off[c]):int(off[c]) + int(kpc[c])]
+    assert (kpc == k).all() and (g[:, 0] == np.arange(n)).all()
+    shards = [O.compress(g, 1, 0)]
+    lab = np.random.default_rng(1).integers(0, n, b).astype(np.uint32)
+    got, _ = a.select_active_classes(torch.from_numpy(lab.view(np.int32)).cuda())
+    rc, want, _ = O.select_shards("oracle", n, shards, lab, m, 3)
+    assert rc == 0 and np.array_equal(got.cpu().numpy().view(np.uint32), want)
+    a.close()
