@@ -321,9 +321,12 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
         args.precision]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
+        # per-shard active capacity: uniform labels put ~M/P active classes on each shard; the
+        # worst-case default min(shard, M) would size P~ at B x M (164 GB per GPU at C4 on 4)
+        cap = 0 if world == 1 else int(math.ceil(m / world * 1.05)) + 4096
         layer = X.KnnSoftmaxLayer(n, D, rank=rank, world=world, m_active=m, max_batch=b,
                                   scale=SCALE, momentum=MOMENTUM, rng_seed=SEED, precision=prec,
-                                  comm=comm, stream=stream)
+                                  comm=comm, stream=stream, active_capacity=cap)
         gw = torch.Generator(device="cuda")
         gw.manual_seed(10 + rank)
         wv = layer.weights_view().tensor

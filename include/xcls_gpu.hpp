@@ -157,6 +157,7 @@ struct FcOptions {  // SimOptions (parallel.hpp:130-146) fields of the fc layer
   SelectionConfig selection;
   std::size_t max_batch = 0;          // largest global batch
   int precision = XKNN_PREC_BF16;     // xknn_precision_t
+  std::size_t active_capacity = 0;    // xknn_config_t::active_capacity (0 = worst case)
 };
 struct FcStepResult {
   double loss = 0.0;

@@ -70,6 +70,12 @@ typedef struct {
   uint64_t max_batch;    /* largest global batch B a step will see (sizes scratch)           */
   int32_t precision;     /* xknn_precision_t                                                 */
   int32_t flags;         /* XKNN_FLAG_*                                                      */
+  /* per-shard capacity of the active set (sizes W_sub, P~ and dW: P~ alone is max_batch x
+     capacity); 0 = min(shard size, m_active), the worst case.  With uniform labels a shard
+     holds ~m_active / world active classes; a step whose selection puts more on this shard
+     fails with XKNN_ERR_OUT_OF_MEMORY before any parameter is touched.  C4 on 4 GPUs needs it
+     (worst case: 8192 x 10M x 2 B = 164 GB of P~ per GPU). */
+  uint64_t active_capacity;
 } xknn_config_t;
 
 /* The step's device work (selection .. update) is captured once per batch size into a CUDA

@@ -39,7 +39,7 @@ class XknnConfig(C.Structure):
     """xknn_config_t (include/xknn.h) == SimOptions + SelectionConfig of the reference."""
     _fields_ = [("scale", C.c_float), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("m_active", U64), ("rng_seed", U64), ("max_batch", U64),
-                ("precision", C.c_int32), ("flags", C.c_int32)]
+                ("precision", C.c_int32), ("flags", C.c_int32), ("active_capacity", U64)]
 
 
 # ---- errors.hpp:10-54 -------------------------------------------------------------------------
@@ -375,14 +375,15 @@ class KnnSoftmaxLayer:
     def __init__(self, num_classes: int, dim: int, *, rank: int = 0, world: int = 1,
                  m_active: int, max_batch: int, scale: float = 30.0, momentum: float = 0.9,
                  weight_decay: float = 0.0, rng_seed: int = 0, precision: int = PREC_BF16,
-                 comm=None, stream=None, use_graph: bool = True, select_only: bool = False):
+                 comm=None, stream=None, use_graph: bool = True, select_only: bool = False,
+                 active_capacity: int = 0):
         import torch  # plumbing only: device memory and streams
 
         self._torch = torch
         self.num_classes, self.dim, self.rank, self.world = num_classes, dim, rank, world
         self.cfg = XknnConfig(scale, momentum, weight_decay, m_active, rng_seed, max_batch,
                               precision, (0 if use_graph else FLAG_NO_GRAPH) |
-                              (FLAG_SELECT_ONLY if select_only else 0))
+                              (FLAG_SELECT_ONLY if select_only else 0), active_capacity)
         # the layer works on its own stream (capturable into a CUDA graph); every call is
         # ordered after the caller's current stream and the caller's stream after it
         self.stream = stream if stream is not None else torch.cuda.Stream()

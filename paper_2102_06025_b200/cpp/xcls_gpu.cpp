@@ -296,6 +296,7 @@ HybridSimFc::HybridSimFc(std::size_t num_classes, std::size_t dim, const FcOptio
   c.rng_seed = opt.selection.rng_seed;
   c.max_batch = opt.max_batch;
   c.precision = opt.precision;
+  c.active_capacity = opt.active_capacity;
   cudaStream_t s = nullptr;
   cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
   stream_ = s;

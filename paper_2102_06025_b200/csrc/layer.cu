@@ -61,6 +61,7 @@ xknn_status_t Layer::init(int rank_, int world_, uint64_t n_, uint64_t d_,
   nwords = (nw + 31) / 32;
   bmax = cfg.max_batch;
   mw_cap = std::min<uint64_t>(nw, cfg.m_active);
+  if (cfg.active_capacity) mw_cap = std::min<uint64_t>(mw_cap, cfg.active_capacity);
 
   select_only = (cfg.flags & XKNN_FLAG_SELECT_ONLY) != 0;
   if (!select_only) {
@@ -710,8 +711,9 @@ xknn_status_t xknn_layer_set_config(xknn_layer_t* h, const xknn_config_t* cfg) {
   GUARD_H(h);
   Layer& L = h->L;
   if (cfg->m_active != L.cfg.m_active || cfg->max_batch != L.cfg.max_batch ||
-      cfg->precision != L.cfg.precision)
-    return fail(XKNN_ERR_CONFIG, "m_active, max_batch and precision are fixed at creation");
+      cfg->precision != L.cfg.precision || cfg->active_capacity != L.cfg.active_capacity)
+    return fail(XKNN_ERR_CONFIG,
+                "m_active, max_batch, precision and active_capacity are fixed at creation");
   XK_TRY_H(check_scale(cfg));
   // a prepared selection drew from the old rng_seed: the next step selects again
   XK_TRY_H(L.cancel_prepared());

@@ -135,7 +135,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
                              uint32_t nblocks, uint32_t base, uint32_t* __restrict__ out,
                              uint32_t* __restrict__ pos_of, unsigned long long* pool_counts,
                              int rank, uint32_t* __restrict__ samp,
-                             const unsigned long long* __restrict__ err) {
+                             unsigned long long* __restrict__ err, uint32_t cap) {
   griddep_wait();
   griddep_launch();
   using BS = cub::BlockScan<uint32_t, kCompactBlock>;
@@ -143,7 +143,12 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
   const uint64_t w = (uint64_t)blockIdx.x * kCompactBlock + threadIdx.x;
   // a step that already failed (MTooSmall, LabelOutOfRange, ...) gets an empty active set: the
   // reference throws before any of it runs, and an over-full set would not fit the capacity
-  const bool dead = mode == 1 && *err != 0;
+  // a final set larger than the layer's active capacity (xknn_config_t::active_capacity) is not
+  // written: OutOfMemory, as an allocation failure of the reference would be
+  const bool over = mode == 1 && blk_off[nblocks] > cap;
+  if (over && blockIdx.x == 0 && threadIdx.x == 0)
+    raise_error(err, XKNN_ERR_OUT_OF_MEMORY, blk_off[nblocks]);
+  const bool dead = mode == 1 && (over || *err != 0);
   uint32_t word = 0;
   if (w < nwords && !dead) word = final_word(mode, st, act, pool, lab, w);
   uint32_t pos;
@@ -166,7 +171,7 @@ __global__ void k_bits_write(int mode, SelState* st, const uint32_t* __restrict_
       pool_counts[2 * rank] = total;              // exchanged: [pool, distinct labels] per shard
       pool_counts[2 * rank + 1] = st->labels_local;
     } else {
-      st->active_count = dead ? 0u : total;
+      st->active_count = (dead || over) ? 0u : total;
     }
   }
 }
@@ -506,7 +511,7 @@ static xknn_status_t compact_bits(Layer& L, int mode, uint32_t* out, uint32_t* p
   launch_pdl(k_bits_write, nblocks, kCompactBlock, 0, L.stream, 
       mode, L.st, L.act_bits, L.pool_bits, L.lab_bits, L.nwords, L.blk_counts + nblocks + 1,
       nblocks, (uint32_t)L.begin, out, pos_of, L.pool_counts, L.rank,
-      mode == 0 ? L.pool_samp : nullptr, L.err);
+      mode == 0 ? L.pool_samp : nullptr, L.err, mode == 0 ? 0xffffffffu : (uint32_t)L.mw_cap);
   ++L.launches;
   return L.cuda_ok(cudaGetLastError(), __FILE__, __LINE__, "k_bits_write");
 }

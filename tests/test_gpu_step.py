@@ -288,3 +288,28 @@ def test_step_loss_into_pinned_host_memory():
         out.append(float(buf.cpu()[0]))
         layer.close()
     assert out[0] == out[1] and np.isfinite(out[0]) and out[0] > 0
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32tc"])
+def test_step_active_capacity_exceeded(precision):
+    """xknn_config_t::active_capacity below the shard's active count: the step fails with
+    OutOfMemory at sync and touches no parameter; a layer with room runs the same step."""
+    import paper_2102_06025_b200 as X
+
+    torch = torch_cuda()
+    prec = {"bf16": X.PREC_BF16, "fp32tc": X.PREC_FP32}[precision]
+    n, b, k, m = 20_000, 128, 10, 2_000
+    rng = np.random.default_rng(3)
+    w = (rng.standard_normal((n, 512)) * 0.05).astype(np.float32)
+    g = O.random_graph(n, k, 2)
+    x = torch.from_numpy(rng.standard_normal((b, 512)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, n, b).astype(np.int32)).cuda()
+    small = make_layer(n, 512, 1, 0, m, b, w, g, precision=prec, seed=42, active_capacity=1_500)
+    with pytest.raises(X.OutOfMemory):
+        small.train_step(x, lab, 0.1)
+    assert np.array_equal(small.weights().cpu().numpy(), w)
+    roomy = make_layer(n, 512, 1, 0, m, b, w, g, precision=prec, seed=42, active_capacity=2_000)
+    loss = roomy.train_step(x, lab, 0.1)
+    assert np.isfinite(loss)
+    small.close()
+    roomy.close()
