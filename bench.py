@@ -32,6 +32,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+if os.environ.get("XKNN_PKG_DIR"):  # A/B runs against another build of the package
+    sys.path.insert(0, os.environ["XKNN_PKG_DIR"])
 
 WORKLOADS = {
     "c1": dict(n=100_000, b=256, k=10),

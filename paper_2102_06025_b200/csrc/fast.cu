@@ -78,10 +78,18 @@ struct Cfg2<kF> {  // P~ rows leave through one staging block per warp (plain st
   static constexpr uint32_t NBUF = 2, ACC = 256, STG = 2048, NSTG = 1;
 };
 template <>
+#ifndef XKNN_DX_KC
+#define XKNN_DX_KC 64
+#endif
 struct Cfg2<kDX> {
-  static constexpr uint32_t STAGES = 6, A_BYTES = 128 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
+  // KC classes of K per stage: A = this CTA's 128 batch rows x KC (P~, K-major, KC * 2 B rows),
+  // B = KC rows x 4 atoms of 64 d (W_sub, MN-major) -- 64 fills the 128-B swizzle rows of A and
+  // halves the stages (and TMA transactions / barrier round trips) per unit of work vs 32
+  static constexpr uint32_t KC = XKNN_DX_KC;
+  static constexpr uint32_t STAGES = KC == 64 ? 4 : 6, A_BYTES = 128 * KC * 2,
+                            B_BYTES = 4 * 64 * KC * 2;
   static constexpr uint32_t ARES_BYTES = 0;
-  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = 2;  // TMA-store staging
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = KC == 64 ? 1 : 2;
 };
 template <>
 struct Cfg2<kDW> {
@@ -128,6 +136,7 @@ __device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
   return a.nbt / MCP * a.splits;  // nbt = batch pair-tiles (256 rows), splits = ranges per tile
 }
 
+
 template <int KIND, int MCP>
 __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32_t u,
                                           uint32_t pc) {
@@ -157,7 +166,7 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
   const uint32_t nbc = a.nbt / MCP;
   const uint32_t bp = (u % nbc) * MCP + pc, r = u / nbc;
   x.id = bp + r * a.nbt;  // the pair-tile unit index (dX partial slots)
-  const uint32_t nt = KIND == kF ? (mw + 255) / 256 : (mw + 31) / 32;
+  const uint32_t nt = KIND == kF ? (mw + 255) / 256 : (mw + Cfg2<kDX>::KC - 1) / Cfg2<kDX>::KC;
   x.row0 = bp * 256;
   x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
   x.t1 = (uint32_t)((uint64_t)(r + 1) * nt / a.splits);
@@ -475,7 +484,9 @@ __global__ void __launch_bounds__(384, 1)
               tc::tma_load_2d_2sm_mc(dB + pc * 8192, &tmB, &full[stage], (int32_t)(kc * 64),
                                      (int32_t)(ct * 256 + cta * 128 + pc * 64), bmask);
           } else {
-            const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * 32);
+            constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : 32;
+            constexpr uint32_t BOX = 64 * KC * 2;  // one B atom (64 d x KC rows)
+            const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * KC);
             if (KIND == kDX) {
               tc::tma_load_2d_2sm(dA, &tmA, &full[stage], kk, myrow);  // P~ [b][class]
             } else {
@@ -488,12 +499,12 @@ __global__ void __launch_bounds__(384, 1)
               for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)  // this CTA's half of each 256-wide N instruction
-                  tc::tma_load_2d_2sm(dB + (j * 2 + h) * 4096, &tmB, &full[stage],
+                  tc::tma_load_2d_2sm(dB + (j * 2 + h) * BOX, &tmB, &full[stage],
                                       (int32_t)(256 * j + 128 * cta + 64 * h), kk);
             } else {  // pair pc fetches the h = pc pieces for both pairs
 #pragma unroll
               for (int j = 0; j < 2; ++j)
-                tc::tma_load_2d_2sm_mc(dB + (j * 2 + pc) * 4096, &tmB, &full[stage],
+                tc::tma_load_2d_2sm_mc(dB + (j * 2 + pc) * BOX, &tmB, &full[stage],
                                        (int32_t)(256 * j + 128 * cta + 64 * pc), kk, bmask);
             }
           }
@@ -535,15 +546,19 @@ __global__ void __launch_bounds__(384, 1)
                                  (k | kk) != 0);
             } else {
               constexpr uint32_t id = tc::idesc_bf16(256, 256, KIND == kDW, true);
+              constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : 32;
+              constexpr uint32_t BOX = 64 * KC * 2;
 #pragma unroll
-              for (uint32_t kk = 0; kk < 2; ++kk) {
+              for (uint32_t kk = 0; kk < KC / 16; ++kk) {
                 const uint64_t da =
-                    KIND == kDX ? tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64)
-                                : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                    KIND == kDX
+                        ? (KC == 64 ? tc::smem_desc(a0 + kk * 32, 16, 1024, tc::kSwizzle128)
+                                    : tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64))
+                        : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
 #pragma unroll
                 for (uint32_t j = 0; j < 2; ++j)
                   tc::mma_bf16_2sm(dcol + j * 256, da,
-                                   tc::smem_desc(b0 + j * 8192 + kk * 2048, 4096, 1024,
+                                   tc::smem_desc(b0 + j * 2 * BOX + kk * 2048, BOX, 1024,
                                                  tc::kSwizzle128),
                                    id, (k | kk) != 0);
               }
@@ -1110,8 +1125,10 @@ xknn_status_t Layer::init_fast() {
   ok &= make_map(&f->mF_A, Xhat16, d, f->bpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mF2_B, Wsub16, d, f->mwpad, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mF2_B64, Wsub16, d, f->mwpad, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B);
-  ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  constexpr uint32_t KC = Cfg2<kDX>::KC;
+  ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, KC, 128,
+                 KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+  ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, KC, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mPt_st, Pt, ldp, f->bpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1240,9 +1257,10 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
                        f->mDX_B, f->mDXP_st, ga);
   XK_LAUNCH();
   mark(7);
-  launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred, (uint32_t)B,
-             nbp, dx_splits, 256u, cfg.scale, (const int32_t*)label_col, (const uint32_t*)active,
-             begin, (const float*)W, (const float*)wnorm, world > 1 ? dXpart : dX);
+  launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred,
+             (uint32_t)B, nbp, dx_splits, 256u, cfg.scale, (const int32_t*)label_col,
+             (const uint32_t*)active, begin, (const float*)W, (const float*)wnorm,
+             world > 1 ? dXpart : dX);
   XK_LAUNCH();
   const uint64_t bl = B / world;
   if (world > 1) {
