@@ -92,12 +92,19 @@ struct Cfg2<kDX> {
   static constexpr uint32_t NBUF = 1, ACC = 512, STG = 4096, NSTG = KC == 64 ? 1 : 2;
 };
 template <>
+#ifndef XKNN_DW_KC
+#define XKNN_DW_KC 64
+#endif
 struct Cfg2<kDW> {
-  static constexpr uint32_t STAGES = 6, A_BYTES = 2 * 64 * 32 * 2, B_BYTES = 4 * 64 * 32 * 2;
+  // KC batch rows of K per stage: A = 2 atoms of 64 classes x KC (P~ᵀ, MN-major), B = 4 atoms of
+  // 64 d x KC (X_hat', MN-major)
+  static constexpr uint32_t KC = XKNN_DW_KC;
+  static constexpr uint32_t STAGES = KC == 64 ? 4 : 6, A_BYTES = 2 * 64 * KC * 2,
+                            B_BYTES = 4 * 64 * KC * 2;
   static constexpr uint32_t ARES_BYTES = 0;
-  // bf16 output: 2 KB per 32x32 chunk, four chunks in flight per warp (the accumulator is
+  // bf16 output: 2 KB per 32x32 chunk, NSTG chunks in flight per warp (the accumulator is
   // single-buffered, so the drain's store waits sit on the MMA's critical path)
-  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 2048, NSTG = 4;
+  static constexpr uint32_t NBUF = 1, ACC = 512, STG = 2048, NSTG = KC == 64 ? 2 : 4;
 };
 
 template <>
@@ -468,7 +475,7 @@ __global__ void __launch_bounds__(384, 1)
         } else if (KIND == kDX) {
           nk = x.t1 - x.t0;
         } else {
-          nk = a.bpad / 32;
+          nk = a.bpad / Cfg2<kDW>::KC;
         }
         for (uint32_t k = 0; k < nk; ++k) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -484,15 +491,15 @@ __global__ void __launch_bounds__(384, 1)
               tc::tma_load_2d_2sm_mc(dB + pc * 8192, &tmB, &full[stage], (int32_t)(kc * 64),
                                      (int32_t)(ct * 256 + cta * 128 + pc * 64), bmask);
           } else {
-            constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : 32;
-            constexpr uint32_t BOX = 64 * KC * 2;  // one B atom (64 d x KC rows)
+            constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : Cfg2<kDW>::KC;
+            constexpr uint32_t BOX = 64 * KC * 2;  // one MN-major atom (64 columns x KC rows)
             const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * KC);
             if (KIND == kDX) {
               tc::tma_load_2d_2sm(dA, &tmA, &full[stage], kk, myrow);  // P~ [b][class]
             } else {
 #pragma unroll
               for (int j = 0; j < 2; ++j)  // P~ᵀ: this CTA's 128 classes at batch rows kk..
-                tc::tma_load_2d_2sm(dA + j * 4096, &tmA, &full[stage], myrow + j * 64, kk);
+                tc::tma_load_2d_2sm(dA + j * BOX, &tmA, &full[stage], myrow + j * 64, kk);
             }
             if (MCP == 1 || KIND == kDW) {
 #pragma unroll
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(384, 1)
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
           const uint32_t nk =
-              (KIND == kF || KIND == kG) ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / 32);
+              (KIND == kF || KIND == kG) ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / Cfg2<kDW>::KC);
           for (uint32_t k = 0; k < nk; ++k) {
             tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(384, 1)
                                  (k | kk) != 0);
             } else {
               constexpr uint32_t id = tc::idesc_bf16(256, 256, KIND == kDW, true);
-              constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : 32;
+              constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : Cfg2<kDW>::KC;
               constexpr uint32_t BOX = 64 * KC * 2;
 #pragma unroll
               for (uint32_t kk = 0; kk < KC / 16; ++kk) {
@@ -554,7 +561,7 @@ __global__ void __launch_bounds__(384, 1)
                     KIND == kDX
                         ? (KC == 64 ? tc::smem_desc(a0 + kk * 32, 16, 1024, tc::kSwizzle128)
                                     : tc::smem_desc(a0 + kk * 32, 16, 512, tc::kSwizzle64))
-                        : tc::smem_desc(a0 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                        : tc::smem_desc(a0 + kk * 2048, BOX, 1024, tc::kSwizzle128);
 #pragma unroll
                 for (uint32_t j = 0; j < 2; ++j)
                   tc::mma_bf16_2sm(dcol + j * 256, da,
@@ -1129,8 +1136,8 @@ xknn_status_t Layer::init_fast() {
   ok &= make_map(&f->mDX_A, Pt, ldp, f->bpad, KC, 128,
                  KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   ok &= make_map(&f->mDX_B, Wsub16, d, f->mwpad, 64, KC, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mDW_A, Pt, ldp, f->bpad, 64, Cfg2<kDW>::KC, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&f->mDW_B, Xs16, d, f->bpad, 64, Cfg2<kDW>::KC, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&f->mPt_st, Pt, ldp, f->bpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   ok &= make_map(&f->mDXP_st, f->partial_dx, 512, f->dx_units_cap, 32, 32,
                  CU_TENSOR_MAP_SWIZZLE_128B, true);
