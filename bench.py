@@ -2,7 +2,11 @@
 """KNN-softmax fwd+bwd+update throughput on B200 (samples/s), driver contract of this repo.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c3|c4|c1] [--precision bf16|fp32]
+                    [--workload c2|c3|c4|c4r|c1] [--precision fp32|bf16|fp32_exact]
+                    [--no-bf16-line]
+
+The headline runs XKNN_PREC_FP32 (3xTF32 tensor cores, within 1e-5 of the fp32 reference);
+the same workload in the bf16 tensor-core mode is reported beside it as `bf16_mode`.
 
 One step = the fc half of HybridSim::train_step (parallel.cpp:455-572, :638-668) over one global
 batch: feature/label all-gather, Algorithm-1 active-class selection, active-row gather +
@@ -303,7 +307,7 @@ def reference_cpu(wl, steps, warmup, budget_s=150.0, workers=None, max_n=1_000_0
 # ----------------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------------
-def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
+def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
     import torch
 
     import paper_2102_06025_b200 as X
@@ -319,8 +323,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             uid.copy_(torch.frombuffer(bytearray(X.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         comm = X.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
-    prec = {"bf16": X.PREC_BF16, "fp32": X.PREC_FP32, "fp32_exact": X.PREC_FP32_EXACT}[
-        args.precision]
+    precision = precision or args.precision
+    prec = {"bf16": X.PREC_BF16, "fp32": X.PREC_FP32, "fp32_exact": X.PREC_FP32_EXACT}[precision]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         # per-shard active capacity: uniform labels put ~M/P active classes on each shard; the
@@ -482,11 +486,11 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
         burst = (clocks.get("sm_mhz") is not None and clocks.get("sm_max_mhz") is not None and
                  clocks["sm_mhz"] >= 0.98 * clocks["sm_max_mhz"] and not clocks["reasons"])
         splits = max(1, -(-148 // max(1, -(-b // 256))))  # dX split-K ranges (upper bound)
-        kern, floor_ms = kernel_rooflines(phase_ms, args.precision, b, active_local, splits, pk,
+        kern, floor_ms = kernel_rooflines(phase_ms, precision, b, active_local, splits, pk,
                                           burst)
         dom = max(kern, key=lambda k_: kern[k_]["ms"])
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "r02", f"traffic_{wl_name}_{args.precision}.json")
+        tp = os.path.join(ROOT, "profiles", "r02", f"traffic_{wl_name}_{precision}.json")
         if os.path.exists(tp):
             try:
                 traffic = json.load(open(tp)).get(dom)
@@ -497,13 +501,13 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
                 "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
                 "work_per_launch": kd["work"], "launch_ms": kd["ms"],
                 "peak_source": (pk["tf32_src"] + " / 3 (three TF32 MMAs per fp32 product)"
-                                if args.precision != "bf16" and kd["bound"] == "tensor" else
+                                if precision != "bf16" and kd["bound"] == "tensor" else
                                 pk["src"] + (" burst" if burst else " sustained")),
                 "how": "work per launch / the kernel's CUDA-event time on the layer stream "
                        "(phase_ms, second pass); dominant = the longest phase"}
         # whole-step floors: every kernel at its own roofline, serialized (the step's kernels
         # run back to back), and the SURVEY 8(d) overlap bound max(flops/peak, bytes/peak)
-        tpk = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if args.precision != "bf16" \
+        tpk = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if precision != "bf16" \
             else (pk["bf16_burst"] if burst else pk["bf16_sus"])
         t_roof = max(6.0 * b * mw_max * D / (tpk * 1e12), 16.0 * mw_max * D / (pk["hbm"] * 1e9))
         res = {
@@ -518,11 +522,11 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
             "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None,
-            "dtype": "bf16" if args.precision == "bf16" else "f32",
+            "dtype": "bf16" if precision == "bf16" else "f32",
             "precision": {"bf16": "bf16 operands, fp32 accumulation (stated bound, DESIGN.md 2)",
                           "fp32": "3xTF32 tensor cores, fp32 accuracy (1e-5 of the reference)",
                           "fp32_exact": "CUDA-core fp32 in the reference's summation order"}[
-                              args.precision],
+                              precision],
             "data": "synthetic (W~N(0,0.05^2), X~N(0,1), uniform labels, seeded random "
                     "self-first k-NN graph)",
             "config": {"workload": wl_name, "num_classes": n, "dim": D, "global_batch": b,
@@ -558,17 +562,22 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist):
         if world > 1:
             # N = 1 runs C2 (the largest single-GPU config, BASELINE configs[1]); this line's
             # workload also runs on one GPU, measured separately -- the base of its strong scaling
-            ref1 = os.path.join(ROOT, "profiles", "r01d", f"bench_{wl_name}_1gpu.json")
+            ref1 = os.path.join(ROOT, "profiles", "r02", f"bench_{wl_name}_1gpu_{precision}.json")
             if os.path.exists(ref1):
                 try:
                     d1 = json.load(open(ref1))
                     res["same_workload_1gpu"] = {
                         "value": d1["value"], "ms_per_step": d1["ms_per_step"],
                         "strong_scaling_efficiency": round(value / (world * d1["value"]), 4),
-                        "source": f"profiles/r01d/bench_{wl_name}_1gpu.json "
+                        "source": f"profiles/r02/bench_{wl_name}_1gpu_{precision}.json "
                                   f"(bench.py --workload {wl_name}, one B200, another box)"}
                 except (OSError, KeyError, ValueError):
                     pass
+    layer.close()
+    if comm is not None:
+        X.nccl_comm_destroy(comm)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     return res
 
 
@@ -597,7 +606,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32", "fp32_exact"])
+    ap.add_argument("--precision", default="fp32", choices=["bf16", "fp32", "fp32_exact"],
+                    help="headline arithmetic: fp32 = 3xTF32 tensor cores at the reference's "
+                         "fp32 accuracy (default); bf16 = bf16 operands, stated bound")
+    ap.add_argument("--no-bf16-line", action="store_true",
+                    help="skip the secondary bf16 measurement (bf16_mode) of the default run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
@@ -640,6 +653,14 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, wl_name, wl, rank, world, local_rank, dist)
+    if args.precision == "fp32" and not args.no_bf16_line:
+        # the same workload in the bf16 tensor-core mode (stated bound), same process
+        r16 = run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision="bf16")
+        if rank == 0:
+            res["bf16_mode"] = {k_: r16[k_] for k_ in ("value", "unit", "ms_per_step", "dtype",
+                                                       "precision", "e2e", "roofline", "kernels",
+                                                       "step_roofline", "phase_ms", "clocks",
+                                                       "gpu_launches")}
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and wl_name in ("c1", "c2"):
             # the reference on all host cores (P = nproc worker threads) and on one
