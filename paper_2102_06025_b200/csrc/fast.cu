@@ -1190,7 +1190,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ++launches;
   launch_pdl(k_zero_rows_bf16, 64, 256, 0, stream, st, Wsub16, f->mwpad, D);
   XK_LAUNCH();
-  XK_TRY(wait_features());  // features staged / all-gathered on the side stream
+  if (world > 1) XK_TRY(wait_features());
   XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, nullptr, Xhat16, xnorm, err, stream));
   ++launches;
 

@@ -653,7 +653,7 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ++launches;
   launch_pdl(k_zero_rows32, 64, 256, 0, stream, (const SelState*)st, f->w_hi, f->w_lo, f->mwpad);
   XK_LAUNCH();
-  XK_TRY(wait_features());  // features staged / all-gathered on the side stream
+  if (world > 1) XK_TRY(wait_features());
   XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, f->xh_hi, nullptr, xnorm, err,
                                 stream, false, f->xh_lo));
   ++launches;

@@ -285,7 +285,7 @@ xknn_status_t Layer::run_core(uint64_t B) {
   // feature rows normalized; active weight rows gathered + normalized (only M_w rows, never the
   // whole shard as parallel.cpp:490-492 does -- row-wise identical)
   // (the BF16 core waits for the feature all-gather only after its weight-row gather)
-  if (cfg.precision == XKNN_PREC_FP32_EXACT) XK_TRY(wait_features());
+  if (world > 1 && cfg.precision == XKNN_PREC_FP32_EXACT) XK_TRY(wait_features());
   if (cfg.precision == XKNN_PREC_FP32_EXACT) {
     XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, Xhat, nullptr, xnorm, err, stream));
     ++launches;
@@ -527,22 +527,12 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   }
   // the learning rate travels through device memory so the captured core stays valid
   if (world == 1 && (reinterpret_cast<uintptr_t>(feats_local) & 15) == 0 && d % 4 == 0) {
-    // the labels (unless prepared) and lr on the layer stream; the features on the side stream,
-    // after the previous step's last reader of X, under this step's selection and W-row gather
-    // (the core waits for them right before the feature normalize, as for the all-gather)
     const uint64_t n4 = B * d / 4;
-    launch_pdl(k_stage_inputs, grid_for(B, 256, 148u), 256, 0, stream, (float4*)nullptr,
-               (const float4*)nullptr, (uint64_t)0,
+    launch_pdl(k_stage_inputs, grid_for(n4, 256, 148u * 8u), 256, 0, stream,
+               reinterpret_cast<float4*>(X), reinterpret_cast<const float4*>(feats_local), n4,
                core_prepared ? (uint32_t*)nullptr : labels_all, labels_local, (uint64_t)B, lr_dev,
                lr);
     XK_LAUNCH();
-    XK_CUDA(cudaEventRecord(ev_in, stream));
-    XK_CUDA(cudaStreamWaitEvent(side, ev_in, 0));
-    launch_pdl(k_stage_inputs, grid_for(n4, 256, 148u * 8u), 256, 0, side,
-               reinterpret_cast<float4*>(X), reinterpret_cast<const float4*>(feats_local), n4,
-               (uint32_t*)nullptr, (const uint32_t*)nullptr, (uint64_t)0, lr_dev, lr);
-    XK_LAUNCH();
-    XK_CUDA(cudaEventRecord(ev_feat, side));
   } else {
     if (world == 1) {
       XK_CUDA(cudaMemcpyAsync(X, feats_local, B * d * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -550,7 +540,6 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
       if (!core_prepared)
         XK_CUDA(cudaMemcpyAsync(labels_all, labels_local, B * sizeof(uint32_t),
                                 cudaMemcpyDeviceToDevice, stream));
-      XK_CUDA(cudaEventRecord(ev_feat, stream));
     }
     launch_pdl(k_set_f32, 1, 1, 0, stream, lr_dev, lr);
     XK_LAUNCH();
