@@ -79,9 +79,16 @@ struct Gemm3Args {
 template <int KIND>
 struct Cfg3;
 template <>
+#ifndef XKNN_F3_KB
+#define XKNN_F3_KB 32
+#endif
 struct Cfg3<kF3> {
-  static constexpr uint32_t STAGES = 3, A_BYTES = 2 * 128 * 128, B_BYTES = 2 * 128 * 128;
-  static constexpr uint32_t NBUF = 2, ACC = 256, KB = 32;  // KB: K elements per stage
+  // KB fp32 of K per stage (KB * 4 B rows: 128B swizzle at 32, 64B at 16); 16 halves the stage
+  // size for twice the stages -- more bytes in flight while the MMAs consume one
+  static constexpr uint32_t KB = XKNN_F3_KB;
+  static constexpr uint32_t STAGES = KB == 32 ? 3 : 6, A_BYTES = 2 * 128 * KB * 4,
+                            B_BYTES = 2 * 128 * KB * 4;
+  static constexpr uint32_t NBUF = 2, ACC = 256;
 };
 template <>
 struct Cfg3<kDX3> {
@@ -235,8 +242,9 @@ __global__ void __launch_bounds__(384, 1)
           uint8_t* dA = sA + stage * C::A_BYTES;
           uint8_t* dB = sB + stage * C::B_BYTES;
           if (KIND == kF3) {
-            const int32_t kc = (int32_t)((k % 16) * 32);
-            const int32_t crow = (int32_t)((x.t0 + k / 16) * 256 + cta * 128);
+            constexpr uint32_t NKB = 512 / C::KB;  // stages per class tile
+            const int32_t kc = (int32_t)((k % NKB) * C::KB);
+            const int32_t crow = (int32_t)((x.t0 + k / NKB) * 256 + cta * 128);
             tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
             tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
             tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(384, 1)
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
           const uint32_t nk =
-              KIND == kF3 ? 16 : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
+              KIND == kF3 ? 512 / C::KB : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
           for (uint32_t k = 0; k < nk; ++k) {
             tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
@@ -290,12 +298,14 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t bh = tc::smem_u32(sB + stage * C::B_BYTES), bl = bh + C::B_BYTES / 2;
             if (KIND == kF3) {
               constexpr uint32_t id = idesc_tf32(256, 256, false, false);
+              constexpr uint32_t SBO = C::KB * 4 * 8;  // 8-row group of KB * 4-byte rows
+              constexpr uint32_t SW = C::KB == 32 ? tc::kSwizzle128 : tc::kSwizzle64;
 #pragma unroll
-              for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 8 fp32 = 32 B per instruction
-                const uint64_t dah = tc::smem_desc(ah + kk * 32, 16, 1024, tc::kSwizzle128);
-                const uint64_t dal = tc::smem_desc(al + kk * 32, 16, 1024, tc::kSwizzle128);
-                const uint64_t dbh = tc::smem_desc(bh + kk * 32, 16, 1024, tc::kSwizzle128);
-                const uint64_t dbl = tc::smem_desc(bl + kk * 32, 16, 1024, tc::kSwizzle128);
+              for (uint32_t kk = 0; kk < C::KB / 8; ++kk) {  // K = 8 fp32 = 32 B per instruction
+                const uint64_t dah = tc::smem_desc(ah + kk * 32, 16, SBO, SW);
+                const uint64_t dal = tc::smem_desc(al + kk * 32, 16, SBO, SW);
+                const uint64_t dbh = tc::smem_desc(bh + kk * 32, 16, SBO, SW);
+                const uint64_t dbl = tc::smem_desc(bl + kk * 32, 16, SBO, SW);
                 mma_tf32_2sm(dcol, dal, dbh, id, (k | kk) != 0);  // small terms first
                 mma_tf32_2sm(dcol, dah, dbl, id, 1u);
                 mma_tf32_2sm(dcol, dah, dbh, id, 1u);
@@ -599,10 +609,12 @@ xknn_status_t Layer::init_fast32() {
   const auto S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
   const auto S32G = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;  // MN-major tf32 operands
   bool ok = true;
-  ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, 32, 128, S128);
-  ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, 32, 128, S128);
-  ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, 32, 128, S128);
-  ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, 32, 128, S128);
+  constexpr uint32_t FKB = Cfg3<kF3>::KB;
+  const auto SF = FKB == 32 ? S128 : S64;
+  ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, FKB, 128, SF);
+  ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, FKB, 128, SF);
+  ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, FKB, 128, SF);
+  ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, FKB, 128, SF);
   ok &= make_map32(&f->mDX_Ah, f->p_hi, f->mwpad, f->bpad, 16, 128, S64);
   ok &= make_map32(&f->mDX_Al, f->p_lo, f->mwpad, f->bpad, 16, 128, S64);
   ok &= make_map32(&f->mDX_Bh, f->w_hi, 512, f->mwpad, 32, 16, S32G);
