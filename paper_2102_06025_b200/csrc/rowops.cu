@@ -118,8 +118,12 @@ __device__ __forceinline__ float4 load_g4(const __nv_bfloat16* __restrict__ G, u
                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
 }
 
+#ifndef XKNN_UPD_MINB
+#define XKNN_UPD_MINB 2
+#endif
 template <int DV, typename GT = float>
-__global__ void k_update_rows(float* __restrict__ W, float* __restrict__ V,
+__global__ void __launch_bounds__(256, XKNN_UPD_MINB)
+    k_update_rows(float* __restrict__ W, float* __restrict__ V,
                               const GT* __restrict__ G, const uint32_t* __restrict__ active,
                               const unsigned int* count, uint64_t begin, uint32_t d,
                               const float* __restrict__ wnorm, const float* __restrict__ lr_dev,
