@@ -611,6 +611,8 @@ def main():
                          "fp32 accuracy (default); bf16 = bf16 operands, stated bound")
     ap.add_argument("--no-bf16-line", action="store_true",
                     help="skip the secondary bf16 measurement (bf16_mode) of the default run")
+    ap.add_argument("--bf16-pause", type=float, default=15.0,
+                    help="seconds idle between the fp32 run and the bf16 line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
@@ -654,7 +656,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, wl_name, wl, rank, world, local_rank, dist)
     if args.precision == "fp32" and not args.no_bf16_line:
-        # the same workload in the bf16 tensor-core mode (stated bound), same process
+        # the same workload in the bf16 tensor-core mode (stated bound), same
+        # process, after a pause that lets the power limiter recover from the fp32 run
+        time.sleep(args.bf16_pause)
         r16 = run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision="bf16")
         if rank == 0:
             res["bf16_mode"] = {k_: r16[k_] for k_ in ("value", "unit", "ms_per_step", "dtype",

@@ -35,6 +35,7 @@ __device__ __forceinline__ void epilogue_bar() {  // the 8 epilogue warps only
 struct GemmArgs {
   const SelState* st;
   uint32_t B, bpad, nbt, splits, dim;
+  uint32_t dwsplit;  // GEMM-dW: split the tail units along K (dw_split) -- see Layer::run_fast_core
   float scale;
   const int32_t* label_col;
   __nv_bfloat16* Pt;
@@ -123,9 +124,10 @@ constexpr uint32_t smem_bytes2() {
 
 struct Unit2 {
   uint32_t row0;   // F/dX: first batch row of the pair; dW: first class of the pair
-  uint32_t t0, t1; // F: class-tile range; dX: 32-class K-chunk range; dW: unused
-  uint32_t id;
+  uint32_t t0, t1; // F: class-tile range; dX: K-chunk range; dW: K-stage range (batch rows)
+  uint32_t id;     // dX: partial slot; dW: partial slot of a split tail unit
   bool valid;
+  bool part;       // dW: a K-partial of a tail unit (fp32 partial rows, dw_split)
 };
 
 // Work units of one CTA pair.  With MCP = 2 the two pairs of a 4-CTA cluster take sibling
@@ -133,7 +135,11 @@ struct Unit2 {
 // -- and every B tile is fetched once per cluster and multicast to both pairs.
 template <int KIND, int MCP>
 __device__ __forceinline__ uint32_t num_units2(const GemmArgs& a, uint32_t mw) {
-  if (KIND == kDW) return (mw + 255) / 256;
+  if (KIND == kDW) {
+    const uint32_t units = (mw + 255) / 256;
+    const DwSplit sp = a.dwsplit ? dw_split(units, gridDim.x / (2 * MCP)) : DwSplit{units, 1};
+    return sp.full + (units - sp.full) * sp.s;
+  }
   if (KIND == kG) {  // chunk-major: every pair's row blocks against chunk 0, then chunk 1, ...
     const uint32_t npairs = gridDim.x / (2 * MCP);
     const uint32_t nrb = (a.nrows + 256 * MCP - 1) / (256 * MCP);
@@ -150,8 +156,22 @@ __device__ __forceinline__ Unit2 unit2_of(const GemmArgs& a, uint32_t mw, uint32
   Unit2 x{};
   x.id = u;
   if (KIND == kDW) {
-    x.row0 = u * 256;
+    const uint32_t nk = a.bpad / Cfg2<kDW>::KC;
+    const uint32_t units = (mw + 255) / 256;
+    const DwSplit sp = a.dwsplit ? dw_split(units, gridDim.x / (2 * MCP)) : DwSplit{units, 1};
     x.valid = true;
+    if (u < sp.full) {
+      x.row0 = u * 256;
+      x.t0 = 0;
+      x.t1 = nk;
+      return x;
+    }
+    const uint32_t v = u - sp.full, tt = v / sp.s, p = v % sp.s;
+    x.row0 = (sp.full + tt) * 256;
+    x.t0 = p * nk / sp.s;
+    x.t1 = (p + 1) * nk / sp.s;
+    x.id = v;  // = tt * s + p
+    x.part = true;
     return x;
   }
   if (KIND == kG) {
@@ -395,7 +415,8 @@ __device__ __noinline__ void merge_candidates(float2* __restrict__ list, uint32_
 template <int KIND, int MCP = 1>
 __global__ void __launch_bounds__(384, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            const __grid_constant__ CUtensorMap tmOut, GemmArgs a) {
+            const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmOut2,
+            GemmArgs a) {
   using C = Cfg2<KIND>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned by pointer arithmetic on the __shared__ array, so the compiler keeps the
@@ -472,10 +493,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int kc = 0; kc < 8; ++kc)
             tc::tma_load_2d_2sm(sRes + kc * 16384, &tmA, afull, kc * 64, myrow);
           nk = (x.t1 - x.t0) * 8;
-        } else if (KIND == kDX) {
-          nk = x.t1 - x.t0;
         } else {
-          nk = a.bpad / Cfg2<kDW>::KC;
+          nk = x.t1 - x.t0;
         }
         for (uint32_t k = 0; k < nk; ++k) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -493,7 +512,7 @@ __global__ void __launch_bounds__(384, 1)
           } else {
             constexpr uint32_t KC = KIND == kDX ? Cfg2<kDX>::KC : Cfg2<kDW>::KC;
             constexpr uint32_t BOX = 64 * KC * 2;  // one MN-major atom (64 columns x KC rows)
-            const int32_t kk = (int32_t)((KIND == kDX ? x.t0 + k : k) * KC);
+            const int32_t kk = (int32_t)((x.t0 + k) * KC);
             if (KIND == kDX) {
               tc::tma_load_2d_2sm(dA, &tmA, &full[stage], kk, myrow);  // P~ [b][class]
             } else {
@@ -535,8 +554,7 @@ __global__ void __launch_bounds__(384, 1)
           tc::mbar_wait(&tempty[buf], tphase ^ 1);
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
-          const uint32_t nk =
-              (KIND == kF || KIND == kG) ? 8 : (KIND == kDX ? x.t1 - x.t0 : a.bpad / Cfg2<kDW>::KC);
+          const uint32_t nk = (KIND == kF || KIND == kG) ? 8 : x.t1 - x.t0;
           for (uint32_t k = 0; k < nk; ++k) {
             tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
@@ -796,8 +814,11 @@ __global__ void __launch_bounds__(384, 1)
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
         } else {
-          // dX: split-K partial rows of unit x.id; dW: dW rows (compact active order)
-          const int32_t orow = KIND == kDX ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
+          // dX: split-K partial rows of unit x.id; dW: dW rows (compact active order), or the
+          // fp32 K-partial rows of a split tail unit (slot x.id)
+          const bool part = KIND == kDW && x.part;
+          const int32_t orow = (KIND == kDX || part) ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0
+                                                     : grow0;
           const bool zero = KIND == kDX && x.t1 == x.t0;
 #pragma unroll 1
           for (uint32_t ch = 0; ch < 8; ++ch) {
@@ -808,6 +829,20 @@ __global__ void __launch_bounds__(384, 1)
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            if (KIND == kDW && part) {  // fp32 partial through the warp's whole 4 KB staging
+              if (lane == 0) tc::tma_store_wait_read<0>();
+              __syncwarp();
+              stage_f32(stg, lane, v);
+              tc::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tc::tma_store_2d(&tmOut2, stg, (int32_t)col, orow);
+                tc::tma_store_commit();
+                tc::tma_store_wait_read<0>();
+              }
+              __syncwarp();
+              continue;
             }
             if (KIND == kDW) {  // dW rows in bf16 (64-B swizzled staging rows)
               uint32_t pk[16];
@@ -1043,10 +1078,11 @@ struct FastState {
   float* labelterm = nullptr;       // [bpad]
   float* partial_dx = nullptr;      // [units][256][512]
   __nv_bfloat16* dW16 = nullptr;    // [mwpad][512] weight gradient, compact active order
+  float* dw_part = nullptr;         // [74 slots][256][512] GEMM-dW tail-unit K-partials
   int32_t* lab_head = nullptr;      // [mwpad] first batch row labelled with each active column
   int32_t* lab_next = nullptr;      // [bpad]  next batch row with the same label column
   CUtensorMap mF_A, mF2_B, mDX_A, mDX_B, mDW_A, mDW_B;
-  CUtensorMap mPt_st, mDXP_st, mDW_st, mF2_B64;
+  CUtensorMap mPt_st, mDXP_st, mDW_st, mF2_B64, mDWP_st;
 };
 
 // splits per 256-row pair tile so that (pair tiles x splits) units fill the 74 CTA pairs in
@@ -1124,6 +1160,7 @@ xknn_status_t Layer::init_fast() {
   f->dx_units_cap = 148ull * 256;  // pair-tile units x 256 rows (at most 148 units)
   XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
   XK_CUDA(dalloc(&f->dW16, (uint64_t)f->mwpad * d));
+  XK_CUDA(dalloc(&f->dw_part, (uint64_t)kNumSMs / 2 * 256 * 512));
   XK_CUDA(dalloc(&f->lab_head, f->mwpad));
   XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));  // all -1
   XK_CUDA(dalloc(&f->lab_next, f->bpad));
@@ -1142,6 +1179,8 @@ xknn_status_t Layer::init_fast() {
   ok &= make_map(&f->mDXP_st, f->partial_dx, 512, f->dx_units_cap, 32, 32,
                  CU_TENSOR_MAP_SWIZZLE_128B, true);
   ok &= make_map(&f->mDW_st, f->dW16, 512, f->mwpad, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok &= make_map(&f->mDWP_st, f->dw_part, 512, (uint64_t)kNumSMs / 2 * 256, 32, 32,
+                 CU_TENSOR_MAP_SWIZZLE_128B, true);
   if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   XK_CUDA(cudaFuncSetAttribute(k_gemm2<kF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes2<kF>()));
@@ -1165,6 +1204,7 @@ void Layer::free_fast() {
   if (f->dW16) cudaFree(f->dW16);
   if (f->lab_head) cudaFree(f->lab_head);
   if (f->lab_next) cudaFree(f->lab_next);
+  if (f->dw_part) cudaFree(f->dw_part);
   delete f;
   fast = nullptr;
 }
@@ -1218,11 +1258,11 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   if (mc) {
     ga.splits = gemm_pair_splits(nbp / 2, 1u << 30, grid_f4 / 4);
     launch_pdl_cluster(k_gemm2<kF, 2>, grid_f4, 384, smem_bytes2<kF>(), stream, 4u, f->mF_A,
-                       f->mF2_B64, f->mPt_st, ga);
+                       f->mF2_B64, f->mPt_st, f->mPt_st, ga);
   } else {
     ga.splits = gemm_pair_splits(nbp, 1u << 30);
     launch_pdl_cluster(k_gemm2<kF>, kNumSMs, 384, smem_bytes2<kF>(), stream, 2u, f->mF_A,
-                       f->mF2_B, f->mPt_st, ga);
+                       f->mF2_B, f->mPt_st, f->mPt_st, ga);
   }
   XK_LAUNCH();
   mark(4);
@@ -1247,7 +1287,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   // (e) GEMM-dW -> bf16 dW rows (compact active order)
   ga.out16 = f->dW16;
   launch_pdl_cluster(k_gemm2<kDW>, kNumSMs, 384, smem_bytes2<kDW>(), stream, 2u, f->mDW_A,
-                     f->mDW_B, f->mDW_st, ga);
+                     f->mDW_B, f->mDW_st, f->mDWP_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce with s*r_b -> reduce-scatter over class shards
@@ -1258,10 +1298,10 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   ga.splits = dx_splits;
   if (mc)
     launch_pdl_cluster(k_gemm2<kDX, 2>, grid_dx4, 384, smem_bytes2<kDX>(), stream, 4u, f->mDX_A,
-                       f->mDX_B, f->mDXP_st, ga);
+                       f->mDX_B, f->mDXP_st, f->mDXP_st, ga);
   else
     launch_pdl_cluster(k_gemm2<kDX>, kNumSMs, 384, smem_bytes2<kDX>(), stream, 2u, f->mDX_A,
-                       f->mDX_B, f->mDXP_st, ga);
+                       f->mDX_B, f->mDXP_st, f->mDXP_st, ga);
   XK_LAUNCH();
   mark(7);
   launch_pdl(k_dx_reduce, grid_for(B * 128, 256), 256, 0, stream, f->partial_dx, rowred,
@@ -1282,6 +1322,8 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
   //     (a separate HBM-streaming kernel: it runs at the copy roofline, while inside the
   //     GEMM-dW kernel the few spare warps per SM could not keep enough bytes in flight)
   mark(8);
+  // (the GEMM-dW tail split is off here: measured 2 us faster GEMM-dW at C2 but a 5 us slower
+  // bf16 row update; on the FP32 path, whose dW is 5x longer, it pays -- fast32.cu)
   LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B)};
   XK_CUDA(launch_update_rows_bf16(W, V, f->dW16, active, &st->active_count, mw_cap, begin, D,
                                   wnorm, lr_dev, cfg.momentum, cfg.weight_decay, err, stream, lf));
@@ -1346,9 +1388,9 @@ cudaError_t launch_graph_candidates(const __half* own, uint32_t nrows, uint32_t 
   ga.gchunk = gchunk;
   if (mc)
     launch_pdl_cluster(k_gemm2<kG, 2>, cluster_grid(k_gemm2<kG, 2>, 4, smem_bytes2<kG>()), 384,
-                       smem_bytes2<kG>(), s, 4u, mA, mB, mA, ga);
+                       smem_bytes2<kG>(), s, 4u, mA, mB, mA, mA, ga);
   else
-    launch_pdl_cluster(k_gemm2<kG>, kNumSMs, 384, smem_bytes2<kG>(), s, 2u, mA, mB, mA, ga);
+    launch_pdl_cluster(k_gemm2<kG>, kNumSMs, 384, smem_bytes2<kG>(), s, 2u, mA, mB, mA, mA, ga);
   return cudaGetLastError();
 }
 

@@ -110,14 +110,19 @@ constexpr uint32_t smem_bytes3() {
 
 struct Unit3 {
   uint32_t row0;    // F/dX: first batch row of the pair; dW: first class of the pair
-  uint32_t t0, t1;  // F: class-tile range; dX: 16-class K-chunk range; dW: unused
-  uint32_t id;
+  uint32_t t0, t1;  // F: class-tile range; dX: 16-class K-chunk range; dW: K-stage range
+  uint32_t id;      // dX: partial slot; dW: partial slot of a split tail unit
   bool valid;
+  bool part;        // dW: a K-partial of a tail unit (dw_split)
 };
 
 template <int KIND>
 __device__ __forceinline__ uint32_t num_units3(const Gemm3Args& a, uint32_t mw) {
-  if (KIND == kDW3) return (mw + 255) / 256;
+  if (KIND == kDW3) {
+    const uint32_t units = (mw + 255) / 256;
+    const DwSplit sp = dw_split(units, gridDim.x / 2);
+    return sp.full + (units - sp.full) * sp.s;
+  }
   return a.nbt * a.splits;
 }
 
@@ -126,8 +131,21 @@ __device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint3
   Unit3 x{};
   x.id = u;
   if (KIND == kDW3) {
-    x.row0 = u * 256;
+    const uint32_t nk = a.bpad / Cfg3<kDW3>::KB;
+    const DwSplit sp = dw_split((mw + 255) / 256, gridDim.x / 2);
     x.valid = true;
+    if (u < sp.full) {
+      x.row0 = u * 256;
+      x.t0 = 0;
+      x.t1 = nk;
+      return x;
+    }
+    const uint32_t v = u - sp.full, tt = v / sp.s, p = v % sp.s;
+    x.row0 = (sp.full + tt) * 256;
+    x.t0 = p * nk / sp.s;
+    x.t1 = (p + 1) * nk / sp.s;
+    x.id = v;
+    x.part = true;
     return x;
   }
   const uint32_t bp = u % a.nbt, r = u / a.nbt;
@@ -180,7 +198,8 @@ template <int KIND>
 __global__ void __launch_bounds__(384, 1)
     k_gemm3(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
             const __grid_constant__ CUtensorMap tmBhi, const __grid_constant__ CUtensorMap tmBlo,
-            const __grid_constant__ CUtensorMap tmOut, Gemm3Args a) {
+            const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmOut2,
+            Gemm3Args a) {
   using C = Cfg3<KIND>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (uint32_t)(reinterpret_cast<uintptr_t>(smem_raw) & 1023u)) & 1023u);
@@ -234,8 +253,7 @@ __global__ void __launch_bounds__(384, 1)
         const Unit3 x = unit3_of<KIND>(a, mw, u);
         if (!x.valid) continue;
         const int32_t myrow = (int32_t)(x.row0 + cta * 128);
-        const uint32_t nk = KIND == kF3 ? (x.t1 - x.t0) * (512 / C::KB)
-                                        : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
+        const uint32_t nk = KIND == kF3 ? (x.t1 - x.t0) * (512 / C::KB) : x.t1 - x.t0;
         for (uint32_t k = 0; k < nk; ++k) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
@@ -250,7 +268,7 @@ __global__ void __launch_bounds__(384, 1)
             tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
             tc::tma_load_2d_2sm(dB + C::B_BYTES / 2, &tmBlo, &full[stage], kc, crow);
           } else {
-            const int32_t kk = (int32_t)((KIND == kDX3 ? x.t0 + k : k) * 16);
+            const int32_t kk = (int32_t)((x.t0 + k) * 16);
             if (KIND == kDX3) {  // P~ [b][class]: this CTA's 128 batch rows, 16 classes
               tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kk, myrow);
               tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kk, myrow);
@@ -289,8 +307,7 @@ __global__ void __launch_bounds__(384, 1)
           tc::mbar_wait(&tempty[buf], tphase ^ 1);
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
-          const uint32_t nk =
-              KIND == kF3 ? 512 / C::KB : (KIND == kDX3 ? x.t1 - x.t0 : a.bpad / C::KB);
+          const uint32_t nk = KIND == kF3 ? 512 / C::KB : x.t1 - x.t0;
           for (uint32_t k = 0; k < nk; ++k) {
             tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
@@ -413,8 +430,11 @@ __global__ void __launch_bounds__(384, 1)
           a.partial[(uint64_t)(ct * 2 + h) * a.bpad + b] = sum;
           if (has) a.labelterm[b] = lab - a.scale;
         } else {
-          // dX: split-K partial rows of unit x.id; dW: fp32 dW rows (compact active order)
-          const int32_t orow = KIND == kDX3 ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0 : grow0;
+          // dX: split-K partial rows of unit x.id; dW: fp32 dW rows (compact active order), or
+          // the K-partial rows of a split tail unit (slot x.id, through tmOut2)
+          const bool part = KIND == kDW3 && x.part;
+          const int32_t orow = (KIND == kDX3 || part) ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0
+                                                      : grow0;
           const bool zero = KIND == kDX3 && x.t1 == x.t0;
 #pragma unroll 1
           for (uint32_t ch = 0; ch < 8; ++ch) {
@@ -430,7 +450,7 @@ __global__ void __launch_bounds__(384, 1)
             tc::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tc::tma_store_2d(&tmOut, stg, (int32_t)col, orow);
+              tc::tma_store_2d(part ? &tmOut2 : &tmOut, stg, (int32_t)col, orow);
               tc::tma_store_commit();
               tc::tma_store_wait_read<0>();
             }
@@ -569,11 +589,13 @@ struct Fast32State {
   float* labelterm = nullptr;                // [bpad]
   float* partial_dx = nullptr;               // [units][256][512]
   float* dW32 = nullptr;                     // [mwpad][512]
+  float* dw_part = nullptr;                  // [74 slots][256][512] tail-unit K-partials
   int32_t* lab_head = nullptr;               // [mwpad]
   int32_t* lab_next = nullptr;               // [bpad]
   CUtensorMap mF_Ah, mF_Al, mF_Bh, mF_Bl;    // X_hat, W_sub (K-major, 32 x 128 boxes)
   CUtensorMap mDX_Ah, mDX_Al, mDX_Bh, mDX_Bl, mDX_st;  // P~ (16 x 128, SW64), W_sub (32 x 16)
   CUtensorMap mDW_Ah, mDW_Al, mDW_Bh, mDW_Bl, mDW_st;  // P~ (32 x 16), X_hat' (32 x 16)
+  CUtensorMap mDWP_st;                                 // dW tail-unit K-partials
 };
 
 xknn_status_t Layer::init_fast32() {
@@ -602,6 +624,7 @@ xknn_status_t Layer::init_fast32() {
   f->dx_units_cap = 148ull * 256;
   XK_CUDA(dalloc(&f->partial_dx, f->dx_units_cap * 512));
   XK_CUDA(dalloc(&f->dW32, wb));
+  XK_CUDA(dalloc(&f->dw_part, (uint64_t)kNumSMs / 2 * 256 * 512));
   XK_CUDA(dalloc(&f->lab_head, f->mwpad));
   XK_CUDA(cudaMemsetAsync(f->lab_head, 0xff, (uint64_t)f->mwpad * 4, stream));
   XK_CUDA(dalloc(&f->lab_next, f->bpad));
@@ -625,6 +648,7 @@ xknn_status_t Layer::init_fast32() {
   ok &= make_map32(&f->mDW_Bh, f->xs_hi, 512, f->bpad, 32, 16, S32G);
   ok &= make_map32(&f->mDW_Bl, f->xs_lo, 512, f->bpad, 32, 16, S32G);
   ok &= make_map32(&f->mDW_st, f->dW32, 512, f->mwpad, 32, 32, S128);
+  ok &= make_map32(&f->mDWP_st, f->dw_part, 512, (uint64_t)kNumSMs / 2 * 256, 32, 32, S128);
   if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kF3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes3<kF3>()));
@@ -641,6 +665,7 @@ void Layer::free_fast32() {
   for (void* p : {(void*)f->xh_hi, (void*)f->xh_lo, (void*)f->xs_hi, (void*)f->xs_lo,
                   (void*)f->w_hi, (void*)f->w_lo, (void*)f->p_hi, (void*)f->p_lo,
                   (void*)f->partial_f, (void*)f->labelterm, (void*)f->partial_dx, (void*)f->dW32,
+                  (void*)f->dw_part,
                   (void*)f->lab_head, (void*)f->lab_next})
     if (p) cudaFree(p);
   delete f;
@@ -686,7 +711,7 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ga.nbt = nbp;
   ga.splits = gemm_pair_splits(nbp, 1u << 30);
   launch_pdl_cluster(k_gemm3<kF3>, kNumSMs, 384, smem_bytes3<kF3>(), stream, 2u, f->mF_Ah,
-                     f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, ga);
+                     f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, f->mF_Ah, ga);
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over the class shards -> (d) loss, X_hat', label lists
@@ -708,7 +733,7 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   mark(5);
   // (e) GEMM-dW -> fp32 dW rows (compact active order)
   launch_pdl_cluster(k_gemm3<kDW3>, kNumSMs, 384, smem_bytes3<kDW3>(), stream, 2u, f->mDW_Ah,
-                     f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, ga);
+                     f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce (+ one-hot correction) -> reduce-scatter
@@ -717,7 +742,7 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ga.nbt = nbp;
   ga.splits = dx_splits;
   launch_pdl_cluster(k_gemm3<kDX3>, kNumSMs, 384, smem_bytes3<kDX3>(), stream, 2u, f->mDX_Ah,
-                     f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, ga);
+                     f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
   XK_LAUNCH();
   mark(7);
   XK_CUDA(launch_dx_reduce(f->partial_dx, rowred, (uint32_t)B, nbp, dx_splits, cfg.scale,
@@ -732,7 +757,8 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   }
   // (g) normalize-backward + momentum SGD on the active rows, with the one-hot correction
   mark(8);
-  LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B)};
+  LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B),
+              f->dw_part, (uint32_t)kNumSMs / 2};
   XK_CUDA(launch_update_rows(W, V, f->dW32, active, &st->active_count, mw_cap, begin, D, wnorm,
                              lr_dev, cfg.momentum, cfg.weight_decay, err, stream, 148u * 16u, lf));
   ++launches;

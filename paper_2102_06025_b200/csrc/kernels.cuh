@@ -14,7 +14,26 @@ struct LabelFix {
   const float* X = nullptr;      // gathered raw features (B x D)
   const float* xnorm = nullptr;  // their norms
   float sb = 0.f;                // s / B
+  // GEMM-dW tail split (dw_split): the rows of the last, partial wave of 256-class units arrive
+  // as dw_split().s fp32 K-partials [slot][256][D] instead of dW rows; nullptr: none
+  const float* dw_part = nullptr;
+  uint32_t npairs = 0;
 };
+
+// GEMM-dW units are 256 active classes with the whole batch as K; their count rarely fills the
+// 74 CTA pairs in whole waves (C2: 391 units = 5.28 waves).  The `tail` units of the last wave
+// are split along K into s parts (s * tail <= npairs, s <= 4), each writing an fp32 partial that
+// the row update sums in part order; `full` units run whole.
+struct DwSplit {
+  uint32_t full, s;
+};
+__host__ __device__ __forceinline__ DwSplit dw_split(uint32_t units, uint32_t npairs) {
+  const uint32_t tail = units % npairs;
+  uint32_t s = tail ? npairs / tail : 1;
+  s = s > 4 ? 4 : (s < 1 ? 1 : s);
+  if (s == 1) return {units, 1};
+  return {units - tail, s};
+}
 cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,

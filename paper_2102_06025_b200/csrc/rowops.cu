@@ -121,7 +121,7 @@ __device__ __forceinline__ float4 load_g4(const __nv_bfloat16* __restrict__ G, u
 #ifndef XKNN_UPD_MINB
 #define XKNN_UPD_MINB 2
 #endif
-template <int DV, typename GT = float>
+template <int DV, typename GT = float, bool SPLIT = false>
 __global__ void __launch_bounds__(256, XKNN_UPD_MINB)
     k_update_rows(float* __restrict__ W, float* __restrict__ V,
                               const GT* __restrict__ G, const uint32_t* __restrict__ active,
@@ -154,10 +154,37 @@ __global__ void __launch_bounds__(256, XKNN_UPD_MINB)
     double dot = 0.0;
     // every load of the row in flight before the first use (W, G, V: 3 x 2 KiB per warp)
 #pragma unroll
+    // a row of a split GEMM-dW tail unit: the sum of its fp32 K-partials, in part order
+    const uint32_t unit = (uint32_t)(t / 256);
+    bool split = false;
+    DwSplit sp{0, 1};
+    if (SPLIT) {
+      sp = dw_split((uint32_t)((nrows + 255) / 256), lf.npairs);
+      split = unit >= sp.full;
+    }
+#pragma unroll
     for (int c = 0; c < DV; ++c) {
       w[c] = wp[lane + 32 * c];
-      g[c] = load_g4(G, g0 + lane + 32 * c);
+      if (!split) g[c] = load_g4(G, g0 + lane + 32 * c);
       vel[c] = vp[lane + 32 * c];
+    }
+    if (split) {
+      const uint64_t slot0 = (uint64_t)(unit - sp.full) * sp.s;
+      const float4* pp = reinterpret_cast<const float4*>(lf.dw_part) +
+                         ((slot0 * 256 + t % 256) * (uint64_t)d) / 4;
+#pragma unroll
+      for (int c = 0; c < DV; ++c) g[c] = pp[lane + 32 * c];
+      for (uint32_t q = 1; q < sp.s; ++q) {
+        const float4* pq = pp + (uint64_t)q * 256 * d / 4;
+#pragma unroll
+        for (int c = 0; c < DV; ++c) {
+          const float4 y = pq[lane + 32 * c];
+          g[c].x = __fadd_rn(g[c].x, y.x);
+          g[c].y = __fadd_rn(g[c].y, y.y);
+          g[c].z = __fadd_rn(g[c].z, y.z);
+          g[c].w = __fadd_rn(g[c].w, y.w);
+        }
+      }
     }
     if (lh >= 0) {
       float4 xs[DV];
@@ -323,6 +350,12 @@ cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_
                                const unsigned long long* err, cudaStream_t s, unsigned max_grid,
                                LabelFix lf) {
   const unsigned grid = grid_for(max_rows * 32, 256, max_grid);
+  if (lf.dw_part) {  // rows of split GEMM-dW tail units arrive as K-partials (FP32 path, D = 512)
+    if (d != 512) return cudaErrorInvalidValue;
+    launch_pdl(k_update_rows<4, float, true>, grid, 256, 0, s, W, V, G, active, count, begin, d,
+               wnorm, lr, mu, wd, err, lf);
+    return cudaGetLastError();
+  }
   XKNN_DISPATCH_D(d, k_update_rows, grid, 256, s, W, V, G, active, count, begin, d, wnorm, lr, mu,
                   wd, err, lf);
   return cudaGetLastError();
