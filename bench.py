@@ -443,6 +443,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
             ev_copied[s_].record(copy_stream)
 
     barrier()
+    clk_e2e = ClockSampler(local_rank)
+    clk_e2e.__enter__()
     t0 = time.perf_counter()
     copy_in(0)
     for j in range(e2e_steps):
@@ -460,6 +462,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
     e2e_enqueue_ms = (time.perf_counter() - t0) * 1e3  # host time to issue every step
     stream.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3
+    clk_e2e.__exit__(None, None, None)
     barrier()
     layer.sync()
     assert np.isfinite(hloss.numpy()).all()
@@ -541,7 +544,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
                     "how": "host wall clock over a pipelined loop: per step H2D of the rank's "
                            "features+labels from pinned memory on a copy stream, the next step's "
                            "selection prepared as soon as its labels land, the step, D2H of its "
-                           "loss"},
+                           "loss",
+                    "clocks": clk_e2e.summary()},
             "gpu_launches": int(launches),
             "roofline": roof,
             "kernels": kern,
