@@ -38,7 +38,11 @@ namespace xknn {
 
 namespace {
 
-enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2 };
+enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2, kDXb = 3, kDWb = 4 };
+template <int KIND>
+constexpr bool kIsDX = KIND == kDX3 || KIND == kDXb;
+template <int KIND>
+constexpr bool kIsDW = KIND == kDW3 || KIND == kDWb;
 
 // Instruction descriptor, kind::tf32: TF32 A/B (format 2), fp32 D.
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t m, uint32_t n, bool a_mn, bool b_mn) {
@@ -71,6 +75,8 @@ struct Gemm3Args {
   const int32_t* label_col;
   float* p_hi;  // P~ [bpad][ldp] fp32 hi / lo (GEMM-F output)
   float* p_lo;
+  __nv_bfloat16* pb_hi;  // ... or its two bf16 planes (bf16x3 backward GEMMs)
+  __nv_bfloat16* pb_lo;
   uint64_t ldp;
   float* partial;    // F: [2 * class tiles][bpad] row sums; dX: split-K partial rows
   float* labelterm;  // F: [bpad]
@@ -100,7 +106,40 @@ struct Cfg3<kDW3> {
   static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 4 * 2048, B_BYTES = 2 * 8 * 2048;
   static constexpr uint32_t NBUF = 1, ACC = 512, KB = 16;
 };
+// bf16x3 backward GEMMs: P~, W_sub and X_hat' as two bf16 planes (hi = bf16(a), lo = bf16(a - hi),
+// 16-17 significant bits) and a*b ~ lo*hi + hi*lo + hi*hi in kind::f16 -- the same three MMAs per
+// product as 3xTF32 at twice the tensor-core rate, on the BF16 path's layouts (fast.cu) with 32
+// K per stage.  KC = 32: A = 128 rows x 32 (dX: K-major, 64-B rows, SW64; dW: 2 MN-major atoms of
+// 64 classes), B = 4 MN-major atoms of 64 d x 32 rows (SW128); hi | lo planes side by side.
+template <>
+struct Cfg3<kDXb> {
+  static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 128 * 32 * 2, B_BYTES = 2 * 4 * 4096;
+  static constexpr uint32_t NBUF = 1, ACC = 512, KB = 32;
+};
+template <>
+struct Cfg3<kDWb> {
+  static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 2 * 4096, B_BYTES = 2 * 4 * 4096;
+  static constexpr uint32_t NBUF = 1, ACC = 512, KB = 32;
+};
 constexpr uint32_t kStg3 = 4096;  // per epilogue warp: one 32 x 32 fp32 staging block
+#ifndef XKNN_PCONV
+#define XKNN_PCONV 1
+#endif
+#ifndef XKNN_PCONV_TRUNC
+#define XKNN_PCONV_TRUNC 0
+#endif
+#ifndef XKNN_PCONV_GROUPS
+#define XKNN_PCONV_GROUPS 4
+#endif
+constexpr uint32_t kCvtGroups = XKNN_PCONV_GROUPS;
+static_assert(4 % kCvtGroups == 0, "a converter group must own whole stages of the 4-stage ring");
+// GEMM-dW / GEMM-dX read P~ as one fp32 array and split it hi/lo in shared memory (the epilogue
+// warps, idle during the main loop, convert each stage before the MMA reads it) instead of
+// reading HBM-resident hi and lo copies: P~ is written once (4 B per element, not 8) and each
+// consumer reads half the bytes.  The split is the same round-to-nearest one, so the results are
+// bit-identical.
+template <int KIND>
+constexpr bool kConv3 = XKNN_PCONV && (KIND == kDX3 || KIND == kDW3);
 
 template <int KIND>
 constexpr uint32_t smem_bytes3() {
@@ -118,7 +157,7 @@ struct Unit3 {
 
 template <int KIND>
 __device__ __forceinline__ uint32_t num_units3(const Gemm3Args& a, uint32_t mw) {
-  if (KIND == kDW3) {
+  if (kIsDW<KIND>) {
     const uint32_t units = (mw + 255) / 256;
     const DwSplit sp = dw_split(units, gridDim.x / 2);
     return sp.full + (units - sp.full) * sp.s;
@@ -130,8 +169,8 @@ template <int KIND>
 __device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint32_t u) {
   Unit3 x{};
   x.id = u;
-  if (KIND == kDW3) {
-    const uint32_t nk = a.bpad / Cfg3<kDW3>::KB;
+  if (kIsDW<KIND>) {
+    const uint32_t nk = a.bpad / Cfg3<KIND>::KB;
     const DwSplit sp = dw_split((mw + 255) / 256, gridDim.x / 2);
     x.valid = true;
     if (u < sp.full) {
@@ -149,11 +188,11 @@ __device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint3
     return x;
   }
   const uint32_t bp = u % a.nbt, r = u / a.nbt;
-  const uint32_t nt = KIND == kF3 ? (mw + 255) / 256 : (mw + 15) / 16;
+  const uint32_t nt = KIND == kF3 ? (mw + 255) / 256 : (mw + Cfg3<KIND>::KB - 1) / Cfg3<KIND>::KB;
   x.row0 = bp * 256;
   x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
   x.t1 = (uint32_t)((uint64_t)(r + 1) * nt / a.splits);
-  x.valid = KIND == kDX3 || x.t1 > x.t0;  // dX units always write their (maybe zero) partial
+  x.valid = kIsDX<KIND> || x.t1 > x.t0;  // dX units always write their (maybe zero) partial
   return x;
 }
 
@@ -194,6 +233,45 @@ __device__ __forceinline__ void store_f32_block(const uint8_t* buf, float* dst, 
   __syncwarp();
 }
 
+// bf16 planes of a pair of values: hi = bf16(v), lo = bf16(v - hi) (v - hi is exact)
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// one thread's 32 values as bf16 hi / lo planes into two 32 x 64 B staging blocks (buf, buf +
+// 2 KB), 16-B unit c of row r at c ^ ((r >> 1) & 3) (conflict-free both ways)
+__device__ __forceinline__ void stage_bf16_planes(uint8_t* buf, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c) {
+    uint4 h, l;
+    split_bf16x2(v[8 * c + 0], v[8 * c + 1], h.x, l.x);
+    split_bf16x2(v[8 * c + 2], v[8 * c + 3], h.y, l.y);
+    split_bf16x2(v[8 * c + 4], v[8 * c + 5], h.z, l.z);
+    split_bf16x2(v[8 * c + 6], v[8 * c + 7], h.w, l.w);
+    const uint32_t off = r * 64 + ((c ^ ((r >> 1) & 3)) * 16);
+    *reinterpret_cast<uint4*>(buf + off) = h;
+    *reinterpret_cast<uint4*>(buf + 2048 + off) = l;
+  }
+}
+// ... and both blocks to global rows `ld` elements apart: lane l writes row 8i + l/4, 16-B unit
+// l%4 (eight full 64-B row segments per instruction and plane)
+__device__ __forceinline__ void store_bf16_planes(const uint8_t* buf, __nv_bfloat16* dhi,
+                                                  __nv_bfloat16* dlo, uint64_t ld, uint32_t lane) {
+  const uint32_t c = lane & 3;
+#pragma unroll
+  for (uint32_t i = 0; i < 4; ++i) {
+    const uint32_t r = 8 * i + (lane >> 2), off = r * 64 + ((c ^ ((r >> 1) & 3)) * 16);
+    *reinterpret_cast<uint4*>(dhi + (uint64_t)r * ld + c * 8) =
+        *reinterpret_cast<const uint4*>(buf + off);
+    *reinterpret_cast<uint4*>(dlo + (uint64_t)r * ld + c * 8) =
+        *reinterpret_cast<const uint4*>(buf + 2048 + off);
+  }
+  __syncwarp();
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(384, 1)
     k_gemm3(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
@@ -211,7 +289,11 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* lfull = tempty + 2;          // kConv3: this CTA's stage bytes landed (local TMA)
+  uint64_t* conv = lfull + C::STAGES;    // kConv3 (leader): both CTAs' A stage split hi/lo
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + C::STAGES);
+  constexpr bool CONV = kConv3<KIND>;
+  constexpr bool BF = KIND == kDXb || KIND == kDWb;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = tc::cluster_ctarank() & 1;
@@ -222,6 +304,8 @@ __global__ void __launch_bounds__(384, 1)
     for (uint32_t s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&lfull[s], 1);
+      tc::mbar_init(&conv[s], 2 * (8 / kCvtGroups));  // one group's warps in each CTA
     }
     for (uint32_t s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
@@ -256,7 +340,17 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t nk = KIND == kF3 ? (x.t1 - x.t0) * (512 / C::KB) : x.t1 - x.t0;
         for (uint32_t k = 0; k < nk; ++k) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          if (CONV)  // this CTA's fp32 A (the hi half of the A stage) and hi/lo B
+            tc::mbar_expect_tx(&lfull[stage], C::A_BYTES / 2 + C::B_BYTES);
+          else if (leader)
+            tc::mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          // CONV: loads complete on this CTA's own barrier (the converters wait on it)
+          auto load = [&](void* dst, const CUtensorMap* m, int32_t c0, int32_t c1) {
+            if (CONV)
+              tc::tma_load_2d(dst, m, &lfull[stage], c0, c1);
+            else
+              tc::tma_load_2d_2sm(dst, m, &full[stage], c0, c1);
+          };
           uint8_t* dA = sA + stage * C::A_BYTES;
           uint8_t* dB = sB + stage * C::B_BYTES;
           if (KIND == kF3) {
@@ -267,17 +361,37 @@ __global__ void __launch_bounds__(384, 1)
             tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
             tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
             tc::tma_load_2d_2sm(dB + C::B_BYTES / 2, &tmBlo, &full[stage], kc, crow);
+          } else if (BF) {
+            const int32_t kk = (int32_t)((x.t0 + k) * 32);
+            if (kIsDX<KIND>) {  // P~ planes [b][class]: this CTA's 128 batch rows, 32 classes
+              load(dA, &tmAhi, kk, myrow);
+              load(dA + C::A_BYTES / 2, &tmAlo, kk, myrow);
+            } else {  // P~ᵀ planes: this CTA's 128 classes (2 atoms of 64) at batch rows kk..+31
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                load(dA + j * 4096, &tmAhi, myrow + 64 * j, kk);
+                load(dA + C::A_BYTES / 2 + j * 4096, &tmAlo, myrow + 64 * j, kk);
+              }
+            }
+            // B planes [K rows][512 d]: this CTA's 128 d of each 256-wide N instruction j
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int32_t dc = (int32_t)(256 * j + 128 * cta + 64 * h);
+                load(dB + (j * 2 + h) * 4096, &tmBhi, dc, kk);
+                load(dB + C::B_BYTES / 2 + (j * 2 + h) * 4096, &tmBlo, dc, kk);
+              }
           } else {
             const int32_t kk = (int32_t)((x.t0 + k) * 16);
             if (KIND == kDX3) {  // P~ [b][class]: this CTA's 128 batch rows, 16 classes
-              tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kk, myrow);
-              tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kk, myrow);
+              load(dA, &tmAhi, kk, myrow);
+              if (!CONV) load(dA + C::A_BYTES / 2, &tmAlo, kk, myrow);
             } else {  // P~ᵀ: this CTA's 128 classes (4 atoms of 32) at batch rows kk..kk+15
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
-                tc::tma_load_2d_2sm(dA + t * 2048, &tmAhi, &full[stage], myrow + 32 * t, kk);
-                tc::tma_load_2d_2sm(dA + C::A_BYTES / 2 + t * 2048, &tmAlo, &full[stage],
-                                    myrow + 32 * t, kk);
+                load(dA + t * 2048, &tmAhi, myrow + 32 * t, kk);
+                if (!CONV) load(dA + C::A_BYTES / 2 + t * 2048, &tmAlo, myrow + 32 * t, kk);
               }
             }
             // B [K rows][512 d]: this CTA's 128 d of each 256-wide N instruction j, 4 atoms
@@ -286,9 +400,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
                 const int32_t dc = (int32_t)(256 * j + 128 * cta + 32 * t);
-                tc::tma_load_2d_2sm(dB + (j * 4 + t) * 2048, &tmBhi, &full[stage], dc, kk);
-                tc::tma_load_2d_2sm(dB + C::B_BYTES / 2 + (j * 4 + t) * 2048, &tmBlo,
-                                    &full[stage], dc, kk);
+                load(dB + (j * 4 + t) * 2048, &tmBhi, dc, kk);
+                load(dB + C::B_BYTES / 2 + (j * 4 + t) * 2048, &tmBlo, dc, kk);
               }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -309,7 +422,10 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t dcol = tbase + buf * C::ACC;
           const uint32_t nk = KIND == kF3 ? 512 / C::KB : x.t1 - x.t0;
           for (uint32_t k = 0; k < nk; ++k) {
-            tc::mbar_wait(&full[stage], phase);
+            if (CONV)
+              tc::mbar_wait_cluster(&conv[stage], phase);
+            else
+              tc::mbar_wait(&full[stage], phase);
             tc::fence_after_sync();
             const uint32_t ah = tc::smem_u32(sA + stage * C::A_BYTES), al = ah + C::A_BYTES / 2;
             const uint32_t bh = tc::smem_u32(sB + stage * C::B_BYTES), bl = bh + C::B_BYTES / 2;
@@ -326,6 +442,27 @@ __global__ void __launch_bounds__(384, 1)
                 mma_tf32_2sm(dcol, dal, dbh, id, (k | kk) != 0);  // small terms first
                 mma_tf32_2sm(dcol, dah, dbl, id, 1u);
                 mma_tf32_2sm(dcol, dah, dbh, id, 1u);
+              }
+            } else if (BF) {
+              constexpr uint32_t id = tc::idesc_bf16(256, 256, kIsDW<KIND>, true);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 2; ++kk) {  // K = 16 per instruction
+                const uint64_t dah =
+                    kIsDX<KIND> ? tc::smem_desc(ah + kk * 32, 16, 512, tc::kSwizzle64)
+                                : tc::smem_desc(ah + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                const uint64_t dal =
+                    kIsDX<KIND> ? tc::smem_desc(al + kk * 32, 16, 512, tc::kSwizzle64)
+                                : tc::smem_desc(al + kk * 2048, 4096, 1024, tc::kSwizzle128);
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                  const uint64_t dbh =
+                      tc::smem_desc(bh + j * 8192 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                  const uint64_t dbl =
+                      tc::smem_desc(bl + j * 8192 + kk * 2048, 4096, 1024, tc::kSwizzle128);
+                  tc::mma_bf16_2sm(dcol + j * 256, dal, dbh, id, (k | kk) != 0);
+                  tc::mma_bf16_2sm(dcol + j * 256, dah, dbl, id, 1u);
+                  tc::mma_bf16_2sm(dcol + j * 256, dah, dbh, id, 1u);
+                }
               }
             } else {
               constexpr uint32_t id = idesc_tf32(256, 256, KIND == kDW3, true);
@@ -369,9 +506,52 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_addr = (q * 32) << 16;
     uint8_t* stg = sStg + ew * kStg3;
     uint32_t buf = 0, tphase = 0;
+    // CONV: the A stages in MMA order, split hi/lo in place: hi = tf32(x) over x, lo = x - hi
+    // into the stage's second half (both halves keep the TMA swizzle, the split is elementwise)
+    // The warps form kCvtGroups groups that take the stages in turn, so that one stage's
+    // wait -> split -> proxy fence -> arrive chain overlaps the next stage's.
+    constexpr uint32_t NG = kCvtGroups, GT = 256 / NG;  // groups, threads per group
+    const uint32_t grp = ew / (8 / NG), et = (ew % (8 / NG)) * 32 + lane;
+    uint32_t cdone = 0, cend = 0;
+    auto convert_to = [&](uint32_t target) {
+      for (; cdone < target; ++cdone) {
+        if (cdone % NG != grp) continue;
+        const uint32_t cstage = cdone % C::STAGES, cphase = (cdone / C::STAGES) & 1;
+        tc::mbar_wait(&lfull[cstage], cphase);
+        float4* ph = reinterpret_cast<float4*>(sA + cstage * C::A_BYTES);
+        float4* pl = reinterpret_cast<float4*>(sA + cstage * C::A_BYTES + C::A_BYTES / 2);
+#pragma unroll
+        for (uint32_t i = 0; i < C::A_BYTES / 2 / 16 / GT; ++i) {
+          const float4 v = ph[et + GT * i];
+#if XKNN_PCONV_TRUNC
+          auto tr = [](float f) { return __uint_as_float(__float_as_uint(f) & 0xffffe000u); };
+          const float4 hi = make_float4(tr(v.x), tr(v.y), tr(v.z), tr(v.w));
+#else
+          const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+          ph[et + GT * i] = hi;
+#endif
+          pl[et + GT * i] = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        }
+        tc::fence_proxy_async_smem();  // generic-proxy writes -> the tensor core's reads
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_remote(&conv[cstage], 0);
+      }
+    };
     for (uint32_t u = pair; u < nunits; u += npairs) {
       const Unit3 x = unit3_of<KIND>(a, mw, u);
       if (!x.valid) continue;
+      if (CONV) {
+        // this unit's stages, then the next unit's first ones (already loadable: the MMA has
+        // released every stage once this unit's last one is converted), so that its MMA can
+        // start as soon as the accumulator below is drained
+        cend += x.t1 - x.t0;
+        uint32_t pre = 0;
+        if (u + npairs < nunits) {
+          const Unit3 y = unit3_of<KIND>(a, mw, u + npairs);
+          pre = min(C::STAGES, y.t1 - y.t0);
+        }
+        convert_to(cend + pre);
+      }
       const uint32_t ntile = KIND == kF3 ? x.t1 - x.t0 : 1;
       for (uint32_t t = 0; t < ntile; ++t) {
         tc::mbar_wait(&tfull[buf], tphase);
@@ -404,12 +584,22 @@ __global__ void __launch_bounds__(384, 1)
               has = true;
             }
             const uint64_t off = (uint64_t)grow0 * a.ldp + c0;
-            stage_split<false>(stg, lane, e);
-            __syncwarp();
-            store_f32_block(stg, a.p_hi + off, a.ldp, lane);
-            stage_split<true>(stg, lane, e);
-            __syncwarp();
-            store_f32_block(stg, a.p_lo + off, a.ldp, lane);
+            if (a.pb_hi) {  // bf16 hi / lo planes for the bf16x3 backward GEMMs
+              stage_bf16_planes(stg, lane, e);
+              __syncwarp();
+              store_bf16_planes(stg, a.pb_hi + off, a.pb_lo + off, a.ldp, lane);
+            } else if (XKNN_PCONV) {  // one fp32 P~: its consumers split it in shared memory
+              stage_f32(stg, lane, e);
+              __syncwarp();
+              store_f32_block(stg, a.p_hi + off, a.ldp, lane);
+            } else {
+              stage_split<false>(stg, lane, e);
+              __syncwarp();
+              store_f32_block(stg, a.p_hi + off, a.ldp, lane);
+              stage_split<true>(stg, lane, e);
+              __syncwarp();
+              store_f32_block(stg, a.p_lo + off, a.ldp, lane);
+            }
           };
           uint32_t ra[32], rb[32];
           tc::tmem_ld32_issue(tb + h * 128, ra);
@@ -432,10 +622,10 @@ __global__ void __launch_bounds__(384, 1)
         } else {
           // dX: split-K partial rows of unit x.id; dW: fp32 dW rows (compact active order), or
           // the K-partial rows of a split tail unit (slot x.id, through tmOut2)
-          const bool part = KIND == kDW3 && x.part;
-          const int32_t orow = (KIND == kDX3 || part) ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0
+          const bool part = kIsDW<KIND> && x.part;
+          const int32_t orow = (kIsDX<KIND> || part) ? (int32_t)(x.id * 256) + grow0 - (int32_t)x.row0
                                                       : grow0;
-          const bool zero = KIND == kDX3 && x.t1 == x.t0;
+          const bool zero = kIsDX<KIND> && x.t1 == x.t0;
 #pragma unroll 1
           for (uint32_t ch = 0; ch < 8; ++ch) {
             const uint32_t col = h * 256 + ch * 32;
@@ -481,8 +671,9 @@ __global__ void k_fixup32(const double* __restrict__ red, const int32_t* __restr
                           const float* __restrict__ X, const float* __restrict__ xnorm, uint32_t B,
                           uint32_t bpad, float scale, int32_t* __restrict__ lab_head,
                           int32_t* __restrict__ lab_next, float* __restrict__ xs_hi,
-                          float* __restrict__ xs_lo, double* __restrict__ loss, SelState* st,
-                          unsigned long long* err) {
+                          float* __restrict__ xs_lo, __nv_bfloat16* __restrict__ xsb_hi,
+                          __nv_bfloat16* __restrict__ xsb_lo, double* __restrict__ loss,
+                          SelState* st, unsigned long long* err) {
   griddep_wait();
   griddep_launch();
   if (blockIdx.x == 0) {
@@ -508,11 +699,18 @@ __global__ void k_fixup32(const double* __restrict__ red, const int32_t* __restr
        b += (gridDim.x * blockDim.x) >> 5) {
     float4* dh = reinterpret_cast<float4*>(xs_hi + (uint64_t)b * 512);
     float4* dl = reinterpret_cast<float4*>(xs_lo + (uint64_t)b * 512);
+    uint2* bh = reinterpret_cast<uint2*>(xsb_hi + (uint64_t)b * 512);
+    uint2* bl = reinterpret_cast<uint2*>(xsb_lo + (uint64_t)b * 512);
     if (b >= B) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        dh[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dl[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (xsb_hi) {
+          bh[lane + 32 * c] = make_uint2(0u, 0u);
+          bl[lane + 32 * c] = make_uint2(0u, 0u);
+        } else {
+          dh[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          dl[lane + 32 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       continue;
     }
@@ -526,6 +724,14 @@ __global__ void k_fixup32(const double* __restrict__ red, const int32_t* __restr
       const float4 x = xp[lane + 32 * c];
       const float4 v = make_float4(__fmul_rn(__fmul_rn(x.x, inv), rs), __fmul_rn(__fmul_rn(x.y, inv), rs),
                                    __fmul_rn(__fmul_rn(x.z, inv), rs), __fmul_rn(__fmul_rn(x.w, inv), rs));
+      if (xsb_hi) {  // bf16 planes (bf16x3 GEMM-dW)
+        uint2 h, l;
+        split_bf16x2(v.x, v.y, h.x, l.x);
+        split_bf16x2(v.z, v.w, h.y, l.y);
+        bh[lane + 32 * c] = h;
+        bl[lane + 32 * c] = l;
+        continue;
+      }
       const float4 hi = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
       dh[lane + 32 * c] = hi;
       dl[lane + 32 * c] = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
@@ -534,7 +740,8 @@ __global__ void k_fixup32(const double* __restrict__ red, const int32_t* __restr
 }
 
 // rows [count, round_up(count, 256)) of W_sub hi/lo must be zero for GEMM-dX's K loop
-__global__ void k_zero_rows32(const SelState* st, float* whi, float* wlo, uint32_t cap_rows) {
+__global__ void k_zero_rows32(const SelState* st, float* whi, float* wlo, __nv_bfloat16* wbh,
+                              __nv_bfloat16* wbl, uint32_t cap_rows) {
   griddep_wait();
   griddep_launch();
   const uint32_t c = st->active_count;
@@ -542,10 +749,16 @@ __global__ void k_zero_rows32(const SelState* st, float* whi, float* wlo, uint32
   const uint64_t n = (uint64_t)(e - c) * 512 / 4;
   float4* ph = reinterpret_cast<float4*>(whi + (uint64_t)c * 512);
   float4* pl = reinterpret_cast<float4*>(wlo + (uint64_t)c * 512);
+  uint2* bh = wbh ? reinterpret_cast<uint2*>(wbh + (uint64_t)c * 512) : nullptr;
+  uint2* bl = wbh ? reinterpret_cast<uint2*>(wbl + (uint64_t)c * 512) : nullptr;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     ph[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     pl[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bh) {
+      bh[i] = make_uint2(0u, 0u);
+      bl[i] = make_uint2(0u, 0u);
+    }
   }
 }
 
@@ -562,18 +775,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn3() {
   return fn;
 }
 
-// fp32 row-major [outer][inner] tensor, box_inner x box_outer
+// fp32 (or bf16) row-major [outer][inner] tensor, box_inner x box_outer
 bool make_map32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+                uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw, bool bf16 = false) {
   auto fn = encode_fn3();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 4};
+  cuuint64_t strides[1] = {inner * (bf16 ? 2 : 4)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+            const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -584,7 +797,7 @@ struct Fast32State {
   float *xh_hi = nullptr, *xh_lo = nullptr;  // X_hat hi/lo [bpad][512]
   float *xs_hi = nullptr, *xs_lo = nullptr;  // X_hat' hi/lo [bpad][512]
   float *w_hi = nullptr, *w_lo = nullptr;    // W_sub hi/lo [mwpad][512]
-  float *p_hi = nullptr, *p_lo = nullptr;    // P~ hi/lo [bpad][mwpad]
+  float *p_hi = nullptr, *p_lo = nullptr;    // P~ [bpad][mwpad] (fp32; hi/lo if !XKNN_PCONV)
   float* partial_f = nullptr;                // [2 * mwpad/256][bpad]
   float* labelterm = nullptr;                // [bpad]
   float* partial_dx = nullptr;               // [units][256][512]
@@ -596,6 +809,12 @@ struct Fast32State {
   CUtensorMap mDX_Ah, mDX_Al, mDX_Bh, mDX_Bl, mDX_st;  // P~ (16 x 128, SW64), W_sub (32 x 16)
   CUtensorMap mDW_Ah, mDW_Al, mDW_Bh, mDW_Bl, mDW_st;  // P~ (32 x 16), X_hat' (32 x 16)
   CUtensorMap mDWP_st;                                 // dW tail-unit K-partials
+  // bf16x3 backward GEMMs (default; XKNN_FP32_BWD=tf32 selects 3xTF32 for them too): the bf16
+  // planes of P~, W_sub and X_hat' replace P~ fp32 and X_hat' hi/lo as their operands
+  bool bfb = true;
+  __nv_bfloat16 *pb_hi = nullptr, *pb_lo = nullptr;    // P~ [bpad][mwpad]
+  __nv_bfloat16 *wb_hi = nullptr, *wb_lo = nullptr;    // W_sub [mwpad][512]
+  __nv_bfloat16 *xsb_hi = nullptr, *xsb_lo = nullptr;  // X_hat' [bpad][512]
 };
 
 xknn_status_t Layer::init_fast32() {
@@ -605,6 +824,7 @@ xknn_status_t Layer::init_fast32() {
   f->bpad = (uint32_t)((bmax + 255) / 256 * 256);
   f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
   ldp = f->mwpad;
+  if (const char* e = getenv("XKNN_FP32_BWD")) f->bfb = strcmp(e, "tf32") != 0;
   const uint64_t xb = (uint64_t)f->bpad * 512, wb = (uint64_t)f->mwpad * 512,
                  pb = (uint64_t)f->bpad * f->mwpad;
   for (float** p : {&f->xh_hi, &f->xh_lo, &f->xs_hi, &f->xs_lo}) {
@@ -615,9 +835,25 @@ xknn_status_t Layer::init_fast32() {
     XK_CUDA(dalloc(p, wb));
     XK_CUDA(cudaMemsetAsync(*p, 0, wb * 4, stream));
   }
-  for (float** p : {&f->p_hi, &f->p_lo}) {
-    XK_CUDA(dalloc(p, pb));
-    XK_CUDA(cudaMemsetAsync(*p, 0, pb * 4, stream));
+  if (f->bfb) {
+    for (auto* p : {&f->pb_hi, &f->pb_lo}) {
+      XK_CUDA(dalloc(p, pb));
+      XK_CUDA(cudaMemsetAsync(*p, 0, pb * 2, stream));
+    }
+    for (auto* p : {&f->wb_hi, &f->wb_lo}) {
+      XK_CUDA(dalloc(p, wb));
+      XK_CUDA(cudaMemsetAsync(*p, 0, wb * 2, stream));
+    }
+    for (auto* p : {&f->xsb_hi, &f->xsb_lo}) {
+      XK_CUDA(dalloc(p, xb));
+      XK_CUDA(cudaMemsetAsync(*p, 0, xb * 2, stream));
+    }
+  } else {
+    for (float** p : {&f->p_hi, &f->p_lo}) {
+      if (XKNN_PCONV && p == &f->p_lo) continue;
+      XK_CUDA(dalloc(p, pb));
+      XK_CUDA(cudaMemsetAsync(*p, 0, pb * 4, stream));
+    }
   }
   XK_CUDA(dalloc(&f->partial_f, (uint64_t)2 * (f->mwpad / 256) * f->bpad));
   XK_CUDA(dalloc(&f->labelterm, f->bpad));
@@ -638,15 +874,27 @@ xknn_status_t Layer::init_fast32() {
   ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, FKB, 128, SF);
   ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, FKB, 128, SF);
   ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, FKB, 128, SF);
-  ok &= make_map32(&f->mDX_Ah, f->p_hi, f->mwpad, f->bpad, 16, 128, S64);
-  ok &= make_map32(&f->mDX_Al, f->p_lo, f->mwpad, f->bpad, 16, 128, S64);
-  ok &= make_map32(&f->mDX_Bh, f->w_hi, 512, f->mwpad, 32, 16, S32G);
-  ok &= make_map32(&f->mDX_Bl, f->w_lo, 512, f->mwpad, 32, 16, S32G);
+  if (f->bfb) {  // bf16 planes in the BF16 path's layouts (fast.cu), 32 K per stage
+    ok &= make_map32(&f->mDX_Ah, f->pb_hi, f->mwpad, f->bpad, 32, 128, S64, true);
+    ok &= make_map32(&f->mDX_Al, f->pb_lo, f->mwpad, f->bpad, 32, 128, S64, true);
+    ok &= make_map32(&f->mDX_Bh, f->wb_hi, 512, f->mwpad, 64, 32, S128, true);
+    ok &= make_map32(&f->mDX_Bl, f->wb_lo, 512, f->mwpad, 64, 32, S128, true);
+    ok &= make_map32(&f->mDW_Ah, f->pb_hi, f->mwpad, f->bpad, 64, 32, S128, true);
+    ok &= make_map32(&f->mDW_Al, f->pb_lo, f->mwpad, f->bpad, 64, 32, S128, true);
+    ok &= make_map32(&f->mDW_Bh, f->xsb_hi, 512, f->bpad, 64, 32, S128, true);
+    ok &= make_map32(&f->mDW_Bl, f->xsb_lo, 512, f->bpad, 64, 32, S128, true);
+  } else {
+    ok &= make_map32(&f->mDX_Ah, f->p_hi, f->mwpad, f->bpad, 16, 128, S64);
+    float* plo = XKNN_PCONV ? f->p_hi : f->p_lo;  // (unused when the consumers split P~)
+    ok &= make_map32(&f->mDX_Al, plo, f->mwpad, f->bpad, 16, 128, S64);
+    ok &= make_map32(&f->mDX_Bh, f->w_hi, 512, f->mwpad, 32, 16, S32G);
+    ok &= make_map32(&f->mDX_Bl, f->w_lo, 512, f->mwpad, 32, 16, S32G);
+    ok &= make_map32(&f->mDW_Ah, f->p_hi, f->mwpad, f->bpad, 32, 16, S32G);
+    ok &= make_map32(&f->mDW_Al, plo, f->mwpad, f->bpad, 32, 16, S32G);
+    ok &= make_map32(&f->mDW_Bh, f->xs_hi, 512, f->bpad, 32, 16, S32G);
+    ok &= make_map32(&f->mDW_Bl, f->xs_lo, 512, f->bpad, 32, 16, S32G);
+  }
   ok &= make_map32(&f->mDX_st, f->partial_dx, 512, f->dx_units_cap, 32, 32, S128);
-  ok &= make_map32(&f->mDW_Ah, f->p_hi, f->mwpad, f->bpad, 32, 16, S32G);
-  ok &= make_map32(&f->mDW_Al, f->p_lo, f->mwpad, f->bpad, 32, 16, S32G);
-  ok &= make_map32(&f->mDW_Bh, f->xs_hi, 512, f->bpad, 32, 16, S32G);
-  ok &= make_map32(&f->mDW_Bl, f->xs_lo, 512, f->bpad, 32, 16, S32G);
   ok &= make_map32(&f->mDW_st, f->dW32, 512, f->mwpad, 32, 32, S128);
   ok &= make_map32(&f->mDWP_st, f->dw_part, 512, (uint64_t)kNumSMs / 2 * 256, 32, 32, S128);
   if (!ok) return fail_msg(XKNN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -656,6 +904,10 @@ xknn_status_t Layer::init_fast32() {
                                smem_bytes3<kDX3>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDW3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes3<kDW3>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDXb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kDXb>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDWb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kDWb>()));
   return XKNN_OK;
 }
 
@@ -665,8 +917,9 @@ void Layer::free_fast32() {
   for (void* p : {(void*)f->xh_hi, (void*)f->xh_lo, (void*)f->xs_hi, (void*)f->xs_lo,
                   (void*)f->w_hi, (void*)f->w_lo, (void*)f->p_hi, (void*)f->p_lo,
                   (void*)f->partial_f, (void*)f->labelterm, (void*)f->partial_dx, (void*)f->dW32,
-                  (void*)f->dw_part,
-                  (void*)f->lab_head, (void*)f->lab_next})
+                  (void*)f->dw_part, (void*)f->lab_head, (void*)f->lab_next, (void*)f->pb_hi,
+                  (void*)f->pb_lo, (void*)f->wb_hi, (void*)f->wb_lo, (void*)f->xsb_hi,
+                  (void*)f->xsb_lo})
     if (p) cudaFree(p);
   delete f;
   fast32 = nullptr;
@@ -685,10 +938,11 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   if (B > f->bpad) return XKNN_ERR_INVALID_ARGUMENT;
   // (a) operands: the active weight rows gathered + normalized, split hi/lo (feature all-gather
   //     runs under it at P > 1), then X_hat hi/lo
-  XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, f->w_hi, nullptr,
-                                wnorm, err, stream, false, f->w_lo));
+  XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, f->w_hi, f->wb_hi,
+                                wnorm, err, stream, false, f->w_lo, f->wb_lo));
   ++launches;
-  launch_pdl(k_zero_rows32, 64, 256, 0, stream, (const SelState*)st, f->w_hi, f->w_lo, f->mwpad);
+  launch_pdl(k_zero_rows32, 64, 256, 0, stream, (const SelState*)st, f->w_hi, f->w_lo, f->wb_hi,
+             f->wb_lo, f->mwpad);
   XK_LAUNCH();
   if (world > 1) XK_TRY(wait_features());
   XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, f->xh_hi, nullptr, xnorm, err,
@@ -703,6 +957,8 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ga.label_col = label_col;
   ga.p_hi = f->p_hi;
   ga.p_lo = f->p_lo;
+  ga.pb_hi = f->pb_hi;
+  ga.pb_lo = f->pb_lo;
   ga.ldp = ldp;
   ga.labelterm = f->labelterm;
   const uint32_t nbp = (uint32_t)((B + 255) / 256);
@@ -728,12 +984,17 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   }
   launch_pdl(k_fixup32, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, (const double*)rowred,
              (const int32_t*)label_col, (const float*)X, (const float*)xnorm, (uint32_t)B, f->bpad,
-             cfg.scale, f->lab_head, f->lab_next, f->xs_hi, f->xs_lo, loss_dev, st, err);
+             cfg.scale, f->lab_head, f->lab_next, f->xs_hi, f->xs_lo, f->xsb_hi, f->xsb_lo, loss_dev,
+             st, err);
   XK_LAUNCH();
   mark(5);
   // (e) GEMM-dW -> fp32 dW rows (compact active order)
-  launch_pdl_cluster(k_gemm3<kDW3>, kNumSMs, 384, smem_bytes3<kDW3>(), stream, 2u, f->mDW_Ah,
-                     f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
+  if (f->bfb)
+    launch_pdl_cluster(k_gemm3<kDWb>, kNumSMs, 384, smem_bytes3<kDWb>(), stream, 2u, f->mDW_Ah,
+                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
+  else
+    launch_pdl_cluster(k_gemm3<kDW3>, kNumSMs, 384, smem_bytes3<kDW3>(), stream, 2u, f->mDW_Ah,
+                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce (+ one-hot correction) -> reduce-scatter
@@ -741,8 +1002,12 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   const uint32_t dx_splits = gemm_pair_splits(nbp, 148);
   ga.nbt = nbp;
   ga.splits = dx_splits;
-  launch_pdl_cluster(k_gemm3<kDX3>, kNumSMs, 384, smem_bytes3<kDX3>(), stream, 2u, f->mDX_Ah,
-                     f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
+  if (f->bfb)
+    launch_pdl_cluster(k_gemm3<kDXb>, kNumSMs, 384, smem_bytes3<kDXb>(), stream, 2u, f->mDX_Ah,
+                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
+  else
+    launch_pdl_cluster(k_gemm3<kDX3>, kNumSMs, 384, smem_bytes3<kDX3>(), stream, 2u, f->mDX_Ah,
+                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
   XK_LAUNCH();
   mark(7);
   XK_CUDA(launch_dx_reduce(f->partial_dx, rowred, (uint32_t)B, nbp, dx_splits, cfg.scale,
@@ -770,3 +1035,5 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
 static_assert(xknn::smem_bytes3<xknn::kF3>() <= 232448, "GEMM-F tf32 pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDX3>() <= 232448, "GEMM-dX tf32 pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDW3>() <= 232448, "GEMM-dW tf32 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kDXb>() <= 232448, "GEMM-dX bf16x3 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kDWb>() <= 232448, "GEMM-dW bf16x3 pair smem");

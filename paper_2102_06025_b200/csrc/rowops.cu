@@ -40,7 +40,8 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
                                  const uint32_t* __restrict__ row_ids, const unsigned int* count,
                                  uint64_t id_base, float* __restrict__ out32,
                                  __nv_bfloat16* __restrict__ out16, float* __restrict__ norms,
-                                 unsigned long long* err, float* __restrict__ out_lo) {
+                                 unsigned long long* err, float* __restrict__ out_lo,
+                                 __nv_bfloat16* __restrict__ out16_lo) {
   griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = count ? *count : rows;
@@ -100,7 +101,17 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
       } else if (out32) {
         *reinterpret_cast<float4*>(out32 + r * d + col) = o;
       }
-      if (out16) store_bf16x4(out16 + r * d + col, o.x, o.y, o.z, o.w);
+      if (out16_lo) {  // bf16 planes (bf16x3 GEMM operand): out16 = bf16(o), out16_lo = bf16(o - it)
+        const __nv_bfloat162 h0 = __floats2bfloat162_rn(o.x, o.y), h1 = __floats2bfloat162_rn(o.z, o.w);
+        const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&h0);
+        u.y = *reinterpret_cast<const uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(out16 + r * d + col) = u;
+        store_bf16x4(out16_lo + r * d + col, o.x - f0.x, o.y - f0.y, o.z - f1.x, o.w - f1.y);
+      } else if (out16) {
+        store_bf16x4(out16 + r * d + col, o.x, o.y, o.z, o.w);
+      }
     }
   }
 }
@@ -324,13 +335,13 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
                                   float* norms, unsigned long long* err, cudaStream_t s,
-                                  bool seq, float* out_lo) {
+                                  bool seq, float* out_lo, __nv_bfloat16* out16_lo) {
   const unsigned grid = grid_for(rows * 32, 256);
   if (seq) {
 #define XKNN_SEQ_CASE(DV)                                                                      \
   case DV:                                                                                     \
     launch_pdl(k_normalize_rows<DV, true>, grid, 256, 0, s, in, rows, d, row_ids, count, id_base, \
-               out32, out16, norms, err, out_lo);                                              \
+               out32, out16, norms, err, out_lo, out16_lo);                                    \
     break;
     switch (d / 128) {
       XKNN_SEQ_CASE(1) XKNN_SEQ_CASE(2) XKNN_SEQ_CASE(4) XKNN_SEQ_CASE(8)
@@ -340,7 +351,7 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
     return cudaGetLastError();
   }
   XKNN_DISPATCH_D(d, k_normalize_rows, grid, 256, s, in, rows, d, row_ids, count, id_base, out32,
-                  out16, norms, err, out_lo);
+                  out16, norms, err, out_lo, out16_lo);
   return cudaGetLastError();
 }
 
