@@ -38,7 +38,9 @@ namespace xknn {
 
 namespace {
 
-enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2, kDXb = 3, kDWb = 4 };
+enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2, kDXb = 3, kDWb = 4, kFm = 5 };
+template <int KIND>
+constexpr bool kIsF = KIND == kF3 || KIND == kFm;
 template <int KIND>
 constexpr bool kIsDX = KIND == kDX3 || KIND == kDXb;
 template <int KIND>
@@ -94,6 +96,17 @@ struct Cfg3<kF3> {
   static constexpr uint32_t KB = XKNN_F3_KB;
   static constexpr uint32_t STAGES = KB == 32 ? 3 : 6, A_BYTES = 2 * 128 * KB * 4,
                             B_BYTES = 2 * 128 * KB * 4;
+  static constexpr uint32_t NBUF = 2, ACC = 256;
+};
+// GEMM-F in mixed precision: a*b ~ a_t*b_t + [bf16(a)*bf16(b - b_t) + bf16(a - a_t)*bf16(b)]
+// with a_t = tf32(a): the leading product on kind::tf32, the two cross terms (each ~2^-11 of it)
+// on kind::f16 at twice the rate -- 2 TF32-equivalents of MMA per product instead of 3.  A / B
+// stage: the tf32 rows (32 fp32, 128 B, SW128) + the bf16 planes of a and of a - a_t (32 bf16,
+// 64 B rows, SW64): the same 32 KB as the 3xTF32 hi / lo stage.
+template <>
+struct Cfg3<kFm> {
+  static constexpr uint32_t KB = 32, STAGES = 3, A_BYTES = 128 * 32 * 4 + 2 * 128 * 32 * 2,
+                            B_BYTES = A_BYTES;
   static constexpr uint32_t NBUF = 2, ACC = 256;
 };
 template <>
@@ -188,7 +201,7 @@ __device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint3
     return x;
   }
   const uint32_t bp = u % a.nbt, r = u / a.nbt;
-  const uint32_t nt = KIND == kF3 ? (mw + 255) / 256 : (mw + Cfg3<KIND>::KB - 1) / Cfg3<KIND>::KB;
+  const uint32_t nt = kIsF<KIND> ? (mw + 255) / 256 : (mw + Cfg3<KIND>::KB - 1) / Cfg3<KIND>::KB;
   x.row0 = bp * 256;
   x.t0 = (uint32_t)((uint64_t)r * nt / a.splits);
   x.t1 = (uint32_t)((uint64_t)(r + 1) * nt / a.splits);
@@ -277,6 +290,7 @@ __global__ void __launch_bounds__(384, 1)
     k_gemm3(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
             const __grid_constant__ CUtensorMap tmBhi, const __grid_constant__ CUtensorMap tmBlo,
             const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmOut2,
+            const __grid_constant__ CUtensorMap tmAd, const __grid_constant__ CUtensorMap tmBd,
             Gemm3Args a) {
   using C = Cfg3<KIND>;
   extern __shared__ uint8_t smem_raw[];
@@ -316,7 +330,11 @@ __global__ void __launch_bounds__(384, 1)
     tc::tma_prefetch(&tmAlo);
     tc::tma_prefetch(&tmBhi);
     tc::tma_prefetch(&tmBlo);
-    if (KIND != kF3) tc::tma_prefetch(&tmOut);
+    if (KIND == kFm) {
+      tc::tma_prefetch(&tmAd);
+      tc::tma_prefetch(&tmBd);
+    }
+    if (!kIsF<KIND>) tc::tma_prefetch(&tmOut);
   }
   if (warp == 2) tc::tmem_alloc_2sm<512>(tmem_slot);
   tc::fence_before_sync();
@@ -337,7 +355,7 @@ __global__ void __launch_bounds__(384, 1)
         const Unit3 x = unit3_of<KIND>(a, mw, u);
         if (!x.valid) continue;
         const int32_t myrow = (int32_t)(x.row0 + cta * 128);
-        const uint32_t nk = KIND == kF3 ? (x.t1 - x.t0) * (512 / C::KB) : x.t1 - x.t0;
+        const uint32_t nk = kIsF<KIND> ? (x.t1 - x.t0) * (512 / C::KB) : x.t1 - x.t0;
         for (uint32_t k = 0; k < nk; ++k) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           if (CONV)  // this CTA's fp32 A (the hi half of the A stage) and hi/lo B
@@ -353,14 +371,23 @@ __global__ void __launch_bounds__(384, 1)
           };
           uint8_t* dA = sA + stage * C::A_BYTES;
           uint8_t* dB = sB + stage * C::B_BYTES;
-          if (KIND == kF3) {
+          if (kIsF<KIND>) {
             constexpr uint32_t NKB = 512 / C::KB;  // stages per class tile
             const int32_t kc = (int32_t)((k % NKB) * C::KB);
             const int32_t crow = (int32_t)((x.t0 + k / NKB) * 256 + cta * 128);
-            tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
-            tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
-            tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
-            tc::tma_load_2d_2sm(dB + C::B_BYTES / 2, &tmBlo, &full[stage], kc, crow);
+            if (KIND == kFm) {  // tf32 rows | bf16(a) | bf16(a - a_t)
+              tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dA + 16384, &tmAlo, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dA + 24576, &tmAd, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
+              tc::tma_load_2d_2sm(dB + 16384, &tmBlo, &full[stage], kc, crow);
+              tc::tma_load_2d_2sm(dB + 24576, &tmBd, &full[stage], kc, crow);
+            } else {
+              tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
+              tc::tma_load_2d_2sm(dB + C::B_BYTES / 2, &tmBlo, &full[stage], kc, crow);
+            }
           } else if (BF) {
             const int32_t kk = (int32_t)((x.t0 + k) * 32);
             if (kIsDX<KIND>) {  // P~ planes [b][class]: this CTA's 128 batch rows, 32 classes
@@ -415,12 +442,12 @@ __global__ void __launch_bounds__(384, 1)
       for (uint32_t u = pair; u < nunits; u += npairs) {
         const Unit3 x = unit3_of<KIND>(a, mw, u);
         if (!x.valid) continue;
-        const uint32_t ntile = KIND == kF3 ? x.t1 - x.t0 : 1;
+        const uint32_t ntile = kIsF<KIND> ? x.t1 - x.t0 : 1;
         for (uint32_t t = 0; t < ntile; ++t) {
           tc::mbar_wait(&tempty[buf], tphase ^ 1);
           tc::fence_after_sync();
           const uint32_t dcol = tbase + buf * C::ACC;
-          const uint32_t nk = KIND == kF3 ? 512 / C::KB : x.t1 - x.t0;
+          const uint32_t nk = kIsF<KIND> ? 512 / C::KB : x.t1 - x.t0;
           for (uint32_t k = 0; k < nk; ++k) {
             if (CONV)
               tc::mbar_wait_cluster(&conv[stage], phase);
@@ -429,7 +456,23 @@ __global__ void __launch_bounds__(384, 1)
             tc::fence_after_sync();
             const uint32_t ah = tc::smem_u32(sA + stage * C::A_BYTES), al = ah + C::A_BYTES / 2;
             const uint32_t bh = tc::smem_u32(sB + stage * C::B_BYTES), bl = bh + C::B_BYTES / 2;
-            if (KIND == kF3) {
+            if (KIND == kFm) {
+              constexpr uint32_t idt = idesc_tf32(256, 256, false, false);
+              constexpr uint32_t idb = tc::idesc_bf16(256, 256, false, false);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 2; ++kk) {  // cross terms first: K = 16 bf16 = 32 B
+                const uint64_t dah = tc::smem_desc(ah + 16384 + kk * 32, 16, 512, tc::kSwizzle64);
+                const uint64_t dad = tc::smem_desc(ah + 24576 + kk * 32, 16, 512, tc::kSwizzle64);
+                const uint64_t dbh = tc::smem_desc(bh + 16384 + kk * 32, 16, 512, tc::kSwizzle64);
+                const uint64_t dbd = tc::smem_desc(bh + 24576 + kk * 32, 16, 512, tc::kSwizzle64);
+                tc::mma_bf16_2sm(dcol, dah, dbd, idb, (k | kk) != 0);
+                tc::mma_bf16_2sm(dcol, dad, dbh, idb, 1u);
+              }
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk)  // the tf32 products: K = 8 fp32 = 32 B
+                mma_tf32_2sm(dcol, tc::smem_desc(ah + kk * 32, 16, 1024, tc::kSwizzle128),
+                             tc::smem_desc(bh + kk * 32, 16, 1024, tc::kSwizzle128), idt, 1u);
+            } else if (KIND == kF3) {
               constexpr uint32_t id = idesc_tf32(256, 256, false, false);
               constexpr uint32_t SBO = C::KB * 4 * 8;  // 8-row group of KB * 4-byte rows
               constexpr uint32_t SW = C::KB == 32 ? tc::kSwizzle128 : tc::kSwizzle64;
@@ -552,13 +595,13 @@ __global__ void __launch_bounds__(384, 1)
         }
         convert_to(cend + pre);
       }
-      const uint32_t ntile = KIND == kF3 ? x.t1 - x.t0 : 1;
+      const uint32_t ntile = kIsF<KIND> ? x.t1 - x.t0 : 1;
       for (uint32_t t = 0; t < ntile; ++t) {
         tc::mbar_wait(&tfull[buf], tphase);
         tc::fence_after_sync();
         const uint32_t tb = tbase + buf * C::ACC + lane_addr;
         const int32_t grow0 = (int32_t)(x.row0 + cta * 128 + q * 32);  // this warp's 32 rows
-        if (KIND == kF3) {
+        if (kIsF<KIND>) {
           const uint32_t ct = x.t0 + t;
           const uint32_t b = x.row0 + cta * 128 + row;
           const bool vrow = b < a.B;
@@ -748,13 +791,13 @@ __global__ void k_zero_rows32(const SelState* st, float* whi, float* wlo, __nv_b
   const uint32_t e = min(cap_rows, (c + 255) / 256 * 256);
   const uint64_t n = (uint64_t)(e - c) * 512 / 4;
   float4* ph = reinterpret_cast<float4*>(whi + (uint64_t)c * 512);
-  float4* pl = reinterpret_cast<float4*>(wlo + (uint64_t)c * 512);
+  float4* pl = wlo ? reinterpret_cast<float4*>(wlo + (uint64_t)c * 512) : nullptr;
   uint2* bh = wbh ? reinterpret_cast<uint2*>(wbh + (uint64_t)c * 512) : nullptr;
   uint2* bl = wbh ? reinterpret_cast<uint2*>(wbl + (uint64_t)c * 512) : nullptr;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     ph[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    pl[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (pl) pl[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (bh) {
       bh[i] = make_uint2(0u, 0u);
       bl[i] = make_uint2(0u, 0u);
@@ -809,9 +852,13 @@ struct Fast32State {
   CUtensorMap mDX_Ah, mDX_Al, mDX_Bh, mDX_Bl, mDX_st;  // P~ (16 x 128, SW64), W_sub (32 x 16)
   CUtensorMap mDW_Ah, mDW_Al, mDW_Bh, mDW_Bl, mDW_st;  // P~ (32 x 16), X_hat' (32 x 16)
   CUtensorMap mDWP_st;                                 // dW tail-unit K-partials
-  // bf16x3 backward GEMMs (default; XKNN_FP32_BWD=tf32 selects 3xTF32 for them too): the bf16
-  // planes of P~, W_sub and X_hat' replace P~ fp32 and X_hat' hi/lo as their operands
-  bool bfb = true;
+  // GEMM arithmetic (XKNN_FP32_GEMM): "mixed" (default) = GEMM-F mixed tf32/bf16 + bf16x3
+  // GEMM-dW/dX; "f3" = 3xTF32 GEMM-F + bf16x3 dW/dX; "3xtf32" = 3xTF32 throughout.  The bf16
+  // planes of P~, W_sub and X_hat' replace P~ fp32 and X_hat' hi/lo as the bf16x3 operands.
+  bool bfb = true, mixed = true;
+  __nv_bfloat16 *xb_hi = nullptr, *xd = nullptr;  // mixed GEMM-F: bf16(x_hat), bf16(x_hat - tf32)
+  __nv_bfloat16* wd = nullptr;                      // ... bf16(w_sub - tf32(w_sub)) [mwpad][512]
+  CUtensorMap mF_Ad, mF_Bd;
   __nv_bfloat16 *pb_hi = nullptr, *pb_lo = nullptr;    // P~ [bpad][mwpad]
   __nv_bfloat16 *wb_hi = nullptr, *wb_lo = nullptr;    // W_sub [mwpad][512]
   __nv_bfloat16 *xsb_hi = nullptr, *xsb_lo = nullptr;  // X_hat' [bpad][512]
@@ -824,7 +871,10 @@ xknn_status_t Layer::init_fast32() {
   f->bpad = (uint32_t)((bmax + 255) / 256 * 256);
   f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
   ldp = f->mwpad;
-  if (const char* e = getenv("XKNN_FP32_BWD")) f->bfb = strcmp(e, "tf32") != 0;
+  if (const char* e = getenv("XKNN_FP32_GEMM")) {
+    f->mixed = strcmp(e, "mixed") == 0;
+    f->bfb = strcmp(e, "3xtf32") != 0;
+  }
   const uint64_t xb = (uint64_t)f->bpad * 512, wb = (uint64_t)f->mwpad * 512,
                  pb = (uint64_t)f->bpad * f->mwpad;
   for (float** p : {&f->xh_hi, &f->xh_lo, &f->xs_hi, &f->xs_lo}) {
@@ -832,8 +882,17 @@ xknn_status_t Layer::init_fast32() {
     XK_CUDA(cudaMemsetAsync(*p, 0, xb * 4, stream));
   }
   for (float** p : {&f->w_hi, &f->w_lo}) {
+    if (f->mixed && p == &f->w_lo) continue;
     XK_CUDA(dalloc(p, wb));
     XK_CUDA(cudaMemsetAsync(*p, 0, wb * 4, stream));
+  }
+  if (f->mixed) {
+    for (auto* p : {&f->xb_hi, &f->xd}) {
+      XK_CUDA(dalloc(p, xb));
+      XK_CUDA(cudaMemsetAsync(*p, 0, xb * 2, stream));
+    }
+    XK_CUDA(dalloc(&f->wd, wb));
+    XK_CUDA(cudaMemsetAsync(f->wd, 0, wb * 2, stream));
   }
   if (f->bfb) {
     for (auto* p : {&f->pb_hi, &f->pb_lo}) {
@@ -870,10 +929,21 @@ xknn_status_t Layer::init_fast32() {
   bool ok = true;
   constexpr uint32_t FKB = Cfg3<kF3>::KB;
   const auto SF = FKB == 32 ? S128 : S64;
-  ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, FKB, 128, SF);
-  ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, FKB, 128, SF);
-  ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, FKB, 128, SF);
-  ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, FKB, 128, SF);
+  if (f->mixed) {  // tf32 rows (SW128) and the bf16 planes (32 x 128 boxes, SW64)
+    ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, 32, 128, S128);
+    ok &= make_map32(&f->mF_Al, f->xb_hi, 512, f->bpad, 32, 128, S64, true);
+    ok &= make_map32(&f->mF_Ad, f->xd, 512, f->bpad, 32, 128, S64, true);
+    ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, 32, 128, S128);
+    ok &= make_map32(&f->mF_Bl, f->wb_hi, 512, f->mwpad, 32, 128, S64, true);
+    ok &= make_map32(&f->mF_Bd, f->wd, 512, f->mwpad, 32, 128, S64, true);
+  } else {
+    ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, FKB, 128, SF);
+    ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, FKB, 128, SF);
+    ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, FKB, 128, SF);
+    ok &= make_map32(&f->mF_Bl, f->w_lo, 512, f->mwpad, FKB, 128, SF);
+    f->mF_Ad = f->mF_Ah;
+    f->mF_Bd = f->mF_Bh;
+  }
   if (f->bfb) {  // bf16 planes in the BF16 path's layouts (fast.cu), 32 K per stage
     ok &= make_map32(&f->mDX_Ah, f->pb_hi, f->mwpad, f->bpad, 32, 128, S64, true);
     ok &= make_map32(&f->mDX_Al, f->pb_lo, f->mwpad, f->bpad, 32, 128, S64, true);
@@ -904,6 +974,8 @@ xknn_status_t Layer::init_fast32() {
                                smem_bytes3<kDX3>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDW3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes3<kDW3>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kFm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kFm>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDXb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes3<kDXb>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDWb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -919,7 +991,7 @@ void Layer::free_fast32() {
                   (void*)f->partial_f, (void*)f->labelterm, (void*)f->partial_dx, (void*)f->dW32,
                   (void*)f->dw_part, (void*)f->lab_head, (void*)f->lab_next, (void*)f->pb_hi,
                   (void*)f->pb_lo, (void*)f->wb_hi, (void*)f->wb_lo, (void*)f->xsb_hi,
-                  (void*)f->xsb_lo})
+                  (void*)f->xsb_lo, (void*)f->xb_hi, (void*)f->xd, (void*)f->wd})
     if (p) cudaFree(p);
   delete f;
   fast32 = nullptr;
@@ -939,14 +1011,14 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   // (a) operands: the active weight rows gathered + normalized, split hi/lo (feature all-gather
   //     runs under it at P > 1), then X_hat hi/lo
   XK_CUDA(launch_normalize_rows(W, mw_cap, D, active, &st->active_count, begin, f->w_hi, f->wb_hi,
-                                wnorm, err, stream, false, f->w_lo, f->wb_lo));
+                                wnorm, err, stream, false, f->w_lo, f->wb_lo, f->wd));
   ++launches;
   launch_pdl(k_zero_rows32, 64, 256, 0, stream, (const SelState*)st, f->w_hi, f->w_lo, f->wb_hi,
              f->wb_lo, f->mwpad);
   XK_LAUNCH();
   if (world > 1) XK_TRY(wait_features());
-  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, f->xh_hi, nullptr, xnorm, err,
-                                stream, false, f->xh_lo));
+  XK_CUDA(launch_normalize_rows(X, B, D, nullptr, nullptr, 0, f->xh_hi, f->xb_hi, xnorm, err,
+                                stream, false, f->mixed ? nullptr : f->xh_lo, nullptr, f->xd));
   ++launches;
   mark(3);
   Gemm3Args ga{};
@@ -966,8 +1038,12 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ga.partial = f->partial_f;
   ga.nbt = nbp;
   ga.splits = gemm_pair_splits(nbp, 1u << 30);
-  launch_pdl_cluster(k_gemm3<kF3>, kNumSMs, 384, smem_bytes3<kF3>(), stream, 2u, f->mF_Ah,
-                     f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, f->mF_Ah, ga);
+  if (f->mixed)
+    launch_pdl_cluster(k_gemm3<kFm>, kNumSMs, 384, smem_bytes3<kFm>(), stream, 2u, f->mF_Ah,
+                       f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, f->mF_Ah, f->mF_Ad, f->mF_Bd, ga);
+  else
+    launch_pdl_cluster(k_gemm3<kF3>, kNumSMs, 384, smem_bytes3<kF3>(), stream, 2u, f->mF_Ah,
+                       f->mF_Al, f->mF_Bh, f->mF_Bl, f->mF_Ah, f->mF_Ah, f->mF_Ah, f->mF_Ah, ga);
   XK_LAUNCH();
   mark(4);
   // (c) row statistics -> all-reduce over the class shards -> (d) loss, X_hat', label lists
@@ -991,10 +1067,12 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   // (e) GEMM-dW -> fp32 dW rows (compact active order)
   if (f->bfb)
     launch_pdl_cluster(k_gemm3<kDWb>, kNumSMs, 384, smem_bytes3<kDWb>(), stream, 2u, f->mDW_Ah,
-                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
+                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, f->mDW_st,
+                       f->mDW_st, ga);
   else
     launch_pdl_cluster(k_gemm3<kDW3>, kNumSMs, 384, smem_bytes3<kDW3>(), stream, 2u, f->mDW_Ah,
-                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, ga);
+                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, f->mDW_st,
+                       f->mDW_st, ga);
   XK_LAUNCH();
   mark(6);
   // (f) GEMM-dX split-K partials -> reduce (+ one-hot correction) -> reduce-scatter
@@ -1004,10 +1082,12 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   ga.splits = dx_splits;
   if (f->bfb)
     launch_pdl_cluster(k_gemm3<kDXb>, kNumSMs, 384, smem_bytes3<kDXb>(), stream, 2u, f->mDX_Ah,
-                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
+                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, f->mDX_st,
+                       f->mDX_st, ga);
   else
     launch_pdl_cluster(k_gemm3<kDX3>, kNumSMs, 384, smem_bytes3<kDX3>(), stream, 2u, f->mDX_Ah,
-                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, ga);
+                       f->mDX_Al, f->mDX_Bh, f->mDX_Bl, f->mDX_st, f->mDX_st, f->mDX_st,
+                       f->mDX_st, ga);
   XK_LAUNCH();
   mark(7);
   XK_CUDA(launch_dx_reduce(f->partial_dx, rowred, (uint32_t)B, nbp, dx_splits, cfg.scale,
@@ -1036,4 +1116,5 @@ static_assert(xknn::smem_bytes3<xknn::kF3>() <= 232448, "GEMM-F tf32 pair smem")
 static_assert(xknn::smem_bytes3<xknn::kDX3>() <= 232448, "GEMM-dX tf32 pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDW3>() <= 232448, "GEMM-dW tf32 pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDXb>() <= 232448, "GEMM-dX bf16x3 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kFm>() <= 232448, "GEMM-F mixed pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDWb>() <= 232448, "GEMM-dW bf16x3 pair smem");

@@ -39,7 +39,7 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
                                   float* norms, unsigned long long* err, cudaStream_t s,
                                   bool seq = false, float* out_lo = nullptr,
-                                  __nv_bfloat16* out16_lo = nullptr);
+                                  __nv_bfloat16* out16_lo = nullptr, __nv_bfloat16* out_d = nullptr);
 cudaError_t launch_update_rows(float* W, float* V, const float* G, const uint32_t* active,
                                const unsigned int* count, uint64_t max_rows, uint64_t begin,
                                uint32_t d, const float* wnorm, const float* lr, float mu, float wd,

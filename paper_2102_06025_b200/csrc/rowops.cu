@@ -41,7 +41,8 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
                                  uint64_t id_base, float* __restrict__ out32,
                                  __nv_bfloat16* __restrict__ out16, float* __restrict__ norms,
                                  unsigned long long* err, float* __restrict__ out_lo,
-                                 __nv_bfloat16* __restrict__ out16_lo) {
+                                 __nv_bfloat16* __restrict__ out16_lo,
+                                 __nv_bfloat16* __restrict__ out_d) {
   griddep_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nrows = count ? *count : rows;
@@ -93,11 +94,13 @@ __global__ void k_normalize_rows(const float* __restrict__ in, uint64_t rows, ui
       o.z = __fmul_rn(v[c].z, inv);
       o.w = __fmul_rn(v[c].w, inv);
       const uint64_t col = (uint64_t)(lane + 32 * c) * 4;
-      if (out_lo) {  // 3xTF32 operand split: out32 = tf32(o) (round to nearest), out_lo = o - it
+      if (out_lo || out_d) {  // tf32 operand split: out32 = tf32(o) (round to nearest), and
+                              // o - it in fp32 (3xTF32, out_lo) or bf16 (mixed GEMM-F, out_d)
         const float4 hi = make_float4(tf32_rna(o.x), tf32_rna(o.y), tf32_rna(o.z), tf32_rna(o.w));
         *reinterpret_cast<float4*>(out32 + r * d + col) = hi;
-        *reinterpret_cast<float4*>(out_lo + r * d + col) =
-            make_float4(o.x - hi.x, o.y - hi.y, o.z - hi.z, o.w - hi.w);
+        const float4 lo = make_float4(o.x - hi.x, o.y - hi.y, o.z - hi.z, o.w - hi.w);
+        if (out_lo) *reinterpret_cast<float4*>(out_lo + r * d + col) = lo;
+        if (out_d) store_bf16x4(out_d + r * d + col, lo.x, lo.y, lo.z, lo.w);
       } else if (out32) {
         *reinterpret_cast<float4*>(out32 + r * d + col) = o;
       }
@@ -335,13 +338,14 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
                                   const uint32_t* row_ids, const unsigned int* count,
                                   uint64_t id_base, float* out32, __nv_bfloat16* out16,
                                   float* norms, unsigned long long* err, cudaStream_t s,
-                                  bool seq, float* out_lo, __nv_bfloat16* out16_lo) {
+                                  bool seq, float* out_lo, __nv_bfloat16* out16_lo,
+                                  __nv_bfloat16* out_d) {
   const unsigned grid = grid_for(rows * 32, 256);
   if (seq) {
 #define XKNN_SEQ_CASE(DV)                                                                      \
   case DV:                                                                                     \
     launch_pdl(k_normalize_rows<DV, true>, grid, 256, 0, s, in, rows, d, row_ids, count, id_base, \
-               out32, out16, norms, err, out_lo, out16_lo);                                    \
+               out32, out16, norms, err, out_lo, out16_lo, out_d);                             \
     break;
     switch (d / 128) {
       XKNN_SEQ_CASE(1) XKNN_SEQ_CASE(2) XKNN_SEQ_CASE(4) XKNN_SEQ_CASE(8)
@@ -351,7 +355,7 @@ cudaError_t launch_normalize_rows(const float* in, uint64_t rows, uint32_t d,
     return cudaGetLastError();
   }
   XKNN_DISPATCH_D(d, k_normalize_rows, grid, 256, s, in, rows, d, row_ids, count, id_base, out32,
-                  out16, norms, err, out_lo, out16_lo);
+                  out16, norms, err, out_lo, out16_lo, out_d);
   return cudaGetLastError();
 }
 
