@@ -38,13 +38,13 @@ namespace xknn {
 
 namespace {
 
-enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2, kDXb = 3, kDWb = 4, kFm = 5 };
+enum Kind3 : int { kF3 = 0, kDX3 = 1, kDW3 = 2, kDXb = 3, kDWb = 4, kFm = 5, kDWh = 6 };
 template <int KIND>
 constexpr bool kIsF = KIND == kF3 || KIND == kFm;
 template <int KIND>
 constexpr bool kIsDX = KIND == kDX3 || KIND == kDXb;
 template <int KIND>
-constexpr bool kIsDW = KIND == kDW3 || KIND == kDWb;
+constexpr bool kIsDW = KIND == kDW3 || KIND == kDWb || KIND == kDWh;
 
 // Instruction descriptor, kind::tf32: TF32 A/B (format 2), fp32 D.
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t m, uint32_t n, bool a_mn, bool b_mn) {
@@ -103,10 +103,15 @@ struct Cfg3<kF3> {
 // on kind::f16 at twice the rate -- 2 TF32-equivalents of MMA per product instead of 3.  A / B
 // stage: the tf32 rows (32 fp32, 128 B, SW128) + the bf16 planes of a and of a - a_t (32 bf16,
 // 64 B rows, SW64): the same 32 KB as the 3xTF32 hi / lo stage.
+#ifndef XKNN_FM_KB
+#define XKNN_FM_KB 32
+#endif
 template <>
 struct Cfg3<kFm> {
-  static constexpr uint32_t KB = 32, STAGES = 3, A_BYTES = 128 * 32 * 4 + 2 * 128 * 32 * 2,
-                            B_BYTES = A_BYTES;
+  // KB = 16: half-size stages (64-B tf32 rows, SW64; 32-B bf16 rows, SW32), twice as many
+  static constexpr uint32_t KB = XKNN_FM_KB, STAGES = KB == 32 ? 3 : 6,
+                            A_BYTES = 128 * KB * 4 + 2 * 128 * KB * 2, B_BYTES = A_BYTES;
+  static constexpr uint32_t TF = 128 * KB * 4, BP = 128 * KB * 2;  // tf32 rows, one bf16 plane
   static constexpr uint32_t NBUF = 2, ACC = 256;
 };
 template <>
@@ -133,6 +138,19 @@ template <>
 struct Cfg3<kDWb> {
   static constexpr uint32_t STAGES = 4, A_BYTES = 2 * 2 * 4096, B_BYTES = 2 * 4 * 4096;
   static constexpr uint32_t NBUF = 1, ACC = 512, KB = 32;
+};
+// kDWh: GEMM-dW bf16x3 in half-width units -- 256 classes x 256 d (one N = 256 instruction) --
+// so that two 256-column accumulators fit TMEM and a unit's drain overlaps the next unit's MMAs
+// (the K = B loop is short: at C2 a 512-wide unit's drain stalled the tensor core ~15 % of the
+// time).  The two d-halves of a class tile are adjacent units (adjacent pairs, same time), so
+// the second read of the P~ tile comes from L2.
+#ifndef XKNN_DWH
+#define XKNN_DWH 1
+#endif
+template <>
+struct Cfg3<kDWh> {
+  static constexpr uint32_t STAGES = 6, A_BYTES = 2 * 2 * 4096, B_BYTES = 2 * 2 * 4096;
+  static constexpr uint32_t NBUF = 2, ACC = 256, KB = 32;
 };
 constexpr uint32_t kStg3 = 4096;  // per epilogue warp: one 32 x 32 fp32 staging block
 #ifndef XKNN_PCONV
@@ -170,6 +188,7 @@ struct Unit3 {
 
 template <int KIND>
 __device__ __forceinline__ uint32_t num_units3(const Gemm3Args& a, uint32_t mw) {
+  if (KIND == kDWh) return 2 * ((mw + 255) / 256);
   if (kIsDW<KIND>) {
     const uint32_t units = (mw + 255) / 256;
     const DwSplit sp = dw_split(units, gridDim.x / 2);
@@ -182,6 +201,14 @@ template <int KIND>
 __device__ __forceinline__ Unit3 unit3_of(const Gemm3Args& a, uint32_t mw, uint32_t u) {
   Unit3 x{};
   x.id = u;
+  if (KIND == kDWh) {  // class tile u / 2, d-half u % 2 (in id)
+    x.valid = true;
+    x.row0 = (u >> 1) * 256;
+    x.t0 = 0;
+    x.t1 = a.bpad / Cfg3<KIND>::KB;
+    x.id = u & 1;
+    return x;
+  }
   if (kIsDW<KIND>) {
     const uint32_t nk = a.bpad / Cfg3<KIND>::KB;
     const DwSplit sp = dw_split((mw + 255) / 256, gridDim.x / 2);
@@ -307,7 +334,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* conv = lfull + C::STAGES;    // kConv3 (leader): both CTAs' A stage split hi/lo
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + C::STAGES);
   constexpr bool CONV = kConv3<KIND>;
-  constexpr bool BF = KIND == kDXb || KIND == kDWb;
+  constexpr bool BF = KIND == kDXb || KIND == kDWb || KIND == kDWh;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = tc::cluster_ctarank() & 1;
@@ -376,12 +403,13 @@ __global__ void __launch_bounds__(384, 1)
             const int32_t kc = (int32_t)((k % NKB) * C::KB);
             const int32_t crow = (int32_t)((x.t0 + k / NKB) * 256 + cta * 128);
             if (KIND == kFm) {  // tf32 rows | bf16(a) | bf16(a - a_t)
+              constexpr uint32_t TF = Cfg3<kFm>::TF, BP = Cfg3<kFm>::BP;
               tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
-              tc::tma_load_2d_2sm(dA + 16384, &tmAlo, &full[stage], kc, myrow);
-              tc::tma_load_2d_2sm(dA + 24576, &tmAd, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dA + TF, &tmAlo, &full[stage], kc, myrow);
+              tc::tma_load_2d_2sm(dA + TF + BP, &tmAd, &full[stage], kc, myrow);
               tc::tma_load_2d_2sm(dB, &tmBhi, &full[stage], kc, crow);
-              tc::tma_load_2d_2sm(dB + 16384, &tmBlo, &full[stage], kc, crow);
-              tc::tma_load_2d_2sm(dB + 24576, &tmBd, &full[stage], kc, crow);
+              tc::tma_load_2d_2sm(dB + TF, &tmBlo, &full[stage], kc, crow);
+              tc::tma_load_2d_2sm(dB + TF + BP, &tmBd, &full[stage], kc, crow);
             } else {
               tc::tma_load_2d_2sm(dA, &tmAhi, &full[stage], kc, myrow);
               tc::tma_load_2d_2sm(dA + C::A_BYTES / 2, &tmAlo, &full[stage], kc, myrow);
@@ -400,12 +428,13 @@ __global__ void __launch_bounds__(384, 1)
                 load(dA + C::A_BYTES / 2 + j * 4096, &tmAlo, myrow + 64 * j, kk);
               }
             }
-            // B planes [K rows][512 d]: this CTA's 128 d of each 256-wide N instruction j
+            // B planes [K rows][512 d]: this CTA's 128 d of each 256-wide N instruction j (kDWh:
+            // only the unit's d-half)
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < (KIND == kDWh ? 1 : 2); ++j)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const int32_t dc = (int32_t)(256 * j + 128 * cta + 64 * h);
+                const int32_t dc = (int32_t)(256 * (KIND == kDWh ? x.id : j) + 128 * cta + 64 * h);
                 load(dB + (j * 2 + h) * 4096, &tmBhi, dc, kk);
                 load(dB + C::B_BYTES / 2 + (j * 2 + h) * 4096, &tmBlo, dc, kk);
               }
@@ -459,19 +488,23 @@ __global__ void __launch_bounds__(384, 1)
             if (KIND == kFm) {
               constexpr uint32_t idt = idesc_tf32(256, 256, false, false);
               constexpr uint32_t idb = tc::idesc_bf16(256, 256, false, false);
+              constexpr uint32_t KB = Cfg3<kFm>::KB, TF = Cfg3<kFm>::TF, BP = Cfg3<kFm>::BP;
+              // tf32 rows of KB * 4 B, bf16 rows of KB * 2 B: 8-row groups, matching swizzles
+              constexpr uint32_t SWT = KB == 32 ? tc::kSwizzle128 : tc::kSwizzle64;
+              constexpr uint32_t SWB = KB == 32 ? tc::kSwizzle64 : tc::kSwizzle32;
 #pragma unroll
-              for (uint32_t kk = 0; kk < 2; ++kk) {  // cross terms first: K = 16 bf16 = 32 B
-                const uint64_t dah = tc::smem_desc(ah + 16384 + kk * 32, 16, 512, tc::kSwizzle64);
-                const uint64_t dad = tc::smem_desc(ah + 24576 + kk * 32, 16, 512, tc::kSwizzle64);
-                const uint64_t dbh = tc::smem_desc(bh + 16384 + kk * 32, 16, 512, tc::kSwizzle64);
-                const uint64_t dbd = tc::smem_desc(bh + 24576 + kk * 32, 16, 512, tc::kSwizzle64);
+              for (uint32_t kk = 0; kk < KB / 16; ++kk) {  // cross terms first: K = 16 bf16 = 32 B
+                const uint64_t dah = tc::smem_desc(ah + TF + kk * 32, 16, KB * 16, SWB);
+                const uint64_t dad = tc::smem_desc(ah + TF + BP + kk * 32, 16, KB * 16, SWB);
+                const uint64_t dbh = tc::smem_desc(bh + TF + kk * 32, 16, KB * 16, SWB);
+                const uint64_t dbd = tc::smem_desc(bh + TF + BP + kk * 32, 16, KB * 16, SWB);
                 tc::mma_bf16_2sm(dcol, dah, dbd, idb, (k | kk) != 0);
                 tc::mma_bf16_2sm(dcol, dad, dbh, idb, 1u);
               }
 #pragma unroll
-              for (uint32_t kk = 0; kk < 4; ++kk)  // the tf32 products: K = 8 fp32 = 32 B
-                mma_tf32_2sm(dcol, tc::smem_desc(ah + kk * 32, 16, 1024, tc::kSwizzle128),
-                             tc::smem_desc(bh + kk * 32, 16, 1024, tc::kSwizzle128), idt, 1u);
+              for (uint32_t kk = 0; kk < KB / 8; ++kk)  // the tf32 products: K = 8 fp32 = 32 B
+                mma_tf32_2sm(dcol, tc::smem_desc(ah + kk * 32, 16, KB * 32, SWT),
+                             tc::smem_desc(bh + kk * 32, 16, KB * 32, SWT), idt, 1u);
             } else if (KIND == kF3) {
               constexpr uint32_t id = idesc_tf32(256, 256, false, false);
               constexpr uint32_t SBO = C::KB * 4 * 8;  // 8-row group of KB * 4-byte rows
@@ -497,7 +530,7 @@ __global__ void __launch_bounds__(384, 1)
                     kIsDX<KIND> ? tc::smem_desc(al + kk * 32, 16, 512, tc::kSwizzle64)
                                 : tc::smem_desc(al + kk * 2048, 4096, 1024, tc::kSwizzle128);
 #pragma unroll
-                for (uint32_t j = 0; j < 2; ++j) {
+                for (uint32_t j = 0; j < (KIND == kDWh ? 1u : 2u); ++j) {
                   const uint64_t dbh =
                       tc::smem_desc(bh + j * 8192 + kk * 2048, 4096, 1024, tc::kSwizzle128);
                   const uint64_t dbl =
@@ -670,8 +703,8 @@ __global__ void __launch_bounds__(384, 1)
                                                       : grow0;
           const bool zero = kIsDX<KIND> && x.t1 == x.t0;
 #pragma unroll 1
-          for (uint32_t ch = 0; ch < 8; ++ch) {
-            const uint32_t col = h * 256 + ch * 32;
+          for (uint32_t ch = 0; ch < C::ACC / 64; ++ch) {
+            const uint32_t col = h * (C::ACC / 2) + ch * 32;
             float v[32];
             if (!zero) {
               tc::tmem_ld32(tb + col, v);
@@ -683,7 +716,8 @@ __global__ void __launch_bounds__(384, 1)
             tc::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tc::tma_store_2d(part ? &tmOut2 : &tmOut, stg, (int32_t)col, orow);
+              tc::tma_store_2d(part ? &tmOut2 : &tmOut, stg,
+                               (int32_t)(col + (KIND == kDWh ? x.id * 256 : 0)), orow);
               tc::tma_store_commit();
               tc::tma_store_wait_read<0>();
             }
@@ -929,13 +963,15 @@ xknn_status_t Layer::init_fast32() {
   bool ok = true;
   constexpr uint32_t FKB = Cfg3<kF3>::KB;
   const auto SF = FKB == 32 ? S128 : S64;
-  if (f->mixed) {  // tf32 rows (SW128) and the bf16 planes (32 x 128 boxes, SW64)
-    ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, 32, 128, S128);
-    ok &= make_map32(&f->mF_Al, f->xb_hi, 512, f->bpad, 32, 128, S64, true);
-    ok &= make_map32(&f->mF_Ad, f->xd, 512, f->bpad, 32, 128, S64, true);
-    ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, 32, 128, S128);
-    ok &= make_map32(&f->mF_Bl, f->wb_hi, 512, f->mwpad, 32, 128, S64, true);
-    ok &= make_map32(&f->mF_Bd, f->wd, 512, f->mwpad, 32, 128, S64, true);
+  if (f->mixed) {  // tf32 rows and the bf16 planes, KB x 128 boxes
+    constexpr uint32_t MKB = Cfg3<kFm>::KB;
+    const auto ST = MKB == 32 ? S128 : S64, SB = MKB == 32 ? S64 : CU_TENSOR_MAP_SWIZZLE_32B;
+    ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, MKB, 128, ST);
+    ok &= make_map32(&f->mF_Al, f->xb_hi, 512, f->bpad, MKB, 128, SB, true);
+    ok &= make_map32(&f->mF_Ad, f->xd, 512, f->bpad, MKB, 128, SB, true);
+    ok &= make_map32(&f->mF_Bh, f->w_hi, 512, f->mwpad, MKB, 128, ST);
+    ok &= make_map32(&f->mF_Bl, f->wb_hi, 512, f->mwpad, MKB, 128, SB, true);
+    ok &= make_map32(&f->mF_Bd, f->wd, 512, f->mwpad, MKB, 128, SB, true);
   } else {
     ok &= make_map32(&f->mF_Ah, f->xh_hi, 512, f->bpad, FKB, 128, SF);
     ok &= make_map32(&f->mF_Al, f->xh_lo, 512, f->bpad, FKB, 128, SF);
@@ -980,6 +1016,8 @@ xknn_status_t Layer::init_fast32() {
                                smem_bytes3<kDXb>()));
   XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDWb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem_bytes3<kDWb>()));
+  XK_CUDA(cudaFuncSetAttribute(k_gemm3<kDWh>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem_bytes3<kDWh>()));
   return XKNN_OK;
 }
 
@@ -1065,7 +1103,11 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   XK_LAUNCH();
   mark(5);
   // (e) GEMM-dW -> fp32 dW rows (compact active order)
-  if (f->bfb)
+  if (f->bfb && XKNN_DWH)
+    launch_pdl_cluster(k_gemm3<kDWh>, kNumSMs, 384, smem_bytes3<kDWh>(), stream, 2u, f->mDW_Ah,
+                       f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, f->mDW_st,
+                       f->mDW_st, ga);
+  else if (f->bfb)
     launch_pdl_cluster(k_gemm3<kDWb>, kNumSMs, 384, smem_bytes3<kDWb>(), stream, 2u, f->mDW_Ah,
                        f->mDW_Al, f->mDW_Bh, f->mDW_Bl, f->mDW_st, f->mDWP_st, f->mDW_st,
                        f->mDW_st, ga);
@@ -1102,8 +1144,9 @@ xknn_status_t Layer::run_fast32_core(uint64_t B) {
   }
   // (g) normalize-backward + momentum SGD on the active rows, with the one-hot correction
   mark(8);
+  // (tail-unit K-partials: every dW kind but the half-width one)
   LabelFix lf{f->lab_head, f->lab_next, X, xnorm, (float)((double)cfg.scale / (double)B),
-              f->dw_part, (uint32_t)kNumSMs / 2};
+              f->bfb && XKNN_DWH ? nullptr : f->dw_part, (uint32_t)kNumSMs / 2};
   XK_CUDA(launch_update_rows(W, V, f->dW32, active, &st->active_count, mw_cap, begin, D, wnorm,
                              lr_dev, cfg.momentum, cfg.weight_decay, err, stream, 148u * 16u, lf));
   ++launches;
@@ -1118,3 +1161,4 @@ static_assert(xknn::smem_bytes3<xknn::kDW3>() <= 232448, "GEMM-dW tf32 pair smem
 static_assert(xknn::smem_bytes3<xknn::kDXb>() <= 232448, "GEMM-dX bf16x3 pair smem");
 static_assert(xknn::smem_bytes3<xknn::kFm>() <= 232448, "GEMM-F mixed pair smem");
 static_assert(xknn::smem_bytes3<xknn::kDWb>() <= 232448, "GEMM-dW bf16x3 pair smem");
+static_assert(xknn::smem_bytes3<xknn::kDWh>() <= 232448, "GEMM-dW bf16x3 half-unit pair smem");
