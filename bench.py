@@ -5,8 +5,10 @@
                     [--workload c2|c3|c4|c4r|c1] [--precision fp32|bf16|fp32_exact]
                     [--no-bf16-line]
 
-The headline runs XKNN_PREC_FP32 (3xTF32 tensor cores, within 1e-5 of the fp32 reference);
-the same workload in the bf16 tensor-core mode is reported beside it as `bf16_mode`.
+The headline runs XKNN_PREC_FP32 (fp32 accuracy, within 1e-5 of the fp32 reference, on tensor
+cores: mixed tf32/bf16 logits GEMM, bf16x3 gradient GEMMs -- fast32.cu; XKNN_FP32_GEMM=3xtf32
+selects 3xTF32 throughout); the same workload in the bf16 tensor-core mode is reported beside it
+as `bf16_mode`.
 
 One step = the fc half of HybridSim::train_step (parallel.cpp:455-572, :638-668) over one global
 batch: feature/label all-gather, Algorithm-1 active-class selection, active-row gather +
@@ -57,11 +59,8 @@ PHASES = ["allgather", "select", "gather_normalize", "gemm_logits_softmax", "sof
 
 def peaks():
     """Roofline denominators.  HBM GB/s and bf16 TF/s (burst: best of 10; sustained: back to
-    back for 4 s) from the driver-written MEASURED_PEAKS.json.  TF32 (the XKNN_PREC_FP32 GEMMs):
-    not in MEASURED_PEAKS; cuBLAS TF32 measured the same way reaches only 691 / 586 TF/s
-    (profiles/r02/tf32_peak.json), below what the tensor cores sustain in this repo's own 3xTF32
-    kernels, so the denominator is B200_PROFILING.md's dense TF32 figure, 1.1 PF/s, for burst and
-    sustained alike.  Fallbacks: B200_PROFILING.md's figures."""
+    back for 4 s) from the driver-written MEASURED_PEAKS.json.  Fallbacks: B200_PROFILING.md's
+    figures.  The XKNN_PREC_FP32 GEMMs' peaks derive from the bf16 one (fp32_gemm_peaks)."""
     out = {"hbm": 6650.0, "bf16_burst": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -70,10 +69,28 @@ def peaks():
                    bf16_sus=p["bf16_tflops_sustained"], src="MEASURED_PEAKS.json")
     except Exception:
         pass
-    out.update(tf32_burst=1100.0, tf32_sus=1100.0,
-               tf32_src="B200_PROFILING.md dense TF32 1.1 PF/s (cuBLAS TF32 measures lower: "
-                        "profiles/r02/tf32_peak.json)")
     return out
+
+
+FP32_GEMM = os.environ.get("XKNN_FP32_GEMM", "mixed")  # the library reads the same variable
+
+
+def fp32_gemm_peaks(bf16_peak):
+    """fp32-accuracy peaks (TF/s of fp32 flops) of the XKNN_PREC_FP32 GEMMs, from the tensor-pipe
+    time each fp32 product costs with the arithmetic the library uses (fast32.cu), a kind::tf32
+    MMA taking twice a kind::f16 one (dense TF32 = bf16 / 2, as B200_PROFILING.md's 1.1 vs 2.25
+    PF/s; this repo's 3xTF32 GEMM-dX measured 835 TF/s of TF32 MMAs against bf16 / 2 = 832):
+      mixed GEMM-F: one tf32 + two bf16 MMAs = 4 bf16-MMA times  -> bf16 / 4
+      bf16x3 GEMM-dW / dX: three bf16 MMAs                        -> bf16 / 3
+      3xTF32: three tf32 MMAs = 6 bf16-MMA times                  -> bf16 / 6"""
+    f = {"mixed": 4.0, "f3": 6.0, "3xtf32": 6.0}.get(FP32_GEMM, 4.0)
+    bw = 6.0 if FP32_GEMM == "3xtf32" else 3.0
+    return {"gemm_logits_softmax": bf16_peak / f, "gemm_dW": bf16_peak / bw,
+            "gemm_dX": bf16_peak / bw}
+
+
+FP32_GEMM_SRC = ("MEASURED_PEAKS bf16 / (bf16-MMA times per fp32 product: mixed GEMM-F 4, "
+                 "bf16x3 GEMM-dW/dX 3, 3xTF32 6; bench.fp32_gemm_peaks)")
 
 
 def kernel_rooflines(phase_ms, precision, b, mw, splits, pk, burst):
@@ -83,9 +100,13 @@ def kernel_rooflines(phase_ms, precision, b, mw, splits, pk, burst):
     M_w fp32 rows read + their tensor-core operand copy written).  Peak: burst when the clocks
     sat at max with no throttle reason, else sustained."""
     f32 = precision != "bf16"
-    opb = 8 if f32 else 2  # bytes per element of a tensor-core operand copy (hi+lo | bf16)
-    tflops = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if f32 else (
-        pk["bf16_burst"] if burst else pk["bf16_sus"])
+    bf16_peak = pk["bf16_burst"] if burst else pk["bf16_sus"]
+    tpeak = fp32_gemm_peaks(bf16_peak) if f32 else {}
+    # bytes per element of the tensor-core operand copies written by the gather (W_sub) and the
+    # fixup (X_hat'): bf16 | mixed: tf32 + 3 bf16 planes, bf16x3 planes | f3: hi + lo + 2 planes,
+    # planes | 3xTF32: hi + lo, hi + lo
+    opb, opx = {"mixed": (10, 4), "f3": (12, 4), "3xtf32": (8, 8)}.get(FP32_GEMM, (10, 4)) \
+        if f32 else (2, 2)
     gemm = 2.0 * b * mw * D
     work = {
         "gemm_logits_softmax": ("tensor", gemm),
@@ -93,7 +114,7 @@ def kernel_rooflines(phase_ms, precision, b, mw, splits, pk, burst):
         "gemm_dX": ("tensor", gemm),
         "update": ("hbm", 16.0 * mw * D),
         "gather_normalize": ("hbm", (4.0 + opb) * mw * D + (4.0 + opb) * b * D),
-        "softmax_stats": ("hbm", 2.0 * math.ceil(mw / 256) * b * 4 + (4.0 + opb) * b * D),
+        "softmax_stats": ("hbm", 2.0 * math.ceil(mw / 256) * b * 4 + (4.0 + opx) * b * D),
         "dX_reduce_scatter": ("hbm", (splits + 1) * 4.0 * b * D),
         "feature_backward": ("hbm", 3 * 4.0 * b * D),
     }
@@ -103,7 +124,7 @@ def kernel_rooflines(phase_ms, precision, b, mw, splits, pk, burst):
         if not ms:
             continue
         if bound == "tensor":
-            ach, peak, unit = w / (ms / 1e3) / 1e12, tflops, "TFLOP/s"
+            ach, peak, unit = w / (ms / 1e3) / 1e12, tpeak.get(name, bf16_peak), "TFLOP/s"
         else:
             ach, peak, unit = w / (ms / 1e3) / 1e9, pk["hbm"], "GB/s"
         floor_ms += (w / (peak * (1e12 if bound == "tensor" else 1e9))) * 1e3
@@ -503,16 +524,18 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
         roof = {"bound": kd["bound"], "kernel": dom, "achieved": kd["achieved"],
                 "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
                 "work_per_launch": kd["work"], "launch_ms": kd["ms"],
-                "peak_source": (pk["tf32_src"] + " / 3 (three TF32 MMAs per fp32 product)"
+                "peak_source": (FP32_GEMM_SRC + (" burst" if burst else " sustained")
                                 if precision != "bf16" and kd["bound"] == "tensor" else
                                 pk["src"] + (" burst" if burst else " sustained")),
                 "how": "work per launch / the kernel's CUDA-event time on the layer stream "
                        "(phase_ms, second pass); dominant = the longest phase"}
         # whole-step floors: every kernel at its own roofline, serialized (the step's kernels
         # run back to back), and the SURVEY 8(d) overlap bound max(flops/peak, bytes/peak)
-        tpk = (pk["tf32_burst"] if burst else pk["tf32_sus"]) / 3 if precision != "bf16" \
-            else (pk["bf16_burst"] if burst else pk["bf16_sus"])
-        t_roof = max(6.0 * b * mw_max * D / (tpk * 1e12), 16.0 * mw_max * D / (pk["hbm"] * 1e9))
+        bpk = pk["bf16_burst"] if burst else pk["bf16_sus"]
+        gp = fp32_gemm_peaks(bpk) if precision != "bf16" else {
+            "gemm_logits_softmax": bpk, "gemm_dW": bpk, "gemm_dX": bpk}
+        t_roof = max(sum(2.0 * b * mw_max * D / (v * 1e12) for v in gp.values()),
+                     16.0 * mw_max * D / (pk["hbm"] * 1e9))
         res = {
             "metric": "KNN-softmax fwd+bwd+update samples/sec @100M classes d=512, 1/2/4/8 "
                       "B200 vs roofline",
@@ -527,7 +550,10 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
             "vs_baseline": None,
             "dtype": "bf16" if precision == "bf16" else "f32",
             "precision": {"bf16": "bf16 operands, fp32 accumulation (stated bound, DESIGN.md 2)",
-                          "fp32": "3xTF32 tensor cores, fp32 accuracy (1e-5 of the reference)",
+                          "fp32": {"mixed": "fp32 accuracy (1e-5 of the reference) on tensor cores: "
+                                            "GEMM-F tf32 + 2 bf16 cross terms, GEMM-dW/dX bf16x3",
+                                   "f3": "fp32 accuracy: GEMM-F 3xTF32, GEMM-dW/dX bf16x3",
+                                   "3xtf32": "fp32 accuracy: 3xTF32 GEMMs"}.get(FP32_GEMM, FP32_GEMM),
                           "fp32_exact": "CUDA-core fp32 in the reference's summation order"}[
                               precision],
             "data": "synthetic (W~N(0,0.05^2), X~N(0,1), uniform labels, seeded random "
@@ -554,7 +580,8 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
                               "t_roof_overlap_ms": round(t_roof * 1e3, 4),
                               "frac_overlap": round(t_roof * 1e3 / ms_step, 4),
                               "how": "serial: sum over the step's kernels of work/peak; overlap: "
-                                     "max(6*B*M_w*D/tensor peak, 16*M_w*D/HBM peak)"},
+                                     "max(sum over the 3 GEMMs of 2*B*M_w*D/its peak, "
+                                     "16*M_w*D/HBM peak)"},
             "phase_ms": {k_: round(v, 4) for k_, v in phase_ms.items()},
             "phase_profile": {"ms_per_step": round(ms_prof / args.steps, 4), "steps": args.steps,
                               "how": "second pass of the same steps with CUDA events at the "

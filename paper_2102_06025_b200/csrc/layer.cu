@@ -493,7 +493,7 @@ xknn_status_t Layer::run_step(const float* feats_local, const uint32_t* labels_l
   const uint64_t B = bl * world;
   const uint32_t D = (uint32_t)d;
   last_b = B;
-  graph_mode = !(cfg.flags & XKNN_FLAG_NO_GRAPH) && stream != nullptr;
+  graph_mode = !(cfg.flags & XKNN_FLAG_NO_GRAPH) && stream != nullptr && !debug_sync();
   if (prof_on) prof_collect(false);
   mark(0);
   // this step's selection set; a prepared selection (xknn_prepare) for this batch size is used

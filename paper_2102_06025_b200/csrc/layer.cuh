@@ -259,8 +259,15 @@ struct xknn_layer {
     cudaError_t _e = (expr);                                                   \
     if (_e != cudaSuccess) return h->L.cuda_ok(_e, __FILE__, __LINE__, #expr); \
   } while (0)
-#define XK_LAUNCH() \
-  do {              \
-    ++launches;     \
-    XK_CUDA(cudaGetLastError()); \
+// XKNN_DEBUG_SYNC=1 (diagnostics): no CUDA graphs, and a device sync after every launch site, so
+// a faulting kernel is reported at its own XK_LAUNCH line
+inline bool debug_sync() {
+  static const bool on = getenv("XKNN_DEBUG_SYNC") != nullptr;
+  return on;
+}
+#define XK_LAUNCH()                                         \
+  do {                                                      \
+    ++launches;                                             \
+    XK_CUDA(cudaGetLastError());                            \
+    if (debug_sync()) XK_CUDA(cudaDeviceSynchronize());     \
   } while (0)

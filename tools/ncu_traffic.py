@@ -19,7 +19,9 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 def phase_of(name: str) -> str:
     m = re.search(r"k_gemm[23]<[^0-9]*([0-9])", name)
     if m:
-        return {"0": "gemm_logits_softmax", "1": "gemm_dX", "2": "gemm_dW"}[m.group(1)]
+        # k_gemm2 kinds (fast.cu) and k_gemm3 kinds (fast32.cu: 3/4/6 bf16x3 dX/dW, 5 mixed F)
+        return {"0": "gemm_logits_softmax", "1": "gemm_dX", "2": "gemm_dW", "3": "gemm_dX",
+                "4": "gemm_dW", "5": "gemm_logits_softmax", "6": "gemm_dW"}[m.group(1)]
     for key, ph in (("k_update_rows", "update"), ("k_normalize_rows", "gather_normalize"),
                     ("k_zero_rows", "gather_normalize"), ("k_rowreduce", "softmax_stats"),
                     ("k_fixup", "softmax_stats"), ("k_dx_reduce", "dX_reduce_scatter"),

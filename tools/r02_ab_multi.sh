@@ -5,9 +5,9 @@
 set -u
 O=gpurun_out/abm
 mkdir -p $O
-timeout 300 python tools/ab_bitwise.py --save /tmp/abm_cur.pt > $O/bits_cur.txt 2>&1; echo "cur rc=$?"
+timeout 300 python tools/ab_bitwise.py --precision ${AB_PREC:-fp32} --save /tmp/abm_cur.pt > $O/bits_cur.txt 2>&1; echo "cur rc=$?"
 for N in "$@"; do
-  XKNN_PKG_DIR=ab/$N timeout 300 python tools/ab_bitwise.py --save /tmp/abm_$N.pt > $O/bits_$N.txt 2>&1; echo "$N rc=$?"
+  XKNN_PKG_DIR=ab/$N timeout 300 python tools/ab_bitwise.py --precision ${AB_PREC:-fp32} --save /tmp/abm_$N.pt > $O/bits_$N.txt 2>&1; echo "$N rc=$?"
 done
 python - "$@" <<'PY'
 import sys, torch
@@ -20,7 +20,7 @@ PY
 for i in 1 2; do
   for N in cur "$@"; do
     if [ $N = cur ]; then E=""; else E="XKNN_PKG_DIR=ab/$N"; fi
-    env $E timeout 300 python bench.py --precision fp32 --no-bf16-line --no-cpu-baseline --steps 50 --warmup 5 --e2e-steps 10 > $O/bench_${N}_$i.json 2> $O/bench_${N}_$i.err
+    env $E timeout 300 python bench.py --precision ${AB_PREC:-fp32} --no-bf16-line --no-cpu-baseline --steps 50 --warmup 5 --e2e-steps 10 > $O/bench_${N}_$i.json 2> $O/bench_${N}_$i.err
   done
 done
 python - <<PY
