@@ -172,6 +172,22 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
       "l"(0x1000000000000000ull)
       : "memory");
 }
+// ... with an explicit L2 cache policy (kEvictNormal / kEvictFirst / kEvictLast)
+enum : uint64_t {
+  kEvictNormal = 0x1000000000000000ull,
+  kEvictFirst = 0x12F0000000000000ull,
+  kEvictLast = 0x14F0000000000000ull
+};
+__device__ __forceinline__ void tma_load_2d_2sm_hint(void* smem_dst, const CUtensorMap* m,
+                                                     uint64_t* bar, int32_t c0, int32_t c1,
+                                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "l"(policy)
+      : "memory");
+}
 // ... multicast to the CTAs of ctamask (same smem offset in each); every destination pair's
 // leader barrier is signalled for the bytes landing in that pair
 __device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* m,
