@@ -18,7 +18,6 @@
 //   4. finalize: sort under `better`, self first, keep k.
 // compress_graph (knn_graph.cpp:235-266) of the row-distributed result is an all-to-all of
 // graph entries by owning shard (xknn_layer_rebuild_graph, layer_graph.cu).
-#include <cub/cub.cuh>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -252,31 +251,173 @@ __global__ void k_rescore(const float* __restrict__ own, uint32_t n, uint32_t d,
   }
 }
 
-// exact scores of one query row against every row of a block (keys ordered like `better`,
-// key 0 marks the query itself)
-__global__ void k_exact_scan(const float* __restrict__ q, const float* __restrict__ blk,
-                             uint32_t nc, uint32_t d, uint32_t cb, uint32_t self,
-                             uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-    uint32_t key = 0;
-    if (cb + i != self) {
-      float s = exact_dot(q, blk + (uint64_t)i * d, d);
-      if (s == 0.0f) s = 0.0f;  // -0 == +0 under `better`: one key
-      key = fkey(s);
-    }
-    keys[i] = key;
-    idx[i] = i;
+// ---- batched exact top-`need` of query rows against a block (rows whose fp16 certificate
+// failed, classify queries, the D != 512 path).  Per batch of up to kXR rows: every row's
+// exact keys against the block (the reference's dot order), then a 4-pass 8-bit radix select
+// per row for the `need`-th best key T, then the keys above T plus the first ties of T in column
+// order (`better` breaks score ties to the lower id), sentinel-padded when the block has fewer.
+// Replaces a scan + a full CUB sort per row and block.
+constexpr uint32_t kXR = 16;        // query rows per batch (their rows staged in smem)
+constexpr uint32_t kXChunk = 4096;  // columns per select block
+
+struct XSel {
+  uint32_t prefix, mask, rem, gtn, done;  // T's bits so far, their mask, ties still to take,
+};                                        // keys above T, fewer valid keys than `need`
+
+__global__ void k_xinit(XSel* st, uint32_t nr, uint32_t need, uint32_t* ctr) {
+  const uint32_t u = threadIdx.x;
+  if (u < nr) {
+    st[u] = XSel{0u, 0u, need, 0u, 0u};
+    ctr[u] = 0;
   }
 }
 
-// first `need` entries of a descending-sorted scan as (score, global id); sentinels pad
-__global__ void k_take(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                       uint32_t nc, uint32_t need, uint32_t cb, float2* __restrict__ out) {
-  for (uint32_t e = threadIdx.x; e < need; e += blockDim.x) {
-    float2 v = make_float2(-INFINITY, __uint_as_float(0xffffffffu));
-    if (e < nc && keys[e] != 0) v = make_float2(funkey(keys[e]), __uint_as_float(cb + idx[e]));
-    out[e] = v;
+// keys[u][i]: the order-preserving key of the exact score of query row rows[u] against block
+// row i (0 = the query itself, self id = self_base + rows[u]; self_base = ~0: no self)
+__global__ void k_xscan_rows(const float* __restrict__ q, const uint32_t* __restrict__ rows,
+                             uint32_t nr, uint32_t self_base, const float* __restrict__ blk,
+                             uint32_t nc, uint32_t d, uint32_t cb, uint32_t* __restrict__ keys) {
+  extern __shared__ float sq[];  // nr x d
+  for (uint32_t t = threadIdx.x; t < nr * d; t += blockDim.x)
+    sq[t] = q[(uint64_t)rows[t / d] * d + t % d];
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    const float* col = blk + (uint64_t)i * d;
+    for (uint32_t u = 0; u < nr; ++u) {
+      uint32_t key = 0;
+      if (self_base == 0xffffffffu || cb + i != self_base + rows[u]) {
+        float sc = exact_dot(sq + (uint64_t)u * d, col, d);
+        if (sc == 0.0f) sc = 0.0f;  // -0 == +0 under `better`: one key
+        key = fkey(sc);
+      }
+      keys[(uint64_t)u * nc + i] = key;
+    }
   }
+}
+
+// radix-select pass: histogram of the `shift` digit over the keys matching the prefix so far
+__global__ void k_xhist(const uint32_t* __restrict__ keys, uint32_t nc, const XSel* __restrict__ st,
+                        uint32_t* __restrict__ hist, uint32_t shift) {
+  __shared__ uint32_t h[256];
+  const uint32_t u = blockIdx.y;
+  const XSel x = st[u];
+  if (x.done) return;  // uniform per block
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t* k = keys + (uint64_t)u * nc;
+  const uint32_t i1 = min(nc, (blockIdx.x + 1) * kXChunk);
+  for (uint32_t i = blockIdx.x * kXChunk + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t key = k[i];
+    if (key != 0 && (key & x.mask) == x.prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[u * 256 + threadIdx.x], h[threadIdx.x]);
+}
+
+// ... and the digit of the rem-th best key; clears the histogram for the next pass
+__global__ void k_xpick(uint32_t* __restrict__ hist, XSel* __restrict__ st, uint32_t shift,
+                        uint32_t need) {
+  __shared__ uint32_t h[256];
+  const uint32_t u = blockIdx.x;
+  h[threadIdx.x] = hist[u * 256 + threadIdx.x];
+  hist[u * 256 + threadIdx.x] = 0;
+  __syncthreads();
+  if (threadIdx.x) return;
+  XSel x = st[u];
+  if (x.done) return;
+  uint32_t tot = 0;
+  for (int dg = 0; dg < 256; ++dg) tot += h[dg];
+  if (shift == 24 && tot < x.rem) {  // fewer valid keys than `need`: take them all (T = 0)
+    st[u] = XSel{0u, 0u, 0u, tot, 1u};
+    return;
+  }
+  uint32_t above = 0;
+  for (int dg = 255; dg >= 0; --dg) {
+    if (above + h[dg] >= x.rem) {
+      x.prefix |= (uint32_t)dg << shift;
+      x.mask |= 255u << shift;
+      x.rem -= above;
+      break;
+    }
+    above += h[dg];
+  }
+  if (shift == 0) x.gtn = need - x.rem;
+  st[u] = x;
+}
+
+// ties of T per chunk, then their exclusive prefix over the chunks (column order)
+__global__ void k_xties(const uint32_t* __restrict__ keys, uint32_t nc, const XSel* __restrict__ st,
+                        uint32_t* __restrict__ tiecnt, uint32_t nchunks) {
+  __shared__ uint32_t c;
+  const uint32_t u = blockIdx.y;
+  const XSel x = st[u];
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  if (!x.done && x.rem) {
+    const uint32_t* k = keys + (uint64_t)u * nc;
+    const uint32_t i1 = min(nc, (blockIdx.x + 1) * kXChunk);
+    uint32_t m = 0;
+    for (uint32_t i = blockIdx.x * kXChunk + threadIdx.x; i < i1; i += blockDim.x)
+      m += k[i] == x.prefix;
+    if (m) atomicAdd(&c, m);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tiecnt[(uint64_t)u * nchunks + blockIdx.x] = c;
+}
+__global__ void k_xtiescan(uint32_t* __restrict__ tiecnt, uint32_t nchunks) {
+  uint32_t* t = tiecnt + (uint64_t)blockIdx.x * nchunks;
+  uint32_t run = 0;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    const uint32_t v = t[c];
+    t[c] = run;
+    run += v;
+  }
+}
+
+// the keys above T (any order) and the first `rem` ties of T in column order, as (score, id)
+__global__ void k_xcollect(const uint32_t* __restrict__ keys, uint32_t nc, uint32_t cb,
+                           const XSel* __restrict__ st, const uint32_t* __restrict__ tieoff,
+                           uint32_t nchunks, float2* __restrict__ out, uint64_t ostride,
+                           uint32_t* __restrict__ ctr) {
+  __shared__ uint32_t wcnt[8];
+  const uint32_t u = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const XSel x = st[u];
+  const uint32_t T = x.done ? 0u : x.prefix;
+  const bool ties = !x.done && x.rem;
+  const uint32_t* k = keys + (uint64_t)u * nc;
+  float2* o = out + (uint64_t)u * ostride;
+  uint32_t run = ties ? tieoff[(uint64_t)u * nchunks + blockIdx.x] : 0;
+  const uint32_t i0 = blockIdx.x * kXChunk, i1 = min(nc, i0 + kXChunk);
+  for (uint32_t base = i0; base < i1; base += blockDim.x) {  // uniform trip count
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t key = i < i1 ? k[i] : 0u;
+    if (key > T) o[atomicAdd(&ctr[u], 1u)] = make_float2(funkey(key), __uint_as_float(cb + i));
+    if (!ties) continue;
+    const bool tie = key == T && key != 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, tie);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    uint32_t before_w = 0, all = 0;
+    for (uint32_t v = 0; v < blockDim.x / 32; ++v) {
+      before_w += v < w ? wcnt[v] : 0u;
+      all += wcnt[v];
+    }
+    if (tie) {
+      const uint32_t r = run + before_w + __popc(bal & ((1u << lane) - 1u));
+      if (r < x.rem) o[x.gtn + r] = make_float2(funkey(key), __uint_as_float(cb + i));
+    }
+    run += all;
+    __syncthreads();
+  }
+}
+
+// sentinel padding of rows with fewer valid keys than `need`
+__global__ void k_xpad(const XSel* __restrict__ st, float2* __restrict__ out, uint64_t ostride,
+                       uint32_t need) {
+  const XSel x = st[blockIdx.x];
+  if (!x.done) return;
+  for (uint32_t e = x.gtn + threadIdx.x; e < need; e += blockDim.x)
+    out[(uint64_t)blockIdx.x * ostride + e] = make_float2(-INFINITY, __uint_as_float(0xffffffffu));
 }
 
 // Step 4, one warp per row: sort the row's exactly scored candidates under `better` (warp
@@ -389,43 +530,6 @@ __global__ void k_self_only(uint32_t n, uint32_t row_base, uint32_t* out) {
 
 }  // namespace
 
-// Exact rows by full scans at P = 1 (the whole graph for D != 512).
-static cudaError_t exact_rows(const float* wn, uint32_t n, uint32_t d, uint32_t k,
-                              uint32_t* out, cudaStream_t s) {
-  uint32_t* keys = nullptr;
-  void* tmp = nullptr;
-  size_t tb = 0;
-  float2* row = nullptr;
-  cudaError_t e = cudaMalloc(&keys, (size_t)n * 16);
-  if (e != cudaSuccess) return e;
-  uint32_t* idx = keys + n;
-  uint32_t* keys2 = keys + 2 * (size_t)n;
-  uint32_t* idx2 = keys + 3 * (size_t)n;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, keys2, idx, idx2, (int)n, 0, 32, s);
-  e = cudaMalloc(&tmp, tb);
-  if (e == cudaSuccess) e = cudaMalloc(&row, (size_t)std::max<uint32_t>(k, 1) * sizeof(float2));
-  std::vector<float2> h(k);
-  for (uint32_t j = 0; j < n && e == cudaSuccess; ++j) {
-    k_exact_scan<<<grid_for(n, 256), 256, 0, s>>>(wn + (uint64_t)j * d, wn, n, d, 0, j, keys, idx);
-    size_t t2 = tb;
-    e = cub::DeviceRadixSort::SortPairsDescending(tmp, t2, keys, keys2, idx, idx2, (int)n, 0, 32, s);
-    if (e != cudaSuccess) break;
-    k_take<<<1, 128, 0, s>>>(keys2, idx2, n, k - 1, 0, row);
-    e = cudaMemcpyAsync(h.data(), row, (size_t)(k - 1) * sizeof(float2), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    std::vector<uint32_t> r(k);
-    r[0] = j;
-    for (uint32_t t = 1; t < k; ++t) std::memcpy(&r[t], &h[t - 1].y, 4);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(out + (uint64_t)j * k, r.data(), (size_t)k * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  }
-  cudaStreamSynchronize(s);
-  cudaFree(row);
-  cudaFree(tmp);
-  cudaFree(keys);
-  return e;
-}
 
 namespace {
 // RAII device scratch, stream-ordered from the device's default memory pool.  Freed blocks stay
@@ -463,6 +567,83 @@ struct Dev {
       }
   }
 };
+
+// The `need` best (score, global id) under `better` of query rows rows_dev[0..nr) of q (d floats
+// each) against blk (nc rows, global ids cb..), excluding id self_base + rows[u] (~0: none):
+// out[u * ostride + e], e < need, in no particular order (k_finalize / k_top1 sort), sentinel-
+// padded where the block has fewer.  Bit-identical to a full descending sort of the exact keys
+// (stable on the column index) and its first `need` entries.
+cudaError_t exact_topk(const float* q, const uint32_t* rows_dev, uint32_t nr, uint32_t self_base,
+                       const float* blk, uint32_t nc, uint32_t d, uint32_t cb, uint32_t need,
+                       float2* out, uint64_t ostride, Dev& mem, cudaStream_t s) {
+  if (!nr || !need) return cudaSuccess;
+  uint32_t R = std::min<uint32_t>(kXR, std::max<uint32_t>(1u, 12288u / d));  // rows in 48 KB smem
+  R = std::min<uint64_t>(R, std::max<uint64_t>(1, (256ull << 20) / 4 / std::max(nc, 1u)));
+  const uint32_t nchunks = (nc + kXChunk - 1) / kXChunk;
+  uint32_t *keys = nullptr, *hist = nullptr, *tie = nullptr, *ctr = nullptr;
+  XSel* st = nullptr;
+  cudaError_t e;
+  if ((e = mem.get(&keys, (uint64_t)R * nc)) != cudaSuccess) return e;
+  if ((e = mem.get(&hist, (uint64_t)R * 256)) != cudaSuccess) return e;
+  if ((e = mem.get(&tie, (uint64_t)R * nchunks)) != cudaSuccess) return e;
+  if ((e = mem.get(&ctr, R)) != cudaSuccess) return e;
+  if ((e = mem.get(&st, R)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(hist, 0, (size_t)R * 256 * 4, s)) != cudaSuccess) return e;
+  const unsigned sgrid = grid_for(nc, 256, 148u * 8u);
+  for (uint32_t u0 = 0; u0 < nr; u0 += R) {
+    const uint32_t r = std::min(R, nr - u0);
+    float2* o = out + (uint64_t)u0 * ostride;
+    k_xinit<<<1, 32, 0, s>>>(st, r, need, ctr);
+    k_xscan_rows<<<sgrid, 256, (size_t)r * d * 4, s>>>(q, rows_dev + u0, r, self_base, blk, nc, d,
+                                                       cb, keys);
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      k_xhist<<<dim3(nchunks, r), 256, 0, s>>>(keys, nc, st, hist, (uint32_t)shift);
+      k_xpick<<<r, 256, 0, s>>>(hist, st, (uint32_t)shift, need);
+    }
+    k_xties<<<dim3(nchunks, r), 256, 0, s>>>(keys, nc, st, tie, nchunks);
+    k_xtiescan<<<r, 1, 0, s>>>(tie, nchunks);
+    k_xcollect<<<dim3(nchunks, r), 256, 0, s>>>(keys, nc, cb, st, tie, nchunks, o, ostride, ctr);
+    k_xpad<<<r, 128, 0, s>>>(st, o, ostride, need);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+__global__ void k_iota_rows(uint32_t* rows, uint32_t* flag, uint32_t n) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    rows[j] = j;
+    flag[j] = j + 1;
+  }
+}
+
+// Exact rows by full scans at P = 1 (the whole graph for D != 512): every row's exact k-1 best
+// (exact_topk), then self first + sorted by k_finalize.
+cudaError_t exact_rows(const float* wn, uint32_t n, uint32_t d, uint32_t k, uint32_t* out,
+                       cudaStream_t s) {
+  Dev mem(s);
+  const uint32_t need = k - 1;
+  uint32_t *rows = nullptr, *flag = nullptr;
+  float2* ubuf = nullptr;
+  cudaError_t e;
+  if ((e = mem.get(&rows, n)) != cudaSuccess) return e;
+  if ((e = mem.get(&flag, n)) != cudaSuccess) return e;
+  if ((e = mem.get(&ubuf, (uint64_t)n * need)) != cudaSuccess) return e;
+  k_iota_rows<<<grid_for(n, 256), 256, 0, s>>>(rows, flag, n);
+  if ((e = exact_topk(wn, rows, n, 0, wn, n, d, 0, need, ubuf, need, mem, s)) != cudaSuccess)
+    return e;
+  uint32_t cap = 1;
+  while (cap < need) cap <<= 1;
+  const uint32_t warps = 4;
+  const size_t smem = (size_t)warps * cap * 8;
+  if (smem > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem)) != cudaSuccess)
+    return e;
+  k_finalize<<<grid_for((uint64_t)n * 32, warps * 32, 148u * 32u), warps * 32, smem, s>>>(
+      n, 0, k, 1, cap, nullptr, nullptr, nullptr, flag, ubuf, need, out);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
 
 inline void shard_range_of(uint64_t n, uint64_t p, uint64_t s, uint64_t* b, uint64_t* e) {
   const uint64_t base = n / p, rem = n % p;
@@ -694,8 +875,6 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   uint32_t nu = 0;
   G_CUDA(cudaMemcpyAsync(&nu, unc, 4, cudaMemcpyDeviceToHost, s));
   G_CUDA(cudaStreamSynchronize(s));
-  std::vector<uint32_t> urows(nu);
-  if (nu) G_CUDA(cudaMemcpy(urows.data(), unc + 1, (size_t)nu * 4, cudaMemcpyDeviceToHost));
   if (stats) stats->uncertified_rows = nu;
 
   // ---- 3. exact ring (fp32) ----
@@ -708,19 +887,7 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
   }
   const uint32_t ulen = (uint32_t)world * need;
   float2* ubuf = nullptr;
-  uint32_t *keys = nullptr, *kidx = nullptr, *keys2 = nullptr, *kidx2 = nullptr;
-  void* stmp = nullptr;
-  size_t stb = 0;
-  if (nu) {
-    G_CUDA(mem.get(&ubuf, (uint64_t)nu * ulen));
-    G_CUDA(mem.get(&keys, maxrows * 4));
-    kidx = keys + maxrows;
-    keys2 = keys + 2 * maxrows;
-    kidx2 = keys + 3 * maxrows;
-    G_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, stb, keys, keys2, kidx, kidx2,
-                                                     (int)maxrows, 0, 32, s));
-    G_CUDA(mem.get(reinterpret_cast<uint8_t**>(&stmp), stb));
-  }
+  if (nu) G_CUDA(mem.get(&ubuf, (uint64_t)nu * ulen));
   const float* held32 = wn;
   for (int h = 0; h < world; ++h) {
     const int o = (rank - h + world) % world;
@@ -748,17 +915,9 @@ xknn_status_t graph_build(const float* wn, uint64_t n_total, uint64_t d64, uint3
     k_rescore<<<grid_for((uint64_t)n * 32, 256), 256, kRescoreSmem, s>>>(wn, n, 512, list, lcnt, flag, kc,
                                                               held32, (uint32_t)cb, nc, ex);
     G_CUDA(cudaGetLastError());
-    for (uint32_t u = 0; u < nu; ++u) {  // rows without a certificate: exact scan of the block
-      const uint32_t j = urows[u];
-      k_exact_scan<<<grid_for(nc, 256), 256, 0, s>>>(wn + (uint64_t)j * 512, held32, nc, 512,
-                                                     (uint32_t)cb, row_base + j, keys, kidx);
-      size_t t2 = stb;
-      G_CUDA(cub::DeviceRadixSort::SortPairsDescending(stmp, t2, keys, keys2, kidx, kidx2, (int)nc,
-                                                       0, 32, s));
-      k_take<<<1, 128, 0, s>>>(keys2, kidx2, nc, need, (uint32_t)cb,
-                               ubuf + (uint64_t)u * ulen + (uint64_t)h * need);
-      G_CUDA(cudaGetLastError());
-    }
+    // rows without a certificate: exact top-`need` against the whole block, batched
+    G_CUDA(exact_topk(wn, unc + 1, nu, row_base, held32, nc, 512, (uint32_t)cb, need,
+                      ubuf + (uint64_t)h * need, ulen, mem, s));
     if (h + 1 < world) {
       G_CUDA(cudaStreamWaitEvent(s, ev_recv, 0));
       held32 = buf32[h % 2];
@@ -865,28 +1024,9 @@ xknn_status_t retrieval_top1_local(const float* qn, uint32_t nq, const float* wn
     G_CUDA(cudaStreamSynchronize(s));
   }
   float2* ubuf = nullptr;
-  if (nu) {
-    std::vector<uint32_t> urows(nu);
-    G_CUDA(cudaMemcpy(urows.data(), unc + 1, (size_t)nu * 4, cudaMemcpyDeviceToHost));
-    uint32_t* keys = nullptr;
-    void* stmp = nullptr;
-    size_t stb = 0;
+  if (nu) {  // queries without a certificate: exact best against every class row, batched
     G_CUDA(mem.get(&ubuf, nu));
-    G_CUDA(mem.get(&keys, (uint64_t)nw * 4));
-    uint32_t *kidx = keys + nw, *keys2 = keys + 2 * (uint64_t)nw, *kidx2 = keys + 3 * (uint64_t)nw;
-    G_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, stb, keys, keys2, kidx, kidx2,
-                                                     (int)nw, 0, 32, s));
-    G_CUDA(mem.get(reinterpret_cast<uint8_t**>(&stmp), stb));
-    for (uint32_t u = 0; u < nu; ++u) {
-      const uint32_t j = urows[u];
-      k_exact_scan<<<grid_for(nw, 256), 256, 0, s>>>(qn + (uint64_t)j * d, wn, nw, d, col_base,
-                                                     0xffffffffu, keys, kidx);
-      size_t t2 = stb;
-      G_CUDA(cub::DeviceRadixSort::SortPairsDescending(stmp, t2, keys, keys2, kidx, kidx2, (int)nw,
-                                                       0, 32, s));
-      k_take<<<1, 32, 0, s>>>(keys2, kidx2, nw, 1, col_base, ubuf + u);
-      G_CUDA(cudaGetLastError());
-    }
+    G_CUDA(exact_topk(qn, unc + 1, nu, 0xffffffffu, wn, nw, d, col_base, 1, ubuf, 1, mem, s));
   }
   k_top1<<<grid_for((uint64_t)nq * 32, 256), 256, 0, s>>>(nq, kc, list, lcnt, ex, flag, ubuf,
                                                           best_score, best_id);

@@ -43,6 +43,25 @@ def test_graph_ties_and_near_duplicates():
     assert rc == 0 and np.array_equal(got, want)
 
 
+def test_graph_many_uncertified_rows():
+    """Groups of 20 rows within 1e-4 of each other (half of them exact copies): a row's k-1
+    best lie inside its group, closer together than the fp16 certificate can separate, so most
+    rows are uncertified and come from the batched exact top-k (many 16-row batches, exact ties
+    spanning the 4096-column select chunks, resolved to the lower ids): bit-exact vs the
+    oracle."""
+    rng = np.random.default_rng(13)
+    base = np.repeat(rng.standard_normal((500, 512)).astype(np.float32), 20, axis=0)
+    noise = 1e-4 * rng.standard_normal(base.shape).astype(np.float32)
+    noise[::2] = 0.0  # exact copies: ties
+    w = (base + noise)[rng.permutation(10000)]
+    w = np.concatenate([w, rng.standard_normal((2000, 512)).astype(np.float32)])
+    wn = _normalized(w)
+    got, unc = _device_graph(wn, 12)
+    rc, want = O.bruteforce_graph("oracle", wn, 12)
+    assert rc == 0 and np.array_equal(got, want)
+    assert unc > 32, unc  # the batched exact path ran for several 16-row batches
+
+
 def test_graph_small_dim_exact_path():
     wn = _normalized(np.random.default_rng(2).standard_normal((400, 64)).astype(np.float32))
     got, _ = _device_graph(wn, 5)
