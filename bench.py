@@ -17,8 +17,8 @@ normalize-backward, sparse momentum-SGD update of the active rows.
 
 Workloads (BASELINE.json configs, D = 512, M = 10% N, s = 30, lr = 0.1, mu = 0.9):
     c1  N=100K  B=256   k=10    (the reference's CPU-runnable case; parity config)
-    c2  N=1M    B=1024  k=50    single B200 -- the default at N=1 (configs[1])
-    c3  N=10M   B=4096  k=100   class-sharded over 2/4/8 GPUs -- the default at N>1 (strong)
+    c2  N=1M    B=1024  k=50    the default at every N (configs[1]; strong-scaled over N GPUs)
+    c3  N=10M   B=4096  k=100   class-sharded over 2/4/8 GPUs (--workload c3)
     c4  N=100M  B=8192  k=100   8 GPUs (paper headline scale); 25M classes/GPU on 4 GPUs
     c4r N=12.5M B=8192  k=100   one GPU: the per-rank work of C4 on 8 GPUs
 Synthetic data: W ~ N(0, 0.05^2), features ~ N(0,1), labels uniform, a seeded self-first random
@@ -651,7 +651,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    wl_name = args.workload or ("c2" if world == 1 else "c3")
+    # the same workload at every N (strong scaling over the class shards), so the per-N lines
+    # compare like for like; C3 / C4 run with --workload (their lines are in profiles/r02/)
+    wl_name = args.workload or "c2"
     wl = WORKLOADS[wl_name]
 
     if args.impl == "reference":
