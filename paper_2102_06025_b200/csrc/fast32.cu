@@ -906,6 +906,8 @@ xknn_status_t Layer::init_fast32() {
   f->mwpad = (uint32_t)((mw_cap + 255) / 256 * 256);
   ldp = f->mwpad;
   if (const char* e = getenv("XKNN_FP32_GEMM")) {
+    if (strcmp(e, "mixed") && strcmp(e, "f3") && strcmp(e, "3xtf32"))
+      return fail_msg(XKNN_ERR_CONFIG, "XKNN_FP32_GEMM must be mixed, f3 or 3xtf32");
     f->mixed = strcmp(e, "mixed") == 0;
     f->bfb = strcmp(e, "3xtf32") != 0;
   }
