@@ -1003,6 +1003,7 @@ __global__ void k_dx_reduce(const float* __restrict__ partial, const double* __r
     const uint32_t b = (uint32_t)(e / 128), c4 = (uint32_t)(e % 128);
     const uint32_t bt = b / rows_per_unit, row = b % rows_per_unit;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8  // 8 partial loads in flight per thread; the sum stays in split order
     for (uint32_t s = 0; s < splits; ++s) {
       const float4 v = reinterpret_cast<const float4*>(
           partial + ((uint64_t)(s * nbt + bt) * rows_per_unit + row) * 512)[c4];
