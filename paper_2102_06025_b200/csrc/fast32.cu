@@ -1,28 +1,34 @@
-// fast32.cu -- XKNN_PREC_FP32: the three fc GEMMs at fp32 accuracy on 5th-gen tensor cores, by
-// 3xTF32 operand splitting (tcgen05.mma kind::tf32, accumulators in TMEM, operands staged by TMA).
+// fast32.cu -- XKNN_PREC_FP32: the three fc GEMMs at fp32 accuracy on 5th-gen tensor cores
+// (tcgen05.mma, accumulators in TMEM, operands staged by TMA), by operand splitting.  A single
+// TF32 (2^-11) or bf16 pass misses the north star's 1e-5 relative tolerance of the fp32 reference
+// (matrix.cpp:57-98); each GEMM uses the cheapest split that meets it:
+//   GEMM-F  (kFm, "mixed"): a_t = tf32(a);  a*b ~ a_t*b_t [kind::tf32] + bf16(a)*bf16(b - b_t)
+//           + bf16(a - a_t)*bf16(b) [kind::f16] -- 2 TF32-MMA-equivalents per product; the
+//           exp(s*S - s) epilogue multiplies logit errors by s = 30, so the leading product keeps
+//           tf32 precision (a plain bf16x3 GEMM-F would leave 6e-6 relative errors in P~)
+//   GEMM-dW (kDWh) / GEMM-dX (kDXb), "bf16x3": hi = bf16(a), lo = bf16(a - hi);  a*b ~
+//           lo*hi + hi*lo + hi*hi [kind::f16] -- 1.5 TF32-equivalents; no amplification downstream
+//   XKNN_FP32_GEMM=3xtf32 (kF3 / kDW3 / kDX3): hi = tf32(a), lo = a - hi;  lo*hi + hi*lo + hi*hi
+//           [kind::tf32], |error| <~ 2^-21 |a*b| -- 3 TF32-equivalents ("f3": kF3 + bf16x3)
+// Measured against the reference, all three give the same errors to within its own fp32
+// rounding.
 //
-// Every fp32 operand a is stored as a_hi = tf32(a) (round to nearest) and a_lo = a - a_hi (exact
-// in fp32; the tensor core keeps its top 11 significant bits), and each product is
-//   a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi        (|error| <~ 2^-21 |a*b|, fp32 accumulation)
-// -- three kind::tf32 MMAs into the same TMEM accumulator.  This meets the north star's 1e-5
-// relative tolerance of the fp32 reference (matrix.cpp:57-98), which a single TF32 (2^-11) or
-// bf16 pass does not.
-//
-// The step has the BF16 path's structure (fast.cu), with fp32 hi/lo operands in place of bf16:
+// The step has the BF16 path's structure (fast.cu):
 //   GEMM-F   S = X_hat * W_subᵀ   (M = 256 batch rows / CTA pair, N = 256 classes, K = 512)
-//            epilogue: P~ = exp(s*S - s) (fixed stabilizer, |cos| <= 1), split hi/lo -> HBM,
-//            per-tile row sums and the label logit (as fast.cu)
-//   GEMM-dW  dW  = P~ᵀ * (diag(s*r) X_hat)     (M = 256 classes, N = 512, K = B) -> fp32 rows
+//            epilogue: P~ = exp(s*S - s) (fixed stabilizer, |cos| <= 1) -> HBM as bf16 hi / lo
+//            planes (fp32, or hi / lo fp32 in the 3xTF32 mode), per-tile row sums and the label
+//            logit (as fast.cu)
+//   GEMM-dW  dW  = P~ᵀ * (diag(s*r) X_hat)     (M = 256 classes, K = B) -> fp32 rows
 //   GEMM-dX  dX  = diag(s*r) * (P~ * W_sub)    (M = 256 batch, N = 512, K = M_w split) -> fp32
 // with r_b = 1 / (B * sum_b); the one-hot part of G is applied exactly in fp32 by k_dx_reduce and
 // the row update (LabelFix), as on the BF16 path.
 //
-// Shared-memory tiles (per CTA of a cta_group::2 pair; 128B swizzle unless noted):
-//   F : A = X_hat rows   K-major, 128 rows x 32 fp32 (128 B), hi + lo;  B = W_sub rows, same
-//   dX: A = P~ rows      K-major, 128 rows x 16 fp32 (64 B, 64B swizzle), hi + lo
-//       B = W_sub        MN-major (d contiguous): 2 N-halves x 4 atoms of 32 d x 16 K rows
-//   dW: A = P~ᵀ          MN-major (classes contiguous): 4 atoms of 32 classes x 16 K rows
-//       B = X_hat'       MN-major, as dX's B
+// Shared-memory tiles (per CTA of a cta_group::2 pair; layouts per kind at their Cfg3):
+//   kFm : tf32 rows (32 fp32 = 128 B, SW128) + the two bf16 planes (64-B rows, SW64), A and B
+//   kDXb/kDWh: the BF16 path's layouts with 32 K per stage, hi | lo planes side by side
+//   kF3 : A = X_hat rows / B = W_sub rows, K-major 128 rows x 32 fp32, hi + lo
+//   kDX3: A = P~ rows K-major 16 fp32 (64B swizzle); B = W_sub MN-major 4 atoms of 32 d x 16 K
+//   kDW3: A = P~ᵀ MN-major 4 atoms of 32 classes x 16 K rows; B = X_hat' as dX's B
 // MN-major tf32 operands exist only in the 128B swizzle with 32-byte granules (UMMA layout type
 // SWIZZLE_128B_BASE32B: 128 B along MN x 4 K rows per atom, granules XORed with row % 4), loaded
 // by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; LBO = stride between MN atoms, SBO = stride
