@@ -515,7 +515,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
         dom = max(kern, key=lambda k_: kern[k_]["ms"])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "r02", f"traffic_{wl_name}_{precision}.json")
-        if os.path.exists(tp):
+        if world == 1 and os.path.exists(tp):  # captured on one GPU: per-rank shapes differ at N > 1
             try:
                 traffic = json.load(open(tp)).get(dom)
             except Exception:
