@@ -1279,7 +1279,7 @@ xknn_status_t Layer::run_fast_core(uint64_t B) {
       XK_NCCL(ncclAllReduce(rowred, rowred, 3 * B, ncclDouble, ncclSum, comm, stream));
     }
   }
-  // (d) label-column fix-up of P~ and the row-scaled X_hat', and the loss (block 0)
+  // (d) the row-scaled X_hat', the label lists and the loss (block 0)
   launch_pdl(k_fixup<4>, grid_for((uint64_t)f->bpad * 32, 256), 256, 0, stream, rowred, label_col,
              X, xnorm, (uint32_t)B, f->bpad, D, cfg.scale, f->lab_head, f->lab_next, Xs16,
              loss_dev, st, err);
