@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--prepare", action="store_true", help="pipelined selection (xknn_prepare)")
     ap.add_argument("--micro", type=int, default=1, help="StepOptions::micro_batches")
+    ap.add_argument("--compact", action="store_true",
+                    help="save only the changed weight rows (their local ids and deltas)")
     args = ap.parse_args()
 
     import torch
@@ -73,7 +75,14 @@ def main():
         res[f"loss_{s}"] = layer.train_step(xs, ys, 0.1, grad_features_local=gf,
                                             micro_batches=args.micro)
         res[f"gf_{s}"] = gf.cpu().numpy()
-    res["w"] = layer.weights().cpu().numpy()
+    wg = layer.weights().cpu().numpy()
+    if args.compact:
+        w0 = w[layer.begin:layer.end]
+        rows = np.flatnonzero(np.any(wg != w0, axis=1))
+        res["w_rows"] = rows.astype(np.int64)
+        res["w_delta"] = wg[rows] - w0[rows]
+    else:
+        res["w"] = wg
     np.savez(os.path.join(args.out, f"rank{rank}.npz"), **res)
     layer.close()
     X.nccl_comm_destroy(comm)

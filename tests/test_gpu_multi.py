@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle_lib as O
-from gpu_util import BF16_GRAD, BF16_LOSS, rel_err
+from gpu_util import BF16_GRAD, BF16_LOSS, parity_record, rel_err
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -62,6 +62,49 @@ def test_multi_gpu_step(p, m, precision, tol_loss, tol_g, tmp_path):
     assert rel_err(wg - w, w_or - w) <= tol_g
     untouched = np.all(w_or == w, axis=1)
     assert np.array_equal(wg[untouched], w[untouched])
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("precision,tol_loss,tol_g", [("fp32tc", 1e-5, 1e-5),
+                                                     ("bf16", BF16_LOSS, BF16_GRAD)])
+def test_multi_gpu_step_c2(p, precision, tol_loss, tol_g, tmp_path):
+    """One step at the benchmarked C2 geometry (N = 1M, B = 1024, k = 50, M = 100K -- bench.py's
+    workload at every N) class-sharded over P GPUs vs the oracle at the same P: bit-exact
+    ActiveSet, loss / feature gradient / weight update within the precision's bound, the same
+    set of updated rows."""
+    if _ngpus() < p:
+        pytest.skip(f"needs {p} GPUs")
+    n, b, k, m = 1_000_000, 1024, 50, 100_000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+           "--master-addr=127.0.0.1", f"--master-port={29620 + p}",
+           os.path.join(HERE, "mp_worker.py"), "--out", str(tmp_path), "--num-classes", str(n),
+           "--batch", str(b), "--knn", str(k), "--m-active", str(m), "--steps", "1",
+           "--precision", precision, "--compact"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(os.path.join(tmp_path, f"rank{i}.npz")) for i in range(p)]
+
+    from mp_worker import problem
+
+    w, g = problem(n, 512, k, 7)
+    shards = [O.compress(g, p, s) for s in range(p)]
+    w_or, v_or = w.copy(), np.zeros_like(w)
+    rng = np.random.default_rng(99)
+    x = rng.standard_normal((b, 512)).astype(np.float32)
+    lab = rng.integers(0, n, b).astype(np.uint32)
+    rc, loss_or, act, gf_or, _ = O.fc_train_step(w_or, v_or, x, lab, shards, m, 42)
+    assert rc == 0
+    assert np.array_equal(np.concatenate([r["active_0"] for r in res]), act)
+    for r in res:
+        assert abs(float(r["loss_0"]) - loss_or) <= tol_loss * abs(loss_or)
+    assert rel_err(np.concatenate([r["gf_0"] for r in res]), gf_or) <= tol_g
+    rows = np.concatenate([r["w_rows"] + int(r["begin"]) for r in res])
+    assert np.array_equal(rows, np.flatnonzero(np.any(w_or != w, axis=1)))  # same rows touched
+    delta = np.concatenate([r["w_delta"] for r in res])
+    e = rel_err(delta, (w_or - w)[rows])
+    parity_record(f"multi_c2_{precision}_p{p}", loss_rel=abs(float(res[0]["loss_0"]) - loss_or) / abs(loss_or),
+                  update_relF=e)
+    assert e <= tol_g
 
 
 @pytest.mark.parametrize("p,micro", [(2, 3), (4, 2)])
