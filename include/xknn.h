@@ -55,9 +55,10 @@ typedef enum {
   /* CUDA-core fp32 with the reference's summation order (matrix.cpp:57-98), logits
      materialized and bit-identical; any scale */
   XKNN_PREC_FP32_EXACT = 1,
-  /* tcgen05/TMEM tensor cores at fp32 accuracy: 3xTF32 split operands (hi*hi + hi*lo + lo*hi,
-     kind::tf32), fp32 accumulation; within 1e-5 relative of the fp32 reference.  Needs
-     0 < scale <= 40 (fixed softmax stabilizer). */
+  /* tcgen05/TMEM tensor cores at fp32 accuracy from split operands, fp32 accumulation: logits
+     GEMM tf32 leading product + two bf16 cross terms, gradient GEMMs bf16x3 (environment
+     XKNN_FP32_GEMM=3xtf32: 3xTF32 throughout); within 1e-5 relative of the fp32 reference.
+     Needs 0 < scale <= 40 (fixed softmax stabilizer). */
   XKNN_PREC_FP32 = 2
 } xknn_precision_t;
 

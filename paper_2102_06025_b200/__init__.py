@@ -30,7 +30,7 @@ VP = C.c_void_p
 
 PREC_BF16 = 0
 PREC_FP32_EXACT = 1
-PREC_FP32 = 2  # 3xTF32 tensor cores, fp32 accuracy
+PREC_FP32 = 2  # tensor cores at fp32 accuracy (split operands; include/xknn.h)
 FLAG_NO_GRAPH = 1
 FLAG_SELECT_ONLY = 2
 
