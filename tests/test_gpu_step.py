@@ -315,3 +315,19 @@ def test_step_active_capacity_exceeded(precision):
     assert np.isfinite(loss)
     small.close()
     roomy.close()
+
+
+@pytest.mark.parametrize("mode", ["mixed", "f3", "3xtf32", "bogus"])
+def test_fp32_gemm_modes(mode, monkeypatch):
+    """XKNN_FP32_GEMM selects the FP32 path's GEMM arithmetic; every mode meets the fp32 bar on
+    a small step (the full parity suite runs on the default), an unknown one is a ConfigError."""
+    import paper_2102_06025_b200 as X
+
+    monkeypatch.setenv("XKNN_FP32_GEMM", mode)
+    if mode == "bogus":
+        with pytest.raises(X.ConfigError):
+            X.KnnSoftmaxLayer(1000, 512, m_active=100, max_batch=8, precision=X.PREC_FP32)
+        return
+    out, wg, w_or, vg, v_or, w0 = _run(20_000, 512, 256, 10, 2_000, X.PREC_FP32, steps=2)
+    e = _errors(out, wg, w_or, vg, v_or, w0)
+    assert max(e.values()) <= 1e-5, e
