@@ -498,6 +498,17 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
         mw_max = int(tg.item())
     else:
         mw_max = active_local
+    # every rank's clocks and its own GEMM-F / softmax-statistics phases: at N > 1 the step is the
+    # slowest rank's, and the others wait for it at the softmax all-reduce (softmax_stats)
+    per_rank = None
+    if world > 1:
+        cs = clk.summary()
+        mine = {"rank": rank, "sm_mhz": cs.get("sm_mhz"), "reasons": cs.get("reasons"),
+                "active_rows": int(active_local),
+                "gemm_logits_softmax_ms": round(phase_ms.get("gemm_logits_softmax", 0.0), 4),
+                "softmax_stats_ms": round(phase_ms.get("softmax_stats", 0.0), 4)}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
 
     res = None
     if rank == 0:
@@ -583,6 +594,7 @@ def run_ours(args, wl_name, wl, rank, world, local_rank, dist, precision=None):
                                      "max(sum over the 3 GEMMs of 2*B*M_w*D/its peak, "
                                      "16*M_w*D/HBM peak)"},
             "phase_ms": {k_: round(v, 4) for k_, v in phase_ms.items()},
+            **({"per_rank": per_rank} if per_rank else {}),
             "phase_profile": {"ms_per_step": round(ms_prof / args.steps, 4), "steps": args.steps,
                               "how": "second pass of the same steps with CUDA events at the "
                                      "step's phase boundaries (last step's graph replay)"},
